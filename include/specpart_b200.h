@@ -1,0 +1,234 @@
+/*
+ * specpart_b200.h — C ABI of the B200-native spectral partitioning hot path.
+ *
+ * Drop-in boundary for the reference API
+ *     RunResult specpart::partition_graph(const Graph&, const RunConfig&)
+ *     (/root/reference/proj/include/specpart/pipeline.hpp:106, src/pipeline.cpp:47-167)
+ * plus kernel-level entry points that mirror the reference's internal seams so
+ * parity can be checked stage by stage:
+ *     build_combinatorial / build_normalized / build_degree  (src/laplacian.cpp:53-144)
+ *     kernels::spmv_block                                    (src/kernels.cpp:36-62)
+ *     kernels::gram                                          (src/kernels.cpp:79-110)
+ *     lobpcg                                                 (src/eigensolver.cpp:177-337)
+ *     polynomial_build + GmresPolyPreconditioner::apply      (src/preconditioners.cpp:171-193, 315-382)
+ *     mj_partition                                           (src/partitioner.cpp:140-170)
+ *     make_partition / cutsize / imbalance                   (src/graph.cpp:184-230)
+ *
+ * Conventions: plain C types only. All array arguments are HOST pointers owned
+ * by the caller and read (inputs) or written (outputs) during the call only.
+ * Dense blocks cross the boundary column-major (the reference's Dense layout,
+ * dense.hpp:10-39); the library keeps them row-major on the device.
+ * Every entry point is blocking and returns an sp_status; the message of the
+ * last failure on a context is available from sp_last_error().
+ */
+#ifndef SPECPART_B200_H
+#define SPECPART_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: the reference's exception types (include/specpart/errors.hpp) --- */
+typedef int32_t sp_status;
+enum {
+    SP_OK = 0,
+    SP_ERROR = 1,        /* any other std::exception (CLI exit 1, tools/specpart.cpp:347) */
+    SP_PARSE = 2,        /* ParseError            errors.hpp:10-19  (not produced by this path) */
+    SP_BREAKDOWN = 3,    /* BreakdownError        errors.hpp:23-36 */
+    SP_INFEASIBLE = 4,   /* InfeasibleError       errors.hpp:39-42 */
+    SP_DEGENERATE = 5,   /* DegenerateDegreeError errors.hpp:45-48 */
+    SP_DIMENSION = 6,    /* DimensionError        errors.hpp:51-54 */
+    SP_INVALID = 7,      /* std::invalid_argument (graph.cpp:210-224, laplacian.cpp:54) */
+    SP_CUDA = 8,         /* CUDA runtime failure (new) */
+    SP_NCCL = 9          /* NCCL failure (new) */
+};
+
+/* ---- enums: numeric values follow the reference's enum order (pipeline.hpp:16-18,
+ *      laplacian.hpp:40) so a C++ shim can static_cast between them. ---- */
+enum { SP_PROBLEM_AUTO = 0, SP_PROBLEM_COMBINATORIAL = 1, SP_PROBLEM_GENERALIZED = 2,
+       SP_PROBLEM_NORMALIZED = 3 };
+enum { SP_PRECOND_AUTO = 0, SP_PRECOND_JACOBI = 1, SP_PRECOND_POLYNOMIAL = 2,
+       SP_PRECOND_AMG = 3, SP_PRECOND_NONE = 4 };
+enum { SP_INIT_AUTO = 0, SP_INIT_RANDOM = 1, SP_INIT_PIECEWISE = 2 };
+/* operator kinds for sp_build_laplacian / sp_spmm (laplacian.hpp:24-33) */
+enum { SP_LAP_COMBINATORIAL = 0, SP_LAP_NORMALIZED = 1, SP_LAP_DEGREE = 2 };
+
+/* report warnings bitmask (pipeline.cpp:140-148, 161-163) */
+enum { SP_WARN_BREAKDOWN_RECOVERED = 1, SP_WARN_UNCONVERGED = 2, SP_WARN_IMBALANCE = 4 };
+
+#define SP_MAX_EIG 64
+
+/* Graph (graph.hpp:17-32): symmetric CSR adjacency without stored self-loops,
+ * column indices strictly increasing per row. values == NULL means unit edge
+ * costs, vertex_weights == NULL means unit vertex weights (the CLI's
+ * symmetrize() output, graph.cpp:44-64). */
+typedef struct sp_graph {
+    int64_t n;
+    const int64_t* row_offsets;   /* n+1 */
+    const int32_t* col_indices;   /* row_offsets[n] */
+    const double* values;         /* row_offsets[n] or NULL */
+    const double* vertex_weights; /* n or NULL */
+} sp_graph;
+
+/* RunConfig (pipeline.hpp:20-31). tol <= 0 means "pick by graph kind" (nullopt). */
+typedef struct sp_config {
+    int64_t num_parts;
+    int32_t problem;      /* SP_PROBLEM_* */
+    int32_t precond;      /* SP_PRECOND_* */
+    double tol;
+    int32_t max_iters;
+    int32_t init;         /* SP_INIT_* */
+    uint64_t seed;
+    double epsilon;
+    int32_t doubled_cut;
+    int32_t record_trace;
+} sp_config;
+
+/* TraceRecord (eigensolver.hpp:21-26) */
+typedef struct sp_trace_record {
+    int32_t iter;
+    int32_t ntheta;
+    double min_residual;
+    double max_residual;
+    double theta[SP_MAX_EIG];
+} sp_trace_record;
+
+/* RunReport (pipeline.hpp:53-86) with fixed-size arrays; caller-provided
+ * buffers for the variable-length parts. */
+typedef struct sp_report {
+    /* graph */
+    int64_t n;
+    int64_t edges;
+    int32_t graph_regular;     /* 1 = Regularity::Regular */
+    int32_t pad0;
+    int64_t max_degree;
+    double avg_degree;
+    double degree_ratio;
+    /* resolved configuration (ResolvedConfig, pipeline.hpp:33-39) */
+    int64_t num_parts;
+    int32_t problem;           /* SP_PROBLEM_* (never AUTO) */
+    int32_t precond;           /* SP_PRECOND_* (never AUTO) */
+    double tol;
+    int32_t init;              /* SP_INIT_* (never AUTO) */
+    int32_t eigenvectors;      /* d */
+    uint64_t seed;
+    int32_t max_iters;
+    int32_t doubled_cut;
+    double epsilon;
+    /* solver */
+    int32_t iterations;
+    int32_t breakdown_retries;
+    double theta[SP_MAX_EIG];
+    double residual_norms[SP_MAX_EIG];
+    uint8_t converged[SP_MAX_EIG];
+    int32_t poly_degree;       /* achieved GMRES-polynomial degree, 0 if not used */
+    int32_t warnings;          /* SP_WARN_* bitmask */
+    /* StageTimes (pipeline.hpp:41-46), seconds, same boundary as the reference */
+    double laplacian_s;
+    double eigensolve_s;
+    double partition_s;
+    double total_s;
+    /* partition quality */
+    double cutsize;
+    double imbalance;
+    /* device-side accounting (new): SpMM launches, algorithmic bytes, device ms */
+    int64_t spmm_launches;
+    double spmm_bytes;
+    double spmm_ms;
+    int32_t kernel_launches;
+    int32_t n_gpus;
+    /* caller-provided outputs (may be NULL) */
+    double* part_weights;          /* num_parts */
+    sp_trace_record* trace;        /* trace_capacity records */
+    int32_t trace_capacity;
+    int32_t trace_len;
+} sp_report;
+
+typedef struct sp_context sp_context;
+
+/* ---- context ------------------------------------------------------------- */
+/* One context per GPU. Owns device memory, streams and (for world > 1) the NCCL
+ * communicator. One call in flight per context. */
+sp_status sp_context_create(int device, sp_context** out);
+/* Multi-GPU: one process per GPU, all ranks call this with the same 128-byte
+ * unique id produced by sp_nccl_unique_id() on rank 0. */
+sp_status sp_nccl_unique_id(void* out128);
+sp_status sp_context_create_dist(int device, int rank, int world, const void* nccl_id128,
+                                 sp_context** out);
+void sp_context_destroy(sp_context* ctx);
+const char* sp_last_error(const sp_context* ctx);
+int sp_version(void);
+/* Record CUDA events around every SpMM launch (report.spmm_ms); off by default. */
+sp_status sp_context_set_timing(sp_context* ctx, int on);
+
+/* ---- end to end (pipeline.cpp:47-167) --------------------------------------
+ * assignment_out: n int32 part ids in [0, K). x0_colmajor: optional n x d
+ * initial block replacing the init selection (the CLI's --init-file warm
+ * start, tools/specpart.cpp:94-157); pass NULL for the reference behaviour.
+ * With world > 1 every rank passes the same full graph; every rank receives
+ * the full assignment. */
+sp_status sp_partition(sp_context* ctx, const sp_graph* g, const sp_config* cfg,
+                       int32_t* assignment_out, sp_report* report, const double* x0_colmajor);
+
+/* ---- kernel-level entry points (parity seams) ------------------------------ */
+
+/* Laplacian assembly (laplacian.cpp:53-144): writes the CSR of L (offsets n+1,
+ * cols/vals nnz_L = nnz_A + n; for SP_LAP_DEGREE nnz = n), diag[n] and the
+ * Gershgorin bound (min(bound, 2) for normalized). Bit-exact. */
+sp_status sp_build_laplacian(sp_context* ctx, int32_t kind, const sp_graph* g,
+                             int64_t* offsets_out, int32_t* cols_out, double* vals_out,
+                             double* diag_out, double* bound_out, int32_t* is_diagonal_out);
+
+/* Y = L * X with L assembled from g (kind as above). X, Y are n x m column-major. */
+sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* g, const double* X, int32_t m,
+                  double* Y);
+
+/* Y = A * X for an explicit CSR operator (spmv_block, kernels.cpp:36-62). */
+sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64_t* offsets,
+                      const int32_t* cols, const double* vals, const double* X, int32_t m,
+                      double* Y);
+
+/* G = U^T diag(b) V (kernels::gram, kernels.cpp:79-110; b == NULL means identity).
+ * U: n x mu, V: n x mv column-major; G: mu x mv column-major. Deterministic. */
+sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const double* V,
+                  int32_t mv, const double* b, double* G);
+
+/* Initial blocks (eigensolver.cpp:20-51), n x d column-major, bit-identical. */
+sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed,
+                           double* X_out);
+
+/* LOBPCG (eigensolver.cpp:177-337) on the problem built from g. precond is
+ * SP_PRECOND_JACOBI, SP_PRECOND_POLYNOMIAL (poly_seed feeds PolyConfig.seed) or
+ * SP_PRECOND_NONE. X0 n x nev column-major. Outputs theta[nev], X n x nev,
+ * residual norms, converged flags, iteration count, retries. */
+sp_status sp_lobpcg(sp_context* ctx, const sp_graph* g, int32_t problem, int32_t precond,
+                    uint64_t poly_seed, int32_t poly_degree, const double* X0, int32_t nev,
+                    double tol, int32_t max_iters, int32_t locking, double* theta_out,
+                    double* X_out, double* residuals_out, uint8_t* converged_out,
+                    int32_t* iterations_out, int32_t* retries_out);
+
+/* GMRES polynomial preconditioner (preconditioners.cpp:315-382) built on the
+ * operator of kind `kind` from g, then applied to R (n x m column-major). Also
+ * returns the Leja-ordered roots (capacity degree). */
+sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* g, uint64_t seed,
+                        int32_t degree, const double* R, int32_t m, double* H_out,
+                        double* roots_out, int32_t* achieved_out);
+
+/* Multi-jagged partitioning (partitioner.cpp:140-170) of n points with `dims`
+ * coordinates (n x dims column-major), positive weights (NULL = unit). */
+sp_status sp_mj_partition(sp_context* ctx, int64_t n, int32_t dims, const double* coords,
+                          const double* weights, int64_t num_parts, int32_t* assignment_out,
+                          double* part_weights_out, double* imbalance_out);
+
+/* make_partition (graph.cpp:209-230): validates, tallies part weights, cut, imbalance. */
+sp_status sp_cut_imbalance(sp_context* ctx, const sp_graph* g, const int32_t* assignment,
+                           int64_t num_parts, int32_t doubled, double* cut_out,
+                           double* imbalance_out, double* part_weights_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECPART_B200_H */

@@ -1,0 +1,414 @@
+"""Host-side mirror of the reference's C++ API (include/specpart/*.hpp) over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference:
+    partition_graph(Graph, RunConfig) -> RunResult       pipeline.hpp:106
+    build_combinatorial / build_normalized / build_degree laplacian.hpp:24-33
+    kernels.spmv_block / kernels.gram                    kernels.hpp:16-24
+    initial_guess_random / initial_guess_piecewise       eigensolver.hpp:44-50
+    lobpcg                                               eigensolver.hpp:61-64
+    polynomial_build(...).apply                          preconditioners.hpp:45-46
+    mj_partition                                         partitioner.hpp:39-42
+    make_partition / cutsize / imbalance                 graph.hpp:63-75
+Every call runs the CUDA library (libspecpart_b200.so); a missing library raises
+ImportError — there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi
+
+
+# ---- data types -------------------------------------------------------------
+@dataclass
+class Graph:
+    """Graph (graph.hpp:17-32): symmetric CSR adjacency, no self-loops.
+
+    values=None means unit edge costs (SparseMatrix without values,
+    sparse.hpp:29); vertex_weights=None means unit weights."""
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray | None = None
+    vertex_weights: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.row_offsets = np.ascontiguousarray(self.row_offsets, dtype=np.int64)
+        self.col_indices = np.ascontiguousarray(self.col_indices, dtype=np.int32)
+        if self.values is not None:
+            self.values = np.ascontiguousarray(self.values, dtype=np.float64)
+        if self.vertex_weights is not None:
+            self.vertex_weights = np.ascontiguousarray(self.vertex_weights, dtype=np.float64)
+
+    @property
+    def n(self) -> int:
+        return int(self.row_offsets.shape[0] - 1)
+
+    def edge_count(self) -> int:
+        return int(self.row_offsets[-1]) // 2
+
+    def as_c(self) -> abi.SpGraph:
+        g = abi.SpGraph()
+        g.n = self.n
+        g.row_offsets = self.row_offsets.ctypes.data
+        g.col_indices = self.col_indices.ctypes.data
+        g.values = self.values.ctypes.data if self.values is not None else None
+        g.vertex_weights = self.vertex_weights.ctypes.data if self.vertex_weights is not None else None
+        return g
+
+
+@dataclass
+class RunConfig:
+    """RunConfig (pipeline.hpp:20-31). tol=None picks by graph kind."""
+    num_parts: int = 2
+    problem: str = "auto"
+    precond: str = "auto"
+    tol: float | None = None
+    max_iters: int = 1000
+    seed: int = 42
+    epsilon: float = 0.01
+    doubled_cut: bool = False
+    init: str = "auto"
+    record_trace: bool = False
+
+    def as_c(self) -> abi.SpConfig:
+        c = abi.SpConfig()
+        c.num_parts = int(self.num_parts)
+        c.problem = abi.PROBLEM[self.problem]
+        c.precond = abi.PRECOND[self.precond]
+        c.tol = float(self.tol) if self.tol is not None else -1.0
+        c.max_iters = int(self.max_iters)
+        c.init = abi.INIT[self.init]
+        c.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        c.epsilon = float(self.epsilon)
+        c.doubled_cut = int(bool(self.doubled_cut))
+        c.record_trace = int(bool(self.record_trace))
+        return c
+
+
+@dataclass
+class Partition:
+    assignment: np.ndarray
+    num_parts: int
+    part_weights: np.ndarray
+    cutsize: float = 0.0
+    imbalance: float = 0.0
+
+
+@dataclass
+class TraceRecord:
+    iter: int
+    min_residual: float
+    max_residual: float
+    theta: list
+
+
+@dataclass
+class RunReport:
+    n: int = 0
+    edges: int = 0
+    regular: bool = True
+    max_degree: int = 0
+    avg_degree: float = 0.0
+    degree_ratio: float = 0.0
+    num_parts: int = 0
+    problem: str = ""
+    precond: str = ""
+    tol: float = 0.0
+    init: str = ""
+    eigenvectors: int = 0
+    seed: int = 0
+    max_iters: int = 0
+    epsilon: float = 0.0
+    doubled_cut: bool = False
+    iterations: int = 0
+    breakdown_retries: int = 0
+    theta: list = field(default_factory=list)
+    residual_norms: list = field(default_factory=list)
+    converged: list = field(default_factory=list)
+    poly_degree: int = 0
+    warnings: list = field(default_factory=list)
+    times: dict = field(default_factory=dict)
+    cutsize: float = 0.0
+    imbalance: float = 0.0
+    part_weights: list = field(default_factory=list)
+    trace: list = field(default_factory=list)
+    device: dict = field(default_factory=dict)
+
+
+@dataclass
+class RunResult:
+    partition: Partition
+    report: RunReport
+
+
+@dataclass
+class EigenResult:
+    theta: np.ndarray
+    X: np.ndarray
+    iterations: int
+    residual_norms: np.ndarray
+    converged: np.ndarray
+    breakdown_retries: int
+
+    def all_converged(self) -> bool:
+        return bool(len(self.converged)) and bool(np.all(self.converged))
+
+
+_NAMES_PROBLEM = {v: k for k, v in abi.PROBLEM.items()}
+_NAMES_PRECOND = {v: k for k, v in abi.PRECOND.items()}
+_NAMES_INIT = {v: k for k, v in abi.INIT.items()}
+
+
+def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> RunReport:
+    d = r.eigenvectors
+    warnings = []
+    if r.warnings & abi.WARN_BREAKDOWN_RECOVERED:
+        warnings.append("eigensolver recovered from a basis breakdown by clearing the search directions")
+    if r.warnings & abi.WARN_UNCONVERGED:
+        warnings.append("eigensolver reached max_iters with unconverged columns; "
+                        "partitioning on partially converged eigenvectors")
+    if r.warnings & abi.WARN_IMBALANCE:
+        warnings.append(f"imbalance {r.imbalance:.6f} exceeds 1+epsilon = {1.0 + r.epsilon:.6f}")
+    trace = []
+    if trace_buf is not None:
+        for k in range(r.trace_len):
+            t = trace_buf[k]
+            trace.append(TraceRecord(t.iter, t.min_residual, t.max_residual, list(t.theta[: t.ntheta])))
+    return RunReport(
+        n=r.n, edges=r.edges, regular=bool(r.graph_regular), max_degree=r.max_degree,
+        avg_degree=r.avg_degree, degree_ratio=r.degree_ratio, num_parts=r.num_parts,
+        problem=_NAMES_PROBLEM.get(r.problem, "?"), precond=_NAMES_PRECOND.get(r.precond, "?"),
+        tol=r.tol, init=_NAMES_INIT.get(r.init, "?"), eigenvectors=d, seed=r.seed,
+        max_iters=r.max_iters, epsilon=r.epsilon, doubled_cut=bool(r.doubled_cut),
+        iterations=r.iterations, breakdown_retries=r.breakdown_retries,
+        theta=list(r.theta[:d]), residual_norms=list(r.residual_norms[:d]),
+        converged=[bool(x) for x in r.converged[:d]], poly_degree=r.poly_degree, warnings=warnings,
+        times={"laplacian_s": r.laplacian_s, "eigensolve_s": r.eigensolve_s,
+               "partition_s": r.partition_s, "total_s": r.total_s},
+        cutsize=r.cutsize, imbalance=r.imbalance, part_weights=list(part_weights), trace=trace,
+        device={"spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
+                "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus})
+
+
+def _ptr(a):
+    return a.ctypes.data if a is not None else None
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _colmajor(X):
+    """(n, m) array -> column-major contiguous buffer (the reference Dense layout)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X[:, None]
+    return np.asfortranarray(X)
+
+
+# ---- context ------------------------------------------------------------------
+class Context:
+    """One B200 (one rank). world > 1 needs the same nccl_id on every rank."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self.lib = abi.load_library()
+        self._h = C.c_void_p()
+        if world > 1:
+            buf = C.create_string_buffer(nccl_id, 128)
+            st = self.lib.sp_context_create_dist(device, rank, world, buf, C.byref(self._h))
+        else:
+            st = self.lib.sp_context_create(device, C.byref(self._h))
+        if st != abi.SP_OK:
+            abi.raise_for(st, f"sp_context_create failed ({st}) on device {device}")
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = abi.load_library()
+        buf = C.create_string_buffer(128)
+        abi.raise_for(lib.sp_nccl_unique_id(buf), "ncclGetUniqueId failed")
+        return buf.raw
+
+    def close(self):
+        if self._h:
+            self.lib.sp_context_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != abi.SP_OK:
+            abi.raise_for(st, self.lib.sp_last_error(self._h).decode(errors="replace"))
+
+    def set_timing(self, on: bool):
+        self._check(self.lib.sp_context_set_timing(self._h, int(on)))
+
+    # pipeline.cpp:47-167
+    def partition_graph(self, g: Graph, cfg: RunConfig, x0=None) -> RunResult:
+        n = g.n
+        assignment = np.empty(n, dtype=np.int32)
+        pw = np.zeros(max(int(cfg.num_parts), 1), dtype=np.float64)
+        rep = abi.SpReport()
+        rep.part_weights = pw.ctypes.data_as(C.POINTER(C.c_double))
+        trace_buf = None
+        if cfg.record_trace:
+            cap = int(cfg.max_iters) + 1
+            trace_buf = (abi.SpTraceRecord * cap)()
+            rep.trace = C.cast(trace_buf, C.POINTER(abi.SpTraceRecord))
+            rep.trace_capacity = cap
+        x0b = _colmajor(x0) if x0 is not None else None
+        gc, cc = g.as_c(), cfg.as_c()
+        self._check(self.lib.sp_partition(self._h, C.byref(gc), C.byref(cc), assignment.ctypes.data,
+                                          C.byref(rep), _ptr(x0b)))
+        report = report_from_c(rep, pw, trace_buf)
+        part = Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance)
+        return RunResult(part, report)
+
+    # laplacian.cpp:53-144 (explicit CSR, bit-exact)
+    def build_laplacian(self, kind: str, g: Graph):
+        k = abi.LAP[kind]
+        n, nnz = g.n, int(g.row_offsets[-1])
+        nnz_l = n if k == 2 else nnz + n
+        offs = np.empty(n + 1, dtype=np.int64)
+        cols = np.empty(max(nnz_l, 1), dtype=np.int32)
+        vals = np.empty(max(nnz_l, 1), dtype=np.float64)
+        diag = np.empty(max(n, 1), dtype=np.float64)
+        bound, isdiag = C.c_double(), C.c_int32()
+        gc = g.as_c()
+        self._check(self.lib.sp_build_laplacian(self._h, k, C.byref(gc), offs.ctypes.data, cols.ctypes.data,
+                                                vals.ctypes.data, diag.ctypes.data, C.byref(bound),
+                                                C.byref(isdiag)))
+        return dict(row_offsets=offs, col_indices=cols[:nnz_l], values=vals[:nnz_l], diag=diag[:n],
+                    spectral_bound=bound.value, is_diagonal=bool(isdiag.value))
+
+    def spmm(self, kind: str, g: Graph, X) -> np.ndarray:
+        Xc = _colmajor(X)
+        n, m = Xc.shape
+        Y = np.empty((n, m), dtype=np.float64, order="F")
+        gc = g.as_c()
+        self._check(self.lib.sp_spmm(self._h, abi.LAP[kind], C.byref(gc), Xc.ctypes.data, m, Y.ctypes.data))
+        return Y
+
+    def spmm_csr(self, row_offsets, col_indices, values, X, ncols=None) -> np.ndarray:
+        offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(col_indices, dtype=np.int32)
+        vals = _f64(values) if values is not None else None
+        Xc = _colmajor(X)
+        nrows = offs.shape[0] - 1
+        ncols = Xc.shape[0] if ncols is None else ncols
+        m = Xc.shape[1]
+        Y = np.empty((nrows, m), dtype=np.float64, order="F")
+        self._check(self.lib.sp_spmm_csr(self._h, nrows, ncols, offs.ctypes.data, cols.ctypes.data,
+                                         _ptr(vals), Xc.ctypes.data, m, Y.ctypes.data))
+        return Y
+
+    def gram(self, U, V, b=None) -> np.ndarray:
+        Uc, Vc = _colmajor(U), _colmajor(V)
+        bb = _f64(b) if b is not None else None
+        G = np.empty((Uc.shape[1], Vc.shape[1]), dtype=np.float64, order="F")
+        self._check(self.lib.sp_gram(self._h, Uc.shape[0], Uc.ctypes.data, Uc.shape[1], Vc.ctypes.data,
+                                     Vc.shape[1], _ptr(bb), G.ctypes.data))
+        return G
+
+    def initial_guess(self, init: str, n: int, d: int, seed: int = 0) -> np.ndarray:
+        X = np.empty((n, d), dtype=np.float64, order="F")
+        self._check(self.lib.sp_initial_guess(self._h, abi.INIT[init], n, d, seed, X.ctypes.data))
+        return X
+
+    def lobpcg(self, g: Graph, problem: str, precond: str, X0, tol: float, max_iters: int = 1000,
+               locking: bool = True, poly_seed: int = 0, poly_degree: int = 25) -> EigenResult:
+        X0c = _colmajor(X0)
+        n, nev = X0c.shape
+        theta = np.empty(nev)
+        X = np.empty((n, nev), dtype=np.float64, order="F")
+        res = np.empty(nev)
+        conv = np.empty(nev, dtype=np.uint8)
+        it, rt = C.c_int32(), C.c_int32()
+        gc = g.as_c()
+        self._check(self.lib.sp_lobpcg(self._h, C.byref(gc), abi.PROBLEM[problem], abi.PRECOND[precond],
+                                       poly_seed, poly_degree, X0c.ctypes.data, nev, tol, max_iters,
+                                       int(locking), theta.ctypes.data, X.ctypes.data, res.ctypes.data,
+                                       conv.ctypes.data, C.byref(it), C.byref(rt)))
+        return EigenResult(theta, X, it.value, res, conv.astype(bool), rt.value)
+
+    def poly_apply(self, kind: str, g: Graph, seed: int, degree: int, R):
+        Rc = _colmajor(R)
+        n, m = Rc.shape
+        H = np.empty((n, m), dtype=np.float64, order="F")
+        roots = np.empty(max(degree, 1))
+        ach = C.c_int32()
+        gc = g.as_c()
+        self._check(self.lib.sp_poly_apply(self._h, abi.LAP[kind], C.byref(gc), seed, degree, Rc.ctypes.data,
+                                           m, H.ctypes.data, roots.ctypes.data, C.byref(ach)))
+        return H, roots[: ach.value]
+
+    def mj_partition(self, coords, weights, num_parts: int) -> Partition:
+        Cc = _colmajor(coords)
+        n, dims = Cc.shape
+        w = _f64(weights) if weights is not None else None
+        a = np.empty(n, dtype=np.int32)
+        pw = np.empty(num_parts)
+        imb = C.c_double()
+        self._check(self.lib.sp_mj_partition(self._h, n, dims, Cc.ctypes.data, _ptr(w), num_parts,
+                                             a.ctypes.data, pw.ctypes.data, C.byref(imb)))
+        return Partition(a, num_parts, pw, 0.0, imb.value)
+
+    def make_partition(self, g: Graph, assignment, num_parts: int, doubled_cut: bool = False) -> Partition:
+        a = np.ascontiguousarray(assignment, dtype=np.int32)
+        if a.shape[0] != g.n:
+            raise abi.InvalidArgument("make_partition: assignment length mismatch")
+        pw = np.empty(num_parts)
+        cut, imb = C.c_double(), C.c_double()
+        gc = g.as_c()
+        self._check(self.lib.sp_cut_imbalance(self._h, C.byref(gc), a.ctypes.data, num_parts,
+                                              int(doubled_cut), C.byref(cut), C.byref(imb), pw.ctypes.data))
+        return Partition(a, num_parts, pw, cut.value, imb.value)
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def partition_graph(g: Graph, cfg: RunConfig, device: int = 0, x0=None) -> RunResult:
+    return default_context(device).partition_graph(g, cfg, x0)
+
+
+# Reference-side pure helpers (no device work)
+def eigenvector_count(num_parts: int) -> int:
+    """partitioner.cpp:13-17: floor(log2 K) + 1."""
+    if num_parts < 2:
+        raise abi.InfeasibleError("eigenvector_count: K must be >= 2")
+    return int(num_parts).bit_length()
+
+
+def select_defaults(regular: bool, precond: str):
+    """pipeline.cpp:20-37."""
+    table = {
+        ("jacobi", True): ("combinatorial", 1e-3), ("jacobi", False): ("generalized", 1e-2),
+        ("none", True): ("combinatorial", 1e-3), ("none", False): ("generalized", 1e-2),
+        ("polynomial", True): ("combinatorial", 1e-3), ("polynomial", False): ("normalized", 1e-2),
+        ("amg", True): ("combinatorial", 1e-2), ("amg", False): ("generalized", 1e-2),
+    }
+    if (precond, regular) not in table:
+        raise abi.InvalidArgument("select_defaults: preconditioner must be resolved")
+    return table[(precond, regular)]
+
+
+def select_precond_auto(regular: bool) -> str:
+    return "amg" if regular else "polynomial"
+
+
+def select_initial_vectors(regular: bool) -> str:
+    return "random" if regular else "piecewise"

@@ -1,0 +1,684 @@
+// abi.cu — extern "C" entry points (include/specpart_b200.h) and the
+// partition_graph pipeline (src/pipeline.cpp:47-167) on the device.
+#include "specpart_b200.h"
+
+#include "context.hpp"
+#include "metrics.hpp"
+#include "mj.hpp"
+#include "solver.hpp"
+
+#include <algorithm>
+#include <bit>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+
+namespace spb {
+
+int device_sm_count() {
+    static int sms = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+        return v > 0 ? v : 148;
+    }();
+    return sms;
+}
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+__global__ void rebase_kernel(int64_t n1, int64_t* offs, int64_t base) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n1;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        offs[i] -= base;
+}
+
+template <class T> void h2d(T* dst, const T* src, size_t count, cudaStream_t s) {
+    if (count) SPB_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+}
+
+// Uploads the local row block of the caller's host graph.
+void upload_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
+    if (!hg || hg->n < 0 || (hg->n > 0 && (!hg->row_offsets || !hg->col_indices)))
+        throw_invalid("graph: null arrays");
+    Comm& cm = ctx->comm;
+    cudaStream_t s = ctx->stream;
+    g.n_global = hg->n;
+    g.nnz_global = hg->n > 0 ? hg->row_offsets[hg->n] : 0;
+    cm.setup(hg->n);
+    g.row0 = cm.active() ? cm.row0() : 0;
+    g.n_local = cm.active() ? cm.nloc() : hg->n;
+    const int64_t k0 = hg->n > 0 ? hg->row_offsets[g.row0] : 0;
+    const int64_t k1 = hg->n > 0 ? hg->row_offsets[g.row0 + g.n_local] : 0;
+    g.nnz_local = k1 - k0;
+    g.offs.alloc(g.n_local + 1);
+    g.cols.alloc(std::max<int64_t>(g.nnz_local, 1));
+    if (hg->n > 0) {
+        h2d(g.offs.p, hg->row_offsets + g.row0, g.n_local + 1, s);
+        if (k0 != 0) {
+            rebase_kernel<<<grid_for(g.n_local + 1, 256, 4), 256, 0, s>>>(g.n_local + 1, g.offs.p, k0);
+            SPB_LAUNCH_CHECK();
+        }
+        h2d(g.cols.p, hg->col_indices + k0, g.nnz_local, s);
+    }
+    if (hg->values) {
+        g.vals.alloc(std::max<int64_t>(g.nnz_local, 1));
+        h2d(g.vals.p, hg->values + k0, g.nnz_local, s);
+    } else {
+        g.vals.release();
+    }
+    g.unit_weights = true;
+    if (hg->vertex_weights) {
+        bool unit = true;
+        for (int64_t i = 0; i < hg->n && unit; ++i) unit = hg->vertex_weights[i] == 1.0;
+        g.unit_weights = unit;
+        if (!unit) {
+            g.vw.alloc(std::max<int64_t>(g.n_local, 1));
+            h2d(g.vw.p, hg->vertex_weights + g.row0, g.n_local, s);
+        }
+    }
+    graph_degrees(g, s);
+    g.max_degree_global = g.max_degree_local;
+    if (cm.active()) {
+        DBuf<int64_t> t(cm.world), one(1);
+        int64_t v = g.max_degree_local;
+        h2d(one.p, &v, 1, s);
+        SPB_NCCL(ncclAllGather(one.p, t.p, 1, ncclInt64, cm.nccl, s));
+        std::vector<int64_t> h(cm.world);
+        SPB_CUDA(cudaMemcpyAsync(h.data(), t.p, sizeof(int64_t) * cm.world, cudaMemcpyDeviceToHost, s));
+        int64_t unit_flag = g.unit_values ? 0 : 1;
+        h2d(one.p, &unit_flag, 1, s);
+        cm.sum_i64(one.p, 1, s);
+        SPB_CUDA(cudaMemcpyAsync(&unit_flag, one.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        g.max_degree_global = *std::max_element(h.begin(), h.end());
+        g.unit_values = unit_flag == 0;
+        // all-vertex degrees (isd of halo columns for L_N)
+        DBuf<double> padded(cm.n_pad);
+        SPB_CUDA(cudaMemsetAsync(padded.p, 0, sizeof(double) * cm.n_pad, s));
+        SPB_CUDA(cudaMemcpyAsync(padded.p, g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToDevice, s));
+        g.deg_all.alloc(static_cast<size_t>(cm.n_pad) * cm.world);
+        cm.gather_f64(padded.p, g.deg_all.p, s);
+    }
+}
+
+struct GraphKindInfo {
+    bool regular = true;
+    int64_t max_degree = 0;
+    double avg = 0.0, ratio = 0.0;
+};
+
+// classify (graph.cpp:173-182)
+GraphKindInfo classify(const DevGraph& g) {
+    if (g.n_global == 0) throw_invalid("classify: empty graph");
+    GraphKindInfo k;
+    k.max_degree = g.max_degree_global;
+    k.avg = static_cast<double>(g.nnz_global) / static_cast<double>(g.n_global);
+    k.ratio = k.avg > 0.0 ? static_cast<double>(k.max_degree) / k.avg
+                          : (k.max_degree > 0 ? std::numeric_limits<double>::infinity() : 0.0);
+    k.regular = k.ratio <= 10.0;
+    return k;
+}
+
+int eigenvector_count(int64_t K) {
+    if (K < 2) throw_infeasible("eigenvector_count: K must be >= 2");
+    return static_cast<int>(std::bit_width(static_cast<uint64_t>(K)));  // floor(log2 K) + 1
+}
+
+// select_defaults (pipeline.cpp:20-37): returns (problem, tol)
+std::pair<int, double> select_defaults(bool regular, int precond) {
+    switch (precond) {
+    case SP_PRECOND_JACOBI:
+    case SP_PRECOND_NONE:
+        return regular ? std::pair{SP_PROBLEM_COMBINATORIAL, 1e-3} : std::pair{SP_PROBLEM_GENERALIZED, 1e-2};
+    case SP_PRECOND_POLYNOMIAL:
+        return regular ? std::pair{SP_PROBLEM_COMBINATORIAL, 1e-3} : std::pair{SP_PROBLEM_NORMALIZED, 1e-2};
+    case SP_PRECOND_AMG:
+        return regular ? std::pair{SP_PROBLEM_COMBINATORIAL, 1e-2} : std::pair{SP_PROBLEM_GENERALIZED, 1e-2};
+    }
+    throw_invalid("select_defaults: preconditioner must be resolved");
+    return {};
+}
+
+// problem kind -> Laplacian kind of problem.A
+int operator_kind(int problem) { return problem == SP_PROBLEM_NORMALIZED ? 1 : 0; }
+
+sp_status map_exception(sp_context* ctx) {
+    try {
+        throw;
+    } catch (const BreakdownErr& e) {
+        if (ctx) ctx->err = e.what();
+        return SP_BREAKDOWN;
+    } catch (const SpError& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return SP_ERROR;
+    }
+}
+
+template <class F> sp_status guarded(sp_context* ctx, F&& f) {
+    if (!ctx) return SP_INVALID;
+    try {
+        SPB_CUDA(cudaSetDevice(ctx->device));
+        f();
+        return SP_OK;
+    } catch (...) {
+        return map_exception(ctx);
+    }
+}
+
+// row-major device block <-> column-major host array (local rows)
+void upload_block(const double* host_colmajor, int64_t n_glob, int64_t row0, int64_t nloc, int m,
+                  const View& dst, cudaStream_t s) {
+    DBuf<double> tmp(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * m);
+    for (int c = 0; c < m; ++c)
+        h2d(tmp.p + static_cast<size_t>(c) * nloc, host_colmajor + static_cast<size_t>(c) * n_glob + row0, nloc, s);
+    copy_view(nloc, colmajor(tmp.p, nloc, m), dst, s);
+    SPB_CUDA(cudaStreamSynchronize(s));
+}
+
+void download_block(const View& src, int64_t nloc, int m, double* host_colmajor, cudaStream_t s) {
+    DBuf<double> tmp(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * m);
+    copy_view(nloc, src, colmajor(tmp.p, nloc, m), s);
+    if (nloc * m) SPB_CUDA(cudaMemcpyAsync(host_colmajor, tmp.p, sizeof(double) * nloc * m, cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+}
+
+// Gather a row-major local block (n_loc x m) to all ranks as a global
+// row-major (n_global... padded) block.
+View gather_block(sp_context* ctx, const View& local, int m, DBuf<double>& keep) {
+    Comm& cm = ctx->comm;
+    if (!cm.active()) return local;
+    View g = cm.gather_rows(local, m, ctx->stream);
+    keep.alloc(static_cast<size_t>(cm.n_pad) * cm.world * m);
+    SPB_CUDA(cudaMemcpyAsync(keep.p, g.ptr, sizeof(double) * cm.n_pad * cm.world * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    return rowmajor(keep.p, m, m);
+}
+
+} // namespace
+
+} // namespace spb
+
+using namespace spb;
+
+extern "C" {
+
+int sp_version(void) { return 1; }
+
+sp_status sp_context_create(int device, sp_context** out) {
+    if (!out) return SP_INVALID;
+    *out = nullptr;
+    auto* c = new sp_context();
+    c->device = device;
+    try {
+        SPB_CUDA(cudaSetDevice(device));
+        SPB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        SPB_CUDA(cudaEventCreate(&c->ev0));
+        SPB_CUDA(cudaEventCreate(&c->ev1));
+    } catch (...) {
+        const sp_status st = map_exception(c);
+        delete c;
+        return st;
+    }
+    *out = c;
+    return SP_OK;
+}
+
+sp_status sp_nccl_unique_id(void* out128) {
+    if (!out128) return SP_INVALID;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SP_NCCL;
+    std::memcpy(out128, &id, sizeof(id));
+    return SP_OK;
+}
+
+sp_status sp_context_create_dist(int device, int rank, int world, const void* nccl_id128, sp_context** out) {
+    sp_status st = sp_context_create(device, out);
+    if (st != SP_OK) return st;
+    if (world <= 1) return SP_OK;
+    sp_context* c = *out;
+    try {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id128, sizeof(id));
+        SPB_NCCL(ncclCommInitRank(&c->comm.nccl, world, id, rank));
+        c->comm.rank = rank;
+        c->comm.world = world;
+    } catch (...) {
+        st = map_exception(c);
+        sp_context_destroy(c);
+        *out = nullptr;
+        return st;
+    }
+    return SP_OK;
+}
+
+void sp_context_destroy(sp_context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->comm.nccl) ncclCommDestroy(c->comm.nccl);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* sp_last_error(const sp_context* c) { return c ? c->err.c_str() : "null context"; }
+
+sp_status sp_context_set_timing(sp_context* c, int on) {
+    if (!c) return SP_INVALID;
+    c->time_spmm = on != 0;
+    return SP_OK;
+}
+
+sp_status sp_partition(sp_context* ctx, const sp_graph* hg, const sp_config* cfg, int32_t* assignment_out,
+                       sp_report* rep, const double* x0) {
+    return guarded(ctx, [&] {
+        if (!cfg || !assignment_out) throw_invalid("sp_partition: null argument");
+        const int64_t K = cfg->num_parts;
+        if (K < 2) throw_infeasible("partition_graph: K must be >= 2");
+        if (K > hg->n)
+            throw_infeasible("partition_graph: K exceeds vertex count (K=" + std::to_string(K) +
+                             ", n=" + std::to_string(hg->n) + ")");
+        if (cfg->epsilon < 0.0) throw_infeasible("partition_graph: epsilon < 0");
+        const auto t_total = Clock::now();
+        cudaStream_t s = ctx->stream;
+        ctx->timers = Timers{};
+        ctx->comm.bytes_moved = 0;
+
+        sp_report R{};
+        double* pw_out = rep ? rep->part_weights : nullptr;
+        sp_trace_record* tr_out = rep ? rep->trace : nullptr;
+        const int32_t tr_cap = rep ? rep->trace_capacity : 0;
+
+        // Stage 1: graph upload + operators
+        const auto t_lap = Clock::now();
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        const GraphKindInfo kind = classify(g);
+        R.n = hg->n;
+        R.edges = g.nnz_global / 2;
+        R.graph_regular = kind.regular;
+        R.max_degree = kind.max_degree;
+        R.avg_degree = kind.avg;
+        R.degree_ratio = kind.ratio;
+        R.num_parts = K;
+        R.seed = cfg->seed;
+        R.max_iters = cfg->max_iters;
+        R.epsilon = cfg->epsilon;
+        R.doubled_cut = cfg->doubled_cut;
+        // resolution order: classify -> precond -> (problem, tol) -> init (pipeline.cpp:66-82)
+        R.precond = cfg->precond == SP_PRECOND_AUTO ? (kind.regular ? SP_PRECOND_AMG : SP_PRECOND_POLYNOMIAL)
+                                                    : cfg->precond;
+        if (R.precond == SP_PRECOND_AMG)
+            throw SpError(SP_ERROR, "AMG preconditioner is outside this build's hot path (SURVEY §8(f) rank 1); "
+                                    "pass precond=jacobi or polynomial");
+        const auto [auto_problem, auto_tol] = select_defaults(kind.regular, R.precond);
+        R.problem = cfg->problem == SP_PROBLEM_AUTO ? auto_problem : cfg->problem;
+        R.tol = cfg->tol > 0.0 ? cfg->tol : auto_tol;
+        R.init = cfg->init == SP_INIT_AUTO ? (kind.regular ? SP_INIT_RANDOM : SP_INIT_PIECEWISE) : cfg->init;
+        R.eigenvectors = eigenvector_count(K);
+        const int d = R.eigenvectors;
+        if (d > hg->n)
+            throw_infeasible("partition_graph: needs d=" + std::to_string(d) + " eigenvectors but n=" +
+                             std::to_string(hg->n));
+        if (d > 32) throw_dimension("partition_graph: d > 32 eigenvectors is not supported");
+
+        DevLaplacian A;
+        build_laplacian(operator_kind(R.problem), g, false, A, s);
+        if (!kind.regular) collect_long_rows(g, A, 4096, s);
+        const double* bdiag = nullptr;
+        if (R.problem == SP_PROBLEM_GENERALIZED) {
+            // B = D must be positive (laplacian.cpp:169-173); degrees are integers >= 0 for unit costs
+            std::vector<double> hd(g.n_local);
+            if (g.n_local) SPB_CUDA(cudaMemcpyAsync(hd.data(), g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToHost, s));
+            SPB_CUDA(cudaStreamSynchronize(s));
+            for (double v : hd)
+                if (!(v > 0.0)) throw_degenerate("generalized problem requires positive degrees");
+            bdiag = g.deg.p;
+        }
+        SPB_CUDA(cudaStreamSynchronize(s));
+        R.laplacian_s = since(t_lap);
+
+        // Stage 2: preconditioner + eigensolve
+        const auto t_eig = Clock::now();
+        Solver solver(ctx, A.op, bdiag, d);
+        DBuf<double> inv;
+        if (R.precond == SP_PRECOND_JACOBI) {
+            inverse_diagonal(A, inv, s);
+            solver.set_jacobi(inv.p);
+        } else if (R.precond == SP_PRECOND_POLYNOMIAL) {
+            solver.build_poly(cfg->seed ^ 0x706f6c79ULL, 25);
+            R.poly_degree = static_cast<int32_t>(solver.roots().size());
+        } else {
+            solver.set_none();
+        }
+        const int64_t nloc = g.n_local;
+        DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
+        const View X = rowmajor(Xb.p, d, d);
+        if (x0) upload_block(x0, hg->n, g.row0, nloc, d, X, s);
+        else if (R.init == SP_INIT_RANDOM) initial_block_random(hg->n, d, cfg->seed, g.row0, nloc, X, s);
+        else initial_block_piecewise(hg->n, d, g.row0, nloc, X, s);
+        SolveOpts so;
+        so.nev = d;
+        so.tol = R.tol;
+        so.max_iters = cfg->max_iters;
+        so.record_trace = cfg->record_trace != 0;
+        SolveResult er = solver.lobpcg(X, so, X);
+        SPB_CUDA(cudaStreamSynchronize(s));
+        R.eigensolve_s = since(t_eig);
+        R.iterations = er.iterations;
+        R.breakdown_retries = er.retries;
+        for (int j = 0; j < d; ++j) {
+            R.theta[j] = er.theta[j];
+            R.residual_norms[j] = er.residual_norms[j];
+            R.converged[j] = er.converged[j];
+        }
+        if (er.retries > 0) R.warnings |= SP_WARN_BREAKDOWN_RECOVERED;
+        if (!er.all_converged()) R.warnings |= SP_WARN_UNCONVERGED;
+
+        // Stage 3: embed (drop column 0) + multi-jagged
+        const auto t_mj = Clock::now();
+        DBuf<double> Xall;
+        const View Xg = gather_block(ctx, X, d, Xall);
+        DBuf<int32_t> asg(static_cast<size_t>(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : hg->n, 1)));
+        DBuf<double> wall;
+        const double* wdev = nullptr;
+        if (!g.unit_weights) {
+            wall.alloc(hg->n);
+            h2d(wall.p, hg->vertex_weights, hg->n, s);
+            wdev = wall.p;
+            for (int64_t i = 0; i < hg->n; ++i)
+                if (!(hg->vertex_weights[i] > 0.0)) throw_infeasible("mj_partition: weights must be positive");
+        }
+        mj_partition_dev(hg->n, d - 1, Xg.sub(1, d - 1), wdev, g.unit_weights, K, asg.p, s);
+        R.partition_s = since(t_mj);
+
+        // metrics (make_partition, graph.cpp:209-230)
+        PartitionMetrics pm = make_partition_dev(ctx, g, asg.p, K, cfg->doubled_cut != 0);
+        R.cutsize = pm.cut;
+        R.imbalance = pm.imbalance;
+        if (R.imbalance > 1.0 + cfg->epsilon) R.warnings |= SP_WARN_IMBALANCE;
+        SPB_CUDA(cudaMemcpyAsync(assignment_out, asg.p, sizeof(int32_t) * hg->n, cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        R.total_s = since(t_total);
+
+        R.spmm_launches = ctx->timers.spmm_launches;
+        R.spmm_bytes = ctx->timers.spmm_bytes;
+        R.spmm_ms = ctx->timers.spmm_ms;
+        R.kernel_launches = static_cast<int32_t>(ctx->timers.kernel_launches);
+        R.n_gpus = ctx->comm.world;
+        if (rep) {
+            R.part_weights = pw_out;
+            R.trace = tr_out;
+            R.trace_capacity = tr_cap;
+            if (pw_out) std::memcpy(pw_out, pm.part_weights.data(), sizeof(double) * K);
+            if (tr_out) {
+                int k = 0;
+                for (const TraceRec& t : er.trace) {
+                    if (k >= tr_cap) break;
+                    tr_out[k].iter = t.iter;
+                    tr_out[k].ntheta = static_cast<int32_t>(t.theta.size());
+                    tr_out[k].min_residual = t.min_residual;
+                    tr_out[k].max_residual = t.max_residual;
+                    for (size_t j = 0; j < t.theta.size() && j < SP_MAX_EIG; ++j) tr_out[k].theta[j] = t.theta[j];
+                    ++k;
+                }
+                R.trace_len = k;
+            }
+            *rep = R;
+        }
+    });
+}
+
+sp_status sp_build_laplacian(sp_context* ctx, int32_t kind, const sp_graph* hg, int64_t* offsets_out,
+                             int32_t* cols_out, double* vals_out, double* diag_out, double* bound_out,
+                             int32_t* is_diagonal_out) {
+    return guarded(ctx, [&] {
+        if (kind < 0 || kind > 2) throw_invalid("sp_build_laplacian: unknown kind");
+        if (hg->n == 0)
+            throw_invalid(kind == 0 ? "build_combinatorial: empty graph"
+                                    : kind == 1 ? "build_normalized: empty graph" : "build_degree: empty graph");
+        if (ctx->comm.active()) throw_invalid("sp_build_laplacian: single-GPU entry point");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        DevLaplacian L;
+        build_laplacian(kind, g, true, L, s);
+        const int64_t n = g.n_local;
+        const int64_t nnz = kind == 2 ? n : g.nnz_local + n;
+        if (offsets_out) SPB_CUDA(cudaMemcpyAsync(offsets_out, L.offs_L.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+        if (cols_out) SPB_CUDA(cudaMemcpyAsync(cols_out, L.cols_L.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s));
+        if (vals_out) SPB_CUDA(cudaMemcpyAsync(vals_out, L.vals_L.p, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+        if (diag_out) SPB_CUDA(cudaMemcpyAsync(diag_out, L.diag.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        if (bound_out) *bound_out = L.op.bound;
+        if (is_diagonal_out) *is_diagonal_out = L.op.is_diagonal ? 1 : 0;
+    });
+}
+
+sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* hg, const double* X, int32_t m, double* Y) {
+    return guarded(ctx, [&] {
+        if (ctx->comm.active()) throw_invalid("sp_spmm: single-GPU entry point");
+        if (m < 1 || m > kMaxCols) throw_dimension("sp_spmm: 1 <= m <= 64");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        DevLaplacian L;
+        build_laplacian(kind, g, false, L, s);
+        const int64_t n = g.n_local;
+        DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m), yd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m);
+        upload_block(X, n, 0, n, m, rowmajor(xd.p, m, m), s);
+        EpiArgs ea;
+        ea.mode = EPI_STORE;
+        ea.Y = rowmajor(yd.p, m, m);
+        spmm_launch(L.op, rowmajor(xd.p, m, m), m, ea, s);
+        download_block(rowmajor(yd.p, m, m), n, m, Y, s);
+    });
+}
+
+sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64_t* offsets, const int32_t* cols,
+                      const double* vals, const double* X, int32_t m, double* Y) {
+    return guarded(ctx, [&] {
+        if (m < 1 || m > kMaxCols) throw_dimension("sp_spmm_csr: 1 <= m <= 64");
+        cudaStream_t s = ctx->stream;
+        const int64_t nnz = offsets[nrows];
+        DBuf<int64_t> o(nrows + 1);
+        DBuf<int32_t> c(std::max<int64_t>(nnz, 1));
+        DBuf<double> v(std::max<int64_t>(nnz, 1));
+        h2d(o.p, offsets, nrows + 1, s);
+        h2d(c.p, cols, nnz, s);
+        if (vals) h2d(v.p, vals, nnz, s);
+        else fill_view(nnz, rowmajor(v.p, 1, 1), 1.0, s);
+        DevOp op;
+        op.mode = OP_EXPLICIT;
+        op.n = nrows;
+        op.nnz = nnz;
+        op.offs = o.p;
+        op.cols = c.p;
+        op.vals = v.p;
+        op.long_threshold = int64_t(1) << 40;
+        DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(ncols, 1)) * m), yd(static_cast<size_t>(std::max<int64_t>(nrows, 1)) * m);
+        upload_block(X, ncols, 0, ncols, m, rowmajor(xd.p, m, m), s);
+        EpiArgs ea;
+        ea.mode = EPI_STORE;
+        ea.Y = rowmajor(yd.p, m, m);
+        spmm_launch(op, rowmajor(xd.p, m, m), m, ea, s);
+        download_block(rowmajor(yd.p, m, m), nrows, m, Y, s);
+    });
+}
+
+sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const double* V, int32_t mv,
+                  const double* b, double* G) {
+    return guarded(ctx, [&] {
+        cudaStream_t s = ctx->stream;
+        const size_t rows = static_cast<size_t>(std::max<int64_t>(n, 1));
+        DBuf<double> ud(rows * mu), vd(rows * mv), bd, gd(static_cast<size_t>(mu + mv) * mv + 1),
+            scratch(static_cast<size_t>(device_sm_count()) * 4 * (static_cast<size_t>(mu + mv) * mv + 1));
+        upload_block(U, n, 0, n, mu, rowmajor(ud.p, mu, mu), s);
+        upload_block(V, n, 0, n, mv, rowmajor(vd.p, mv, mv), s);
+        if (b) {
+            bd.alloc(rows);
+            h2d(bd.p, b, n, s);
+        }
+        TsSpec sp;
+        sp.n = n;
+        sp.U0 = rowmajor(ud.p, mu, mu);
+        sp.V = rowmajor(vd.p, mv, mv);
+        sp.b = bd.p;
+        sp.gram = true;
+        sp.gram_left_u = true;
+        sp.gram_left_self = false;
+        if (n > 0) ts_run(sp, gd.p, scratch.p, scratch.n, s);
+        else SPB_CUDA(cudaMemsetAsync(gd.p, 0, sizeof(double) * mu * mv, s));
+        SPB_CUDA(cudaMemcpyAsync(G, gd.p, sizeof(double) * mu * mv, cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed, double* X_out) {
+    return guarded(ctx, [&] {
+        cudaStream_t s = ctx->stream;
+        DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(n, 1)) * std::max(d, 1));
+        const View X = rowmajor(xd.p, d, d);
+        if (init == SP_INIT_PIECEWISE) initial_block_piecewise(n, d, 0, n, X, s);
+        else initial_block_random(n, d, seed, 0, n, X, s);
+        download_block(X, n, d, X_out, s);
+    });
+}
+
+sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_t precond, uint64_t poly_seed,
+                    int32_t poly_degree, const double* X0, int32_t nev, double tol, int32_t max_iters,
+                    int32_t locking, double* theta_out, double* X_out, double* residuals_out,
+                    uint8_t* converged_out, int32_t* iterations_out, int32_t* retries_out) {
+    return guarded(ctx, [&] {
+        if (problem < SP_PROBLEM_COMBINATORIAL || problem > SP_PROBLEM_NORMALIZED)
+            throw_invalid("sp_lobpcg: problem must be explicit");
+        if (nev < 1) throw_infeasible("lobpcg: nev < 1");
+        if (nev > 32) throw_dimension("sp_lobpcg: nev <= 32");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        DevLaplacian A;
+        build_laplacian(operator_kind(problem), g, false, A, s);
+        const double* bdiag = nullptr;
+        if (problem == SP_PROBLEM_GENERALIZED) {
+            std::vector<double> hd(g.n_local);
+            if (g.n_local) SPB_CUDA(cudaMemcpyAsync(hd.data(), g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToHost, s));
+            SPB_CUDA(cudaStreamSynchronize(s));
+            for (double v : hd)
+                if (!(v > 0.0)) throw_degenerate("generalized problem requires positive degrees");
+            bdiag = g.deg.p;
+        }
+        Solver solver(ctx, A.op, bdiag, nev);
+        DBuf<double> inv;
+        if (precond == SP_PRECOND_JACOBI) {
+            inverse_diagonal(A, inv, s);
+            solver.set_jacobi(inv.p);
+        } else if (precond == SP_PRECOND_POLYNOMIAL) {
+            solver.build_poly(poly_seed, poly_degree > 0 ? poly_degree : 25);
+        }
+        const int64_t nloc = g.n_local;
+        DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * nev);
+        const View X = rowmajor(Xb.p, nev, nev);
+        upload_block(X0, hg->n, g.row0, nloc, nev, X, s);
+        SolveOpts so;
+        so.nev = nev;
+        so.tol = tol;
+        so.max_iters = max_iters;
+        so.locking = locking != 0;
+        SolveResult r = solver.lobpcg(X, so, X);
+        for (int j = 0; j < nev; ++j) {
+            theta_out[j] = r.theta[j];
+            if (residuals_out) residuals_out[j] = r.residual_norms[j];
+            if (converged_out) converged_out[j] = r.converged[j];
+        }
+        if (iterations_out) *iterations_out = r.iterations;
+        if (retries_out) *retries_out = r.retries;
+        if (X_out) {
+            DBuf<double> Xall;
+            const View Xg = gather_block(ctx, X, nev, Xall);
+            download_block(Xg, hg->n, nev, X_out, s);
+        }
+    });
+}
+
+sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* hg, uint64_t seed, int32_t degree,
+                        const double* Rh, int32_t m, double* H_out, double* roots_out, int32_t* achieved_out) {
+    return guarded(ctx, [&] {
+        if (ctx->comm.active()) throw_invalid("sp_poly_apply: single-GPU entry point");
+        if (m < 1 || m > 32) throw_dimension("sp_poly_apply: 1 <= m <= 32");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        DevLaplacian A;
+        build_laplacian(kind, g, false, A, s);
+        Solver solver(ctx, A.op, nullptr, m);
+        solver.build_poly(seed, degree > 0 ? degree : 25);
+        const int64_t n = g.n_local;
+        DBuf<double> rd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m), hd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m);
+        upload_block(Rh, n, 0, n, m, rowmajor(rd.p, m, m), s);
+        solver.apply_precond(rowmajor(rd.p, m, m), m, rowmajor(hd.p, m, m));
+        download_block(rowmajor(hd.p, m, m), n, m, H_out, s);
+        const std::vector<double>& rt = solver.roots();
+        if (roots_out) std::memcpy(roots_out, rt.data(), sizeof(double) * rt.size());
+        if (achieved_out) *achieved_out = static_cast<int32_t>(rt.size());
+    });
+}
+
+sp_status sp_mj_partition(sp_context* ctx, int64_t n, int32_t dims, const double* coords, const double* weights,
+                          int64_t K, int32_t* assignment_out, double* part_weights_out, double* imbalance_out) {
+    return guarded(ctx, [&] {
+        if (K < 1) throw_infeasible("mj_partition: K < 1");
+        if (n < K)
+            throw_infeasible("mj_partition: fewer points than parts (n=" + std::to_string(n) + ", K=" +
+                             std::to_string(K) + ")");
+        bool unit = true;
+        if (weights) {
+            for (int64_t i = 0; i < n; ++i) {
+                if (!(weights[i] > 0.0)) throw_infeasible("mj_partition: weights must be positive");
+                unit &= weights[i] == 1.0;
+            }
+        }
+        cudaStream_t s = ctx->stream;
+        DBuf<double> cd(static_cast<size_t>(std::max<int64_t>(n, 1)) * std::max(dims, 1)), wd;
+        upload_block(coords, n, 0, n, dims, rowmajor(cd.p, dims, dims), s);
+        if (!unit) {
+            wd.alloc(n);
+            h2d(wd.p, weights, n, s);
+        }
+        DBuf<int32_t> asg(std::max<int64_t>(n, 1));
+        mj_partition_dev(n, dims, rowmajor(cd.p, dims, dims), wd.p, unit, K, asg.p, s);
+        SPB_CUDA(cudaMemcpyAsync(assignment_out, asg.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        // mj_partition's own tally (partitioner.cpp:161-168): vertex order per part
+        std::vector<double> pw(K, 0.0);
+        for (int64_t v = 0; v < n; ++v) pw[assignment_out[v]] += weights ? weights[v] : 1.0;
+        if (part_weights_out) std::memcpy(part_weights_out, pw.data(), sizeof(double) * K);
+        if (imbalance_out) *imbalance_out = imbalance_of(pw);
+    });
+}
+
+sp_status sp_cut_imbalance(sp_context* ctx, const sp_graph* hg, const int32_t* assignment, int64_t K,
+                           int32_t doubled, double* cut_out, double* imbalance_out, double* part_weights_out) {
+    return guarded(ctx, [&] {
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        if (!g.unit_weights && !g.vw.p) throw_invalid("weights");
+        DBuf<int32_t> a(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : hg->n, 1));
+        h2d(a.p, assignment, hg->n, s);
+        PartitionMetrics pm = make_partition_dev(ctx, g, a.p, K, doubled != 0);
+        if (cut_out) *cut_out = pm.cut;
+        if (imbalance_out) *imbalance_out = pm.imbalance;
+        if (part_weights_out) std::memcpy(part_weights_out, pm.part_weights.data(), sizeof(double) * K);
+    });
+}
+
+} // extern "C"

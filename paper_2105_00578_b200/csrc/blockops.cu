@@ -1,0 +1,428 @@
+// blockops.cu — tall-skinny block kernels on row-major (or column-major) views.
+//
+// Replaces the tall-skinny kernels of src/kernels.cpp: gram (:79-110), mult
+// (:127-142), mult_sub (:144-157), dot/norm2/axpy (:159-185), diag_scale
+// (:187-197), scale_columns (:199-207), and the column copies in lobpcg.
+//
+// One kernel (ts_tile_kernel) streams row tiles of up to three input blocks
+// through shared memory, optionally transforms them (V - U*C for block
+// Gram-Schmidt, V*C for block combines), writes the result, and accumulates a
+// Gram matrix [left]^T diag(b) [right] of the tile in registers (2x2 register
+// blocks, row slices). Per-CTA partials are reduced in a fixed order by a second
+// kernel, so every Gram is bit-reproducible run to run (the reference's
+// chunked-reduction determinism contract, kernels.hpp:10-13).
+#include "ops.cuh"
+
+#include <algorithm>
+
+namespace spb {
+
+namespace {
+
+constexpr int kTsThreads = 256;
+constexpr int kTR = 32;  // rows per tile
+
+struct TsDev {
+    int64_t n;
+    View U0, U1, V, W, W2;
+    const double* C;
+    int ldc;
+    const double* b;
+    int transform;
+    int gram, left_u, left_self;
+    int u0, u1, kv, kw;
+    int P, Q;
+    int nb, slices;
+    double* partial;
+};
+
+__device__ __forceinline__ void load_tile(double* dst, const View& v, int64_t r0, int rows, int cols) {
+    const int total = rows * cols;
+    if (v.cs == 1) {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int r = idx / cols, c = idx - r * cols;
+            dst[r * cols + c] = v.ptr[(r0 + r) * v.rs + c];
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int c = idx / rows, r = idx - c * rows;
+            dst[r * cols + c] = v.ptr[(r0 + r) * v.rs + c * v.cs];
+        }
+    }
+}
+
+__device__ __forceinline__ void store_tile(const View& v, const double* src, int64_t r0, int rows,
+                                           int c_begin, int cols, int src_ld) {
+    // writes src[:, c_begin : c_begin+cols] into view columns 0..cols-1
+    const int total = rows * cols;
+    if (v.cs == 1) {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int r = idx / cols, c = idx - r * cols;
+            v.ptr[(r0 + r) * v.rs + c] = src[r * src_ld + c_begin + c];
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+            const int c = idx / rows, r = idx - c * rows;
+            v.ptr[(r0 + r) * v.rs + c * v.cs] = src[r * src_ld + c_begin + c];
+        }
+    }
+}
+
+template <int MAXB>
+__global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
+    extern __shared__ double smem[];
+    const int u = a.u0 + a.u1;
+    double* Ut = smem;                       // kTR x u
+    double* Vt = Ut + kTR * u;               // kTR x kv
+    double* Wt = Vt + kTR * a.kv;            // kTR x kw
+    double* Bt = Wt + kTR * a.kw;            // kTR
+    double* Cs = Bt + kTR;                   // inner x kw
+
+    const int inner = a.transform == TS_UPDATE ? u : a.kv;
+    const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
+    if (a.transform != TS_NONE)
+        for (int i = threadIdx.x; i < inner * a.kw; i += blockDim.x) {
+            const int c = i / inner, q = i - c * inner;
+            Cs[i] = a.C[q + static_cast<int64_t>(c) * a.ldc];
+        }
+
+    const double* right = (a.transform == TS_NONE) ? Vt : Wt;
+    const int rq = (a.transform == TS_NONE) ? a.kv : a.kw;
+
+    // gram thread assignment
+    double acc[MAXB][4];
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+    const int nbi = (a.P + 1) / 2;
+
+    const int64_t ntiles = (a.n + kTR - 1) / kTR;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = t * kTR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(kTR), a.n - r0));
+        __syncthreads();
+        if (need_u) {
+            if (a.u0) {
+                // U0 occupies columns [0, u0) of Ut, U1 [u0, u)
+                const int total = rows * a.u0;
+                for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+                    int r, c;
+                    if (a.U0.cs == 1) { r = idx / a.u0; c = idx - r * a.u0; }
+                    else { c = idx / rows; r = idx - c * rows; }
+                    Ut[r * u + c] = a.U0.ptr[(r0 + r) * a.U0.rs + c * a.U0.cs];
+                }
+            }
+            if (a.u1) {
+                const int total = rows * a.u1;
+                for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+                    int r, c;
+                    if (a.U1.cs == 1) { r = idx / a.u1; c = idx - r * a.u1; }
+                    else { c = idx / rows; r = idx - c * rows; }
+                    Ut[r * u + a.u0 + c] = a.U1.ptr[(r0 + r) * a.U1.rs + c * a.U1.cs];
+                }
+            }
+        }
+        load_tile(Vt, a.V, r0, rows, a.kv);
+        if (a.gram && a.b)
+            for (int r = threadIdx.x; r < rows; r += blockDim.x) Bt[r] = a.b[r0 + r];
+        __syncthreads();
+
+        if (a.transform == TS_UPDATE) {
+            const int total = rows * a.kw;
+            for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+                const int r = idx / a.kw, c = idx - r * a.kw;
+                double s = 0.0;
+                for (int q = 0; q < u; ++q) s = fma(Ut[r * u + q], Cs[q + c * u], s);
+                Wt[r * a.kw + c] = Vt[r * a.kv + c] - s;
+            }
+        } else if (a.transform == TS_COMBINE) {
+            const int total = rows * a.kw;
+            for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+                const int r = idx / a.kw, c = idx - r * a.kw;
+                double s = 0.0;
+                for (int q = 0; q < a.kv; ++q) s = fma(Vt[r * a.kv + q], Cs[q + c * a.kv], s);
+                Wt[r * a.kw + c] = s;
+            }
+        }
+        if (a.transform != TS_NONE) {
+            __syncthreads();
+            const int w1 = min(a.kw, a.W.cols);
+            if (w1 > 0) store_tile(a.W, Wt, r0, rows, 0, w1, a.kw);
+            if (a.kw > w1) store_tile(a.W2, Wt, r0, rows, w1, a.kw - w1, a.kw);
+        }
+
+        if (a.gram) {
+            // left column i: i < uL -> Ut[:, i]; else right[:, i - uL]
+            const int uL = a.left_u ? u : 0;
+#pragma unroll
+            for (int bb = 0; bb < MAXB; ++bb) {
+                const int blk = (MAXB == 1) ? (threadIdx.x % a.nb) : (threadIdx.x + bb * blockDim.x);
+                const int sl = (MAXB == 1) ? (threadIdx.x / a.nb) : 0;
+                if (blk >= a.nb || sl >= a.slices) continue;
+                const int bi = blk % nbi, bj = blk / nbi;
+                const int i0 = 2 * bi, j0 = 2 * bj;
+                const bool i1ok = i0 + 1 < a.P, j1ok = j0 + 1 < a.Q;
+                for (int r = sl; r < rows; r += a.slices) {
+                    const double bw = a.b ? Bt[r] : 1.0;
+                    double l0, l1 = 0.0;
+                    l0 = (i0 < uL) ? Ut[r * u + i0] : right[r * rq + (i0 - uL)];
+                    if (i1ok) l1 = (i0 + 1 < uL) ? Ut[r * u + i0 + 1] : right[r * rq + (i0 + 1 - uL)];
+                    double q0 = right[r * rq + j0];
+                    double q1 = j1ok ? right[r * rq + j0 + 1] : 0.0;
+                    if (a.b) { q0 *= bw; q1 *= bw; }
+                    acc[bb][0] = fma(l0, q0, acc[bb][0]);
+                    acc[bb][1] = fma(l1, q0, acc[bb][1]);
+                    acc[bb][2] = fma(l0, q1, acc[bb][2]);
+                    acc[bb][3] = fma(l1, q1, acc[bb][3]);
+                }
+            }
+        }
+    }
+
+    if (!a.gram) return;
+    double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
+    if (MAXB == 1) {
+        // reduce row slices in fixed order through shared memory
+        __syncthreads();
+        double* red = smem;  // blockDim x 4
+        for (int k = 0; k < 4; ++k) red[k * blockDim.x + threadIdx.x] = acc[0][k];
+        __syncthreads();
+        if (threadIdx.x < a.nb) {
+            const int blk = threadIdx.x;
+            const int bi = blk % nbi, bj = blk / nbi;
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int sl = 0; sl < a.slices; ++sl)
+                for (int k = 0; k < 4; ++k) s[k] += red[k * blockDim.x + sl * a.nb + blk];
+            const int i0 = 2 * bi, j0 = 2 * bj;
+            part[i0 + j0 * a.P] = s[0];
+            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = s[1];
+            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = s[2];
+            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = s[3];
+        }
+    } else {
+#pragma unroll
+        for (int bb = 0; bb < MAXB; ++bb) {
+            const int blk = threadIdx.x + bb * blockDim.x;
+            if (blk >= a.nb) continue;
+            const int bi = blk % nbi, bj = blk / nbi;
+            const int i0 = 2 * bi, j0 = 2 * bj;
+            part[i0 + j0 * a.P] = acc[bb][0];
+            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = acc[bb][1];
+            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = acc[bb][2];
+            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = acc[bb][3];
+        }
+    }
+}
+
+__global__ void reduce_gram_kernel(const double* partial, int rows, int PQ, double* out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= PQ) return;
+    double s = 0.0;
+    for (int r = 0; r < rows; ++r) s += partial[static_cast<int64_t>(r) * PQ + e];
+    out[e] = s;
+}
+
+__global__ void scale_cols_kernel(View v, const double* sc, int64_t n) {
+    const int64_t total = n * v.cols;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / v.cols;
+        const int c = static_cast<int>(idx - r * v.cols);
+        v.at(r, c) *= sc[c];
+    }
+}
+
+__global__ void diag_apply_kernel(int64_t n, const double* d, View in, View out) {
+    const int64_t total = n * in.cols;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / in.cols;
+        const int c = static_cast<int>(idx - r * in.cols);
+        out.at(r, c) = __dmul_rn(d[r], in.at(r, c));
+    }
+}
+
+struct ColList {
+    int k;
+    int idx[kMaxCols];
+};
+
+__global__ void gather_cols_kernel(int64_t n, View in, ColList cl, View out) {
+    const int64_t total = n * cl.k;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / cl.k;
+        const int c = static_cast<int>(idx - r * cl.k);
+        out.at(r, c) = in.at(r, cl.idx[c]);
+    }
+}
+
+__global__ void fill_kernel(int64_t n, View v, double value) {
+    const int64_t total = n * v.cols;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / v.cols;
+        const int c = static_cast<int>(idx - r * v.cols);
+        v.at(r, c) = value;
+    }
+}
+
+__global__ void scal_kernel(int64_t n, double a, View in, View out) {
+    const int64_t total = n * in.cols;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / in.cols;
+        const int c = static_cast<int>(idx - r * in.cols);
+        out.at(r, c) = __dmul_rn(a, in.at(r, c));
+    }
+}
+
+int elem_grid(int64_t total) { return grid_for(total, 256, 8); }
+
+__global__ void colsum_kernel(int64_t n, View v, double* partial) {
+    // thread-private sums over a grid-stride of rows, then fixed-order CTA tree
+    __shared__ double red[256];
+    for (int c = 0; c < v.cols; ++c) {
+        double s = 0.0;
+        for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+             r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            s += v.at(r, c);
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[static_cast<int64_t>(blockIdx.x) * v.cols + c] = red[0];
+        __syncthreads();
+    }
+}
+
+} // namespace
+
+int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s) {
+    const int grid = grid_for(n, 256, 2);
+    colsum_kernel<<<grid, 256, 0, s>>>(n, v, scratch);
+    SPB_LAUNCH_CHECK();
+    return grid;
+}
+
+int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_elems, cudaStream_t st) {
+    TsDev a{};
+    a.n = s.n;
+    a.U0 = s.U0;
+    a.U1 = s.U1;
+    a.V = s.V;
+    a.W = s.W;
+    a.W2 = s.W2;
+    a.C = s.C;
+    a.b = s.b;
+    a.transform = s.transform;
+    a.u0 = s.U0.ptr ? s.U0.cols : 0;
+    a.u1 = s.U1.ptr ? s.U1.cols : 0;
+    a.kv = s.V.cols;
+    a.kw = 0;
+    if (s.transform == TS_UPDATE) a.kw = a.kv;
+    if (s.transform == TS_COMBINE) a.kw = s.W.cols + (s.W2.ptr ? s.W2.cols : 0);
+    a.gram = s.gram ? 1 : 0;
+    a.left_u = s.gram_left_u ? 1 : 0;
+    a.left_self = s.gram_left_self ? 1 : 0;
+    const int rq = s.transform == TS_NONE ? a.kv : a.kw;
+    a.Q = rq;
+    a.P = (a.left_u ? a.u0 + a.u1 : 0) + (a.left_self ? rq : 0);
+    if (s.n <= 0) return a.P;
+
+    int maxb = 1;
+    if (a.gram) {
+        a.nb = ((a.P + 1) / 2) * ((a.Q + 1) / 2);
+        if (a.nb <= kTsThreads) {
+            a.slices = kTsThreads / a.nb;
+        } else {
+            a.slices = 1;
+            maxb = (a.nb + kTsThreads - 1) / kTsThreads;
+        }
+    } else {
+        a.nb = 1;
+        a.slices = 1;
+    }
+    const int64_t ntiles = (s.n + kTR - 1) / kTR;
+    int grid = grid_for(ntiles, 1, 4);
+    const size_t PQ = static_cast<size_t>(a.P) * a.Q;
+    if (a.gram) {
+        // shrink the grid if the partial scratch is too small (keeps determinism: grid is a
+        // pure function of (n, P, Q, scratch size))
+        while (static_cast<size_t>(grid) * PQ > scratch_elems && grid > 1) grid = (grid + 1) / 2;
+        if (static_cast<size_t>(grid) * PQ > scratch_elems)
+            throw SpError(1, "ts_run: gram scratch too small");
+    }
+    a.partial = scratch;
+    const int u = a.u0 + a.u1;
+    const int inner = s.transform == TS_UPDATE ? u : a.kv;
+    a.ldc = s.ldc > 0 ? s.ldc : inner;
+    size_t sm = sizeof(double) *
+                (static_cast<size_t>(kTR) * (u + a.kv + a.kw) + kTR +
+                 (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
+    sm = std::max(sm, sizeof(double) * 4 * kTsThreads);
+    auto launch = [&](auto kern) {
+        if (sm > 48 * 1024) SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        kern<<<grid, kTsThreads, sm, st>>>(a);
+    };
+    if (maxb <= 1) launch(ts_tile_kernel<1>);
+    else if (maxb <= 2) launch(ts_tile_kernel<2>);
+    else if (maxb <= 4) launch(ts_tile_kernel<4>);
+    else if (maxb <= 8) launch(ts_tile_kernel<8>);
+    else if (maxb <= 16) launch(ts_tile_kernel<16>);
+    else throw_dimension("ts_run: gram too large");
+    SPB_LAUNCH_CHECK();
+    if (a.gram) {
+        reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 128), 128, 0, st>>>(
+            scratch, grid, static_cast<int>(PQ), gram_out);
+        SPB_LAUNCH_CHECK();
+    }
+    return a.P;
+}
+
+void scale_cols(View V, const double* colscale_dev, cudaStream_t s, int64_t n) {
+    if (n <= 0 || V.cols <= 0) return;
+    scale_cols_kernel<<<elem_grid(n * V.cols), 256, 0, s>>>(V, colscale_dev, n);
+    SPB_LAUNCH_CHECK();
+}
+
+void diag_apply(int64_t n, const double* d, View in, View out, cudaStream_t s) {
+    if (n <= 0 || in.cols <= 0) return;
+    diag_apply_kernel<<<elem_grid(n * in.cols), 256, 0, s>>>(n, d, in, out);
+    SPB_LAUNCH_CHECK();
+}
+
+void jacobi_apply(int64_t n, const double* inv_diag, View in, View out, cudaStream_t s) {
+    diag_apply(n, inv_diag, in, out, s);
+}
+
+void copy_view(int64_t n, View in, View out, cudaStream_t s) {
+    if (n <= 0 || in.cols <= 0) return;
+    scal_kernel<<<elem_grid(n * in.cols), 256, 0, s>>>(n, 1.0, in, out);
+    SPB_LAUNCH_CHECK();
+}
+
+void poly_first_only(int64_t n, double inv0, View R, View H, cudaStream_t s) {
+    if (n <= 0 || R.cols <= 0) return;
+    scal_kernel<<<elem_grid(n * R.cols), 256, 0, s>>>(n, inv0, R, H);
+    SPB_LAUNCH_CHECK();
+}
+
+void gather_cols(int64_t n, View in, const int* cols_host, int k, View out, cudaStream_t s) {
+    if (n <= 0 || k <= 0) return;
+    if (k > kMaxCols) throw_dimension("gather_cols: too many columns");
+    ColList cl{};
+    cl.k = k;
+    for (int i = 0; i < k; ++i) cl.idx[i] = cols_host[i];
+    gather_cols_kernel<<<elem_grid(n * k), 256, 0, s>>>(n, in, cl, out);
+    SPB_LAUNCH_CHECK();
+}
+
+void fill_view(int64_t n, View v, double value, cudaStream_t s) {
+    if (n <= 0 || v.cols <= 0) return;
+    fill_kernel<<<elem_grid(n * v.cols), 256, 0, s>>>(n, v, value);
+    SPB_LAUNCH_CHECK();
+}
+
+} // namespace spb

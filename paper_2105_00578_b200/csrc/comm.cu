@@ -1,0 +1,91 @@
+// comm.cu — NCCL plumbing for the 1-D row partition.
+//
+// The reference has no communication layer (single-node OpenMP). The
+// B200 build shards rows over the GPUs of one box: SpMM inputs are all-gathered
+// over NVLink (halo = everything for R-MAT; a superset of the 2 z-slab halos for
+// meshes), and every block inner product is an all-gather of per-rank partials
+// followed by a rank-order sum, which keeps results bit-identical on every rank
+// and run to run at a fixed GPU count.
+#include "context.hpp"
+
+namespace spb {
+
+namespace {
+
+__global__ void pack_kernel(int64_t n, View in, double* out, int m) {
+    const int64_t total = n * m;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = idx / m;
+        const int c = static_cast<int>(idx - r * m);
+        out[idx] = in.at(r, c);
+    }
+}
+
+__global__ void ordered_sum_kernel(const double* parts, int world, int count, double* out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    double s = 0.0;
+    for (int r = 0; r < world; ++r) s += parts[static_cast<int64_t>(r) * count + e];
+    out[e] = s;
+}
+
+__global__ void ordered_sum_i64_kernel(const int64_t* parts, int world, int count, int64_t* out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    int64_t s = 0;
+    for (int r = 0; r < world; ++r) s += parts[static_cast<int64_t>(r) * count + e];
+    out[e] = s;
+}
+
+} // namespace
+
+View Comm::gather_rows(const View& local, int m, cudaStream_t s) {
+    if (!active()) return local;
+    const int64_t nl = nloc();
+    stage.alloc(static_cast<size_t>(n_pad) * m);
+    full.alloc(static_cast<size_t>(n_pad) * world * m);
+    if (nl > 0) {
+        pack_kernel<<<grid_for(nl * m, 256, 8), 256, 0, s>>>(nl, local, stage.p, m);
+        SPB_LAUNCH_CHECK();
+    }
+    SPB_NCCL(ncclAllGather(stage.p, full.p, static_cast<size_t>(n_pad) * m, ncclDouble, nccl, s));
+    bytes_moved += static_cast<int64_t>(n_pad) * m * 8 * (world - 1);
+    return rowmajor(full.p, m, m);
+}
+
+void Comm::sum_small(double* dev, int count, cudaStream_t s) {
+    if (!active() || count <= 0) return;
+    small.alloc(static_cast<size_t>(count) * world);
+    SPB_NCCL(ncclAllGather(dev, small.p, count, ncclDouble, nccl, s));
+    ordered_sum_kernel<<<ceil_div(count, 128), 128, 0, s>>>(small.p, world, count, dev);
+    SPB_LAUNCH_CHECK();
+}
+
+void Comm::sum_i64(int64_t* dev, int count, cudaStream_t s) {
+    if (!active() || count <= 0) return;
+    DBuf<int64_t> tmp(static_cast<size_t>(count) * world);
+    SPB_NCCL(ncclAllGather(dev, tmp.p, count, ncclInt64, nccl, s));
+    ordered_sum_i64_kernel<<<ceil_div(count, 128), 128, 0, s>>>(tmp.p, world, count, dev);
+    SPB_LAUNCH_CHECK();
+    SPB_CUDA(cudaStreamSynchronize(s));
+}
+
+void Comm::gather_i32(const int32_t* local, int32_t* global, cudaStream_t s) {
+    if (!active()) {
+        SPB_CUDA(cudaMemcpyAsync(global, local, sizeof(int32_t) * n_global, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    // local must hold n_pad entries (the tail beyond nloc() is ignored by readers)
+    SPB_NCCL(ncclAllGather(local, global, n_pad, ncclInt32, nccl, s));
+}
+
+void Comm::gather_f64(const double* local, double* global, cudaStream_t s) {
+    if (!active()) {
+        SPB_CUDA(cudaMemcpyAsync(global, local, sizeof(double) * n_global, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
+    SPB_NCCL(ncclAllGather(local, global, n_pad, ncclDouble, nccl, s));
+}
+
+} // namespace spb

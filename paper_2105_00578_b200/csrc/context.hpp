@@ -1,0 +1,76 @@
+// context.hpp — the opaque sp_context: device, streams, NCCL communicator,
+// reusable scratch, device event timers.
+#pragma once
+
+#include "graph_dev.cuh"
+
+#include <nccl.h>
+
+#include <string>
+
+namespace spb {
+
+#define SPB_NCCL(call)                                                                   \
+    do {                                                                                 \
+        ncclResult_t _r = (call);                                                        \
+        if (_r != ncclSuccess)                                                           \
+            throw ::spb::SpError(9, std::string("NCCL: ") + ncclGetErrorString(_r) + " at " + \
+                                        __FILE__ + ":" + std::to_string(__LINE__));      \
+    } while (0)
+
+// 1-D row partition over the ranks of one box: rank k owns global
+// rows [k*n_pad, min(n, (k+1)*n_pad)), so a row-gathered block indexed by global
+// id is exactly the NCCL all-gather of the equal-size (padded) rank slices.
+struct Comm {
+    int rank = 0;
+    int world = 1;
+    ncclComm_t nccl = nullptr;
+    int64_t n_global = 0;
+    int64_t n_pad = 0;
+    DBuf<double> stage;    // n_pad x m contiguous send slice
+    DBuf<double> full;     // world*n_pad x m gathered block
+    DBuf<double> small;    // world x count for deterministic small sums
+    int64_t bytes_moved = 0;
+
+    bool active() const { return world > 1; }
+    void setup(int64_t n) {
+        n_global = n;
+        n_pad = (n + world - 1) / world;
+    }
+    int64_t row0() const { return static_cast<int64_t>(rank) * n_pad; }
+    int64_t nloc() const {
+        const int64_t r0 = row0();
+        return r0 >= n_global ? 0 : std::min<int64_t>(n_pad, n_global - r0);
+    }
+
+    // Gathers the local n_loc x m block `local` into a row-major (world*n_pad) x m
+    // block indexed by global row id. One GPU: returns `local` untouched.
+    View gather_rows(const View& local, int m, cudaStream_t s);
+    // In-place deterministic sum over ranks of `count` doubles on the device:
+    // all-gather then a fixed rank-order sum (bit-identical on every rank).
+    void sum_small(double* dev, int count, cudaStream_t s);
+    // Sum of int64 counters (exact).
+    void sum_i64(int64_t* dev, int count, cudaStream_t s);
+    // Gathers int32 per-row values (n_loc each) into a global array (world*n_pad).
+    void gather_i32(const int32_t* local, int32_t* global, cudaStream_t s);
+    void gather_f64(const double* local, double* global, cudaStream_t s);
+};
+
+struct Timers {
+    double spmm_ms = 0.0;
+    int64_t spmm_launches = 0;
+    double spmm_bytes = 0.0;
+    int64_t kernel_launches = 0;
+};
+
+} // namespace spb
+
+struct sp_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    spb::Comm comm;
+    std::string err;
+    spb::Timers timers;
+    bool time_spmm = false;   // record CUDA events around every SpMM (bench/diagnostics)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};

@@ -1,0 +1,304 @@
+// mj.cu — multi-jagged partitioning of the eigenvector embedding on the device.
+//
+// Restates mj_partition / mj_recurse / build_plan (src/partitioner.cpp:43-170).
+// The recursion becomes a level-synchronous sweep: at every level all tree
+// nodes of that depth are sorted at once by the composite key
+// (node, coordinate, vertex id), so each node's points are in exactly the
+// reference's std::sort order (coordinate ascending, ties by ascending id,
+// -0.0 == +0.0). Child ranges are exact weighted quantiles: for unit weights
+// their sizes follow in closed form from the reference's greedy loop; for other
+// weights one thread per node replays that loop over the sorted weights, so
+// fp sums happen in the reference's order. Leaves are numbered left to right,
+// which is the reference's depth-first next_part order.
+#include "mj.hpp"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda/std/tuple>
+
+#include <algorithm>
+#include <cmath>
+
+namespace spb {
+
+namespace {
+
+struct MjKey {
+    uint32_t id;
+    uint32_t seg;
+    uint64_t coord;
+};
+
+struct MjDecomposer {
+    __host__ __device__ ::cuda::std::tuple<uint32_t&, uint64_t&, uint32_t&> operator()(MjKey& k) const {
+        return {k.seg, k.coord, k.id};
+    }
+};
+
+__device__ __forceinline__ uint64_t orderable(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 compares equal to +0.0 in the reference comparator
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// seg index of position p: largest r with starts[r] <= p
+__device__ __forceinline__ int find_seg(const int64_t* starts, int nseg, int64_t p) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (starts[mid] <= p) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void make_keys_kernel(int64_t n, const uint32_t* ids, const int64_t* starts,
+                                 const int* seg_dim, int nseg, View coords, MjKey* keys) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int sg = find_seg(starts, nseg, p);
+        const uint32_t id = ids[p];
+        const int dim = seg_dim[sg];
+        MjKey k;
+        k.id = id;
+        k.seg = static_cast<uint32_t>(sg);
+        k.coord = dim >= 0 ? orderable(coords.at(id, dim)) : 0ull;
+        keys[p] = k;
+    }
+}
+
+__global__ void keys_to_ids_kernel(int64_t n, const MjKey* keys, uint32_t* ids) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        ids[p] = keys[p].id;
+}
+
+// General weights: one thread per internal node replays mj_recurse's greedy
+// loop (partitioner.cpp:100-132) over the node's weights in sorted order.
+__global__ void weighted_cuts_kernel(int nnodes, const int64_t* nstart, const int64_t* nsize,
+                                     const int* child_off, const int64_t* child_leaves,
+                                     const int* nchild, const int64_t* nleaves,
+                                     const uint32_t* ids, const double* w, int64_t* child_size) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nnodes) return;
+    const int64_t start = nstart[t], size = nsize[t];
+    double total = 0.0;
+    for (int64_t p = 0; p < size; ++p) total += w[ids[start + p]];
+    const int64_t L = nleaves[t];
+    int64_t pos = 0, leaves_done = 0;
+    double consumed = 0.0;
+    const int nc = nchild[t];
+    for (int s = 0; s < nc; ++s) {
+        const int64_t cl = child_leaves[child_off[t] + s];
+        leaves_done += cl;
+        if (s + 1 == nc) {
+            child_size[child_off[t] + s] = size - pos;
+            pos = size;
+            break;
+        }
+        const double target = total * static_cast<double>(leaves_done) / static_cast<double>(L);
+        const int64_t leaves_after = L - leaves_done;
+        const int64_t max_take = size - pos - leaves_after;
+        const int64_t min_take = cl;
+        int64_t taken = 0;
+        while (pos < size && taken < max_take && (taken < min_take || consumed < target)) {
+            consumed += w[ids[start + pos]];
+            ++pos;
+            ++taken;
+        }
+        child_size[child_off[t] + s] = taken;
+    }
+}
+
+__global__ void assign_kernel(int64_t n, const uint32_t* ids, const int64_t* starts, int nseg,
+                              int32_t* assignment) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        assignment[ids[p]] = find_seg(starts, nseg, p);
+}
+
+__global__ void iota_kernel(int64_t n, uint32_t* ids) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        ids[p] = static_cast<uint32_t>(p);
+}
+
+int g1(int64_t n) { return grid_for(n, 256, 8); }
+
+void build_plan(MjPlanNode& node, int64_t target, int dim, int remaining) {
+    node.leaves = target;
+    node.dim = -1;
+    node.kids.clear();
+    if (target <= 1 || remaining <= 0) return;
+    const double root = std::pow(static_cast<double>(target), 1.0 / remaining);
+    int64_t m = static_cast<int64_t>(std::ceil(root - 1e-12));
+    m = std::min<int64_t>(target, std::max<int64_t>(m, 2));
+    node.dim = dim;
+    const int64_t base = target / m, rem = target % m;
+    node.kids.resize(m);
+    for (int64_t s = 0; s < m; ++s) build_plan(node.kids[s], base + (s < rem ? 1 : 0), dim + 1, remaining - 1);
+}
+
+} // namespace
+
+int64_t MjPlanNode::leaf_count() const {
+    if (kids.empty()) return 1;
+    int64_t t = 0;
+    for (const MjPlanNode& k : kids) t += k.leaf_count();
+    return t;
+}
+
+MjPlanNode mj_plan(int64_t num_parts, int dims) {
+    if (num_parts < 1) throw_infeasible("section_counts: K < 1");
+    if (dims < 1) throw_infeasible("section_counts: dims < 1");
+    MjPlanNode root;
+    build_plan(root, num_parts, 0, dims);
+    return root;
+}
+
+void mj_partition_dev(int64_t n, int dims, const View& coords, const double* weights_dev,
+                      bool unit_weights, int64_t num_parts, int32_t* assignment_dev, cudaStream_t s) {
+    if (num_parts < 1) throw_infeasible("mj_partition: K < 1");
+    if (n < num_parts)
+        throw_infeasible("mj_partition: fewer points than parts (n=" + std::to_string(n) +
+                         ", K=" + std::to_string(num_parts) + ")");
+    if (n >= (int64_t(1) << 32)) throw_dimension("mj_partition: n too large");
+    const MjPlanNode plan = mj_plan(num_parts, dims);
+
+    DBuf<uint32_t> ids(n);
+    DBuf<MjKey> kin(n), kout(n);
+    iota_kernel<<<g1(n), 256, 0, s>>>(n, ids.p);
+    SPB_LAUNCH_CHECK();
+
+    struct Range {
+        int64_t start, size;
+        const MjPlanNode* node;
+    };
+    std::vector<Range> ranges{{0, n, &plan}};
+    DBuf<int64_t> d_starts;
+    DBuf<int> d_dims;
+    DBuf<char> temp;
+    size_t temp_bytes = 0;
+
+    auto upload_ranges = [&](const std::vector<Range>& rs, bool with_dims) {
+        std::vector<int64_t> st(rs.size());
+        std::vector<int> dm(rs.size());
+        for (size_t i = 0; i < rs.size(); ++i) {
+            st[i] = rs[i].start;
+            dm[i] = (with_dims && !rs[i].node->kids.empty()) ? rs[i].node->dim % dims : -1;
+        }
+        d_starts.alloc(st.size());
+        d_dims.alloc(dm.size());
+        SPB_CUDA(cudaMemcpyAsync(d_starts.p, st.data(), sizeof(int64_t) * st.size(), cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemcpyAsync(d_dims.p, dm.data(), sizeof(int) * dm.size(), cudaMemcpyHostToDevice, s));
+    };
+
+    for (;;) {
+        bool any_internal = false;
+        for (const Range& r : ranges)
+            if (!r.node->kids.empty()) any_internal = true;
+        if (!any_internal) break;
+        const int nseg = static_cast<int>(ranges.size());
+        upload_ranges(ranges, true);
+        make_keys_kernel<<<g1(n), 256, 0, s>>>(n, ids.p, d_starts.p, d_dims.p, nseg, coords, kin.p);
+        SPB_LAUNCH_CHECK();
+        int seg_bits = 1;
+        while ((int64_t(1) << seg_bits) < nseg) ++seg_bits;
+        const int end_bit = 64 + 32 + seg_bits;
+        size_t need = 0;
+        SPB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, kin.p, kout.p, n, MjDecomposer{}, 0,
+                                                end_bit, s));
+        if (need > temp_bytes) {
+            temp.alloc(need);
+            temp_bytes = need;
+        }
+        SPB_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, need, kin.p, kout.p, n, MjDecomposer{}, 0,
+                                                end_bit, s));
+        keys_to_ids_kernel<<<g1(n), 256, 0, s>>>(n, kout.p, ids.p);
+        SPB_LAUNCH_CHECK();
+
+        // child ranges
+        std::vector<Range> next;
+        if (unit_weights) {
+            for (const Range& r : ranges) {
+                if (r.node->kids.empty()) {
+                    next.push_back(r);
+                    continue;
+                }
+                const int64_t size = r.size, L = r.node->leaves;
+                const double W = static_cast<double>(size);
+                int64_t pos = 0, leaves_done = 0;
+                const size_t nc = r.node->kids.size();
+                for (size_t c = 0; c < nc; ++c) {
+                    const MjPlanNode& kid = r.node->kids[c];
+                    const int64_t cl = kid.leaf_count();
+                    leaves_done += cl;
+                    int64_t take;
+                    if (c + 1 == nc) {
+                        take = size - pos;
+                    } else {
+                        const double target = W * static_cast<double>(leaves_done) / static_cast<double>(L);
+                        const int64_t max_take = size - pos - (L - leaves_done);
+                        const int64_t t_target = std::max<int64_t>(0, static_cast<int64_t>(std::ceil(target)) - pos);
+                        take = std::max(cl, t_target);
+                        take = std::min(take, max_take);
+                        take = std::min(take, size - pos);
+                        take = std::max<int64_t>(take, 0);
+                    }
+                    next.push_back({r.start + pos, take, &kid});
+                    pos += take;
+                }
+            }
+        } else {
+            std::vector<int64_t> nst, nsz, nl, cleaves;
+            std::vector<int> coff, nch;
+            std::vector<const Range*> internal;
+            for (const Range& r : ranges) {
+                if (r.node->kids.empty()) continue;
+                internal.push_back(&r);
+                nst.push_back(r.start);
+                nsz.push_back(r.size);
+                nl.push_back(r.node->leaves);
+                coff.push_back(static_cast<int>(cleaves.size()));
+                nch.push_back(static_cast<int>(r.node->kids.size()));
+                for (const MjPlanNode& k : r.node->kids) cleaves.push_back(k.leaf_count());
+            }
+            const int nn = static_cast<int>(internal.size());
+            DBuf<int64_t> a(nn), b(nn), c(nn), d(cleaves.size()), out(cleaves.size());
+            DBuf<int> e(nn), f(nn);
+            SPB_CUDA(cudaMemcpyAsync(a.p, nst.data(), sizeof(int64_t) * nn, cudaMemcpyHostToDevice, s));
+            SPB_CUDA(cudaMemcpyAsync(b.p, nsz.data(), sizeof(int64_t) * nn, cudaMemcpyHostToDevice, s));
+            SPB_CUDA(cudaMemcpyAsync(c.p, nl.data(), sizeof(int64_t) * nn, cudaMemcpyHostToDevice, s));
+            SPB_CUDA(cudaMemcpyAsync(d.p, cleaves.data(), sizeof(int64_t) * cleaves.size(), cudaMemcpyHostToDevice, s));
+            SPB_CUDA(cudaMemcpyAsync(e.p, coff.data(), sizeof(int) * nn, cudaMemcpyHostToDevice, s));
+            SPB_CUDA(cudaMemcpyAsync(f.p, nch.data(), sizeof(int) * nn, cudaMemcpyHostToDevice, s));
+            weighted_cuts_kernel<<<ceil_div(nn, 64), 64, 0, s>>>(nn, a.p, b.p, e.p, d.p, f.p, c.p, ids.p,
+                                                                 weights_dev, out.p);
+            SPB_LAUNCH_CHECK();
+            std::vector<int64_t> sizes(cleaves.size());
+            SPB_CUDA(cudaMemcpyAsync(sizes.data(), out.p, sizeof(int64_t) * sizes.size(), cudaMemcpyDeviceToHost, s));
+            SPB_CUDA(cudaStreamSynchronize(s));
+            size_t ii = 0;
+            for (const Range& r : ranges) {
+                if (r.node->kids.empty()) {
+                    next.push_back(r);
+                    continue;
+                }
+                int64_t pos = 0;
+                for (size_t cidx = 0; cidx < r.node->kids.size(); ++cidx) {
+                    const int64_t take = sizes[coff[ii] + cidx];
+                    next.push_back({r.start + pos, take, &r.node->kids[cidx]});
+                    pos += take;
+                }
+                ++ii;
+            }
+        }
+        ranges.swap(next);
+    }
+    // every range is a leaf now; leaves in position order = DFS order
+    upload_ranges(ranges, false);
+    assign_kernel<<<g1(n), 256, 0, s>>>(n, ids.p, d_starts.p, static_cast<int>(ranges.size()), assignment_dev);
+    SPB_LAUNCH_CHECK();
+    SPB_CUDA(cudaStreamSynchronize(s));
+}
+
+} // namespace spb

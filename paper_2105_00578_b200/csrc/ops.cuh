@@ -1,0 +1,106 @@
+// ops.cuh — device operator representation and kernel launchers.
+//
+// The Laplacian operators of laplacian.cpp:53-144 are held on the device in one
+// of four forms. All of them reproduce kernels::spmv_block (kernels.cpp:36-62)
+// bit for bit: each output element is a sequential, FMA-free sum over the row of
+// the explicit CSR of L, in storage order, with the diagonal term inserted at the
+// position build_combinatorial/build_normalized place it (before the first
+// column > i).
+//   OP_EXPLICIT     : explicit CSR (int64 offsets, int32 cols, fp64 values).
+//   OP_LAPLACE_UNIT : L_C of a unit-cost graph from the adjacency pattern alone:
+//                     off-diagonals are -1 (exact), diagonal = degree. 4 B/nnz.
+//   OP_NORMAL_UNIT  : L_N of a unit-cost graph from the pattern and
+//                     isd = 1/sqrt(deg): off-diagonal (-isd_i)*isd_j (laplacian.cpp:114).
+//   OP_DIAGONAL     : y = d .* x (build_degree / is_diagonal, kernels::diag_scale).
+#pragma once
+
+#include "common.cuh"
+
+namespace spb {
+
+enum OpMode { OP_EXPLICIT = 0, OP_LAPLACE_UNIT = 1, OP_NORMAL_UNIT = 2, OP_DIAGONAL = 3 };
+
+struct DevOp {
+    int mode = OP_EXPLICIT;
+    int64_t n = 0;              // local rows
+    int64_t row0 = 0;           // global id of local row 0 (multi-GPU row block)
+    int64_t nnz = 0;            // stored entries traversed by the kernel
+    const int64_t* offs = nullptr;
+    const int32_t* cols = nullptr;  // GLOBAL column ids (multi-GPU: index into the full vector)
+    const double* vals = nullptr;
+    const double* diag = nullptr;   // a_ii (degree for L_C, 1 for L_N, d for diagonal)
+    const double* isd = nullptr;    // OP_NORMAL_UNIT: 1/sqrt(deg), indexed by global column
+    // long-row bin (rows handled by the CTA-per-row kernel)
+    const int32_t* long_rows = nullptr;
+    int64_t n_long = 0;
+    int64_t long_threshold = 1 << 30;
+    double bound = 0.0;
+    bool is_diagonal = false;
+};
+
+// Epilogues fused into the SpMM.
+enum EpiMode { EPI_STORE = 0, EPI_RESIDUAL = 1, EPI_POLY = 2 };
+
+constexpr int kMaxCols = 64;
+
+struct EpiArgs {
+    int mode = EPI_STORE;
+    View Y;                 // STORE: output; RESIDUAL: R; POLY: prod_{i+1}
+    // RESIDUAL: R = A X - theta .* (B X); per-CTA partial sums of R^2 per column
+    const double* bdiag = nullptr;
+    double theta[kMaxCols];
+    double* partial = nullptr;   // [grid_main + n_long] x m
+    // POLY: prod_{i+1} = prod_i - inv_cur * A prod_i; H = (first ? inv_cur*prod_i : H) + inv_next*prod_{i+1}
+    View H;
+    double inv_cur = 0.0;
+    double inv_next = 0.0;
+    int first = 0;
+    int last_h_only = 0;     // unused (kept for ABI of the struct)
+};
+
+// Y-block SpMM with epilogue. X is the gathered block (rows = global columns of
+// A; on one GPU the same n), m columns. Returns the number of partial rows
+// written to ea.partial (for RESIDUAL), so the caller can reduce them.
+int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
+// Reduce partial[rows x m] over rows in fixed order into out[m] (device).
+void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s);
+
+// ---- tall-skinny block kernels (blockops.cu) ----
+// Gram: G = [L0 | L1 | L2]^T diag(b) Rt, with optional pre-transforms:
+//   UPDATE : W = V - [U0 | U1] * C   (C: (u0+u1) x k, column-major), Rt = W
+//   COMBINE: W = V * C  (C: kv x kw column-major), W split across W/W2 views
+struct TsSpec {
+    int64_t n = 0;
+    View U0, U1;            // basis ("against") views, cols may be 0
+    View V;                 // input block
+    View W, W2;             // outputs (W2 receives output columns >= W.cols for COMBINE)
+    const double* C = nullptr;  // device, column-major
+    int ldc = 0;                // leading dimension of C (0 = inner dimension)
+    const double* b = nullptr;  // B diagonal (device) or null
+    int transform = 0;      // 0 none, 1 update, 2 combine
+    // gram request: left = [U0?][U1?][V or W?], right = V or W (post-transform)
+    bool gram = false;
+    bool gram_left_u = false;   // include U0, U1 on the left
+    bool gram_left_self = true; // include the right block itself on the left
+};
+enum { TS_NONE = 0, TS_UPDATE = 1, TS_COMBINE = 2 };
+
+// Runs the tile kernel; if spec.gram, writes the (P x Q) column-major Gram to
+// gram_out (device) and returns P. Deterministic for a fixed n.
+int ts_run(const TsSpec& spec, double* gram_out, double* scratch, size_t scratch_elems,
+           cudaStream_t s);
+
+// Deterministic per-CTA column sums; returns the number of partial rows.
+int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s);
+
+// Elementwise helpers
+void scale_cols(View V, const double* colscale_dev, cudaStream_t s, int64_t n);  // V(:,j) *= s[j]
+void diag_apply(int64_t n, const double* d, View in, View out, cudaStream_t s);    // out = d .* in
+void copy_view(int64_t n, View in, View out, cudaStream_t s);
+void gather_cols(int64_t n, View in, const int* cols_host, int k, View out, cudaStream_t s);
+void fill_view(int64_t n, View v, double value, cudaStream_t s);
+// out = inv_diag_guarded .* in (Jacobi, preconditioners.cpp:44-68)
+void jacobi_apply(int64_t n, const double* inv_diag, View in, View out, cudaStream_t s);
+void poly_first_only(int64_t n, double inv0, View R, View H, cudaStream_t s);  // H = inv0 * R
+
+} // namespace spb

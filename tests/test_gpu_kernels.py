@@ -1,0 +1,203 @@
+"""GPU parity: kernel-level seams of the CUDA library vs the CPU reference.
+
+Bit-exact where the reference is (Laplacian assembly: laplacian_test.cpp:30-211;
+SpMM vs spmv_block_serial: kernels_test.cpp:26-35; initial blocks; MJ; cut /
+imbalance: graph_test.cpp:225-275), fp tolerance where it is not (Gram:
+kernels_test.cpp:37-48 allows 1e-13).
+"""
+import numpy as np
+import pytest
+
+from paper_2105_00578_b200 import DegenerateDegreeError, InfeasibleError, InvalidArgument
+from paper_2105_00578_b200 import generators as gen
+from paper_2105_00578_b200.api import Graph
+
+pytestmark = pytest.mark.gpu
+
+
+def _graphs():
+    yield "path3", gen.path(3)
+    yield "edge", gen.graph_from_edges(2, [(0, 1)])
+    yield "k3", gen.graph_from_edges(3, [(0, 1), (1, 2), (0, 2)])
+    yield "star", gen.graph_from_edges(4, [(0, 1), (0, 2), (0, 3)])
+    yield "ring8", gen.ring(8)
+    yield "grid20", gen.grid2d(20, 17)
+    yield "st7", gen.stencil3d(9, 8, 7, 7)
+    yield "st27", gen.stencil3d(6, 7, 5, 27)
+    for s in range(4):
+        yield f"rand{s}", gen.random_connected_graph(30 + 17 * s, 60 + 40 * s, seed=s)
+    # weighted costs: laplacian_test.cpp:173-211 style
+    g = gen.random_connected_graph(50, 120, seed=9)
+    rng = np.random.default_rng(3)
+    w = rng.uniform(0.5, 3.0, g.col_indices.shape[0])
+    # symmetric costs: w_ij = w_ji
+    n = g.n
+    rows = np.repeat(np.arange(n), np.diff(g.row_offsets))
+    key_lo = np.minimum(rows, g.col_indices) * n + np.maximum(rows, g.col_indices)
+    _, inv = np.unique(key_lo, return_inverse=True)
+    sym = rng.uniform(0.5, 3.0, inv.max() + 1)[inv]
+    yield "weighted", Graph(g.row_offsets, g.col_indices, sym, None)
+
+
+GRAPHS = list(_graphs())
+
+
+@pytest.mark.parametrize("kind", ["combinatorial", "normalized", "degree"])
+@pytest.mark.parametrize("name,g", GRAPHS, ids=[n for n, _ in GRAPHS])
+def test_laplacian_bit_exact(ctx, ref, kind, name, g):
+    a = ctx.build_laplacian(kind, g)
+    b = ref.build_laplacian(kind, g)
+    for key in ("row_offsets", "col_indices"):
+        assert np.array_equal(a[key], b[key]), key
+    assert a["values"].tobytes() == b["values"].tobytes()
+    assert a["diag"].tobytes() == b["diag"].tobytes()
+    assert a["spectral_bound"] == b["spectral_bound"]
+    assert a["is_diagonal"] == b["is_diagonal"]
+
+
+def test_laplacian_kats(ctx):
+    # laplacian_test.cpp:30-87
+    L = ctx.build_laplacian("combinatorial", gen.path(3))
+    dense = np.zeros((3, 3))
+    for i in range(3):
+        for k in range(L["row_offsets"][i], L["row_offsets"][i + 1]):
+            dense[i, L["col_indices"][k]] = L["values"][k]
+    assert np.array_equal(dense, [[1, -1, 0], [-1, 2, -1], [0, -1, 1]])
+    N = ctx.build_laplacian("normalized", gen.graph_from_edges(3, [(0, 1), (1, 2), (0, 2)]))
+    off = N["values"][N["col_indices"] != np.repeat(np.arange(3), 3)]
+    assert np.allclose(off, -0.5)
+    D = ctx.build_laplacian("degree", gen.graph_from_edges(4, [(0, 1), (0, 2), (0, 3)]))
+    assert list(D["diag"]) == [3, 1, 1, 1] and D["is_diagonal"]
+
+
+def test_normalized_rejects_isolated_vertex(ctx):
+    g = gen.graph_from_edges(3, [(0, 1)])
+    with pytest.raises(DegenerateDegreeError):
+        ctx.build_laplacian("normalized", g)
+
+
+@pytest.mark.parametrize("kind", ["combinatorial", "normalized", "degree"])
+@pytest.mark.parametrize("m", [1, 3, 5, 7, 9, 21, 27, 40])
+def test_spmm_bit_exact(ctx, ref, kind, m):
+    g = gen.stencil3d(9, 9, 9, 27)
+    rng = np.random.default_rng(m)
+    X = rng.uniform(-1, 1, (g.n, m))
+    assert ctx.spmm(kind, g, X).tobytes() == ref.spmm(kind, g, X).tobytes()
+
+
+@pytest.mark.parametrize("name,g", GRAPHS[-5:], ids=[n for n, _ in GRAPHS[-5:]])
+def test_spmm_bit_exact_irregular(ctx, ref, name, g):
+    X = np.random.default_rng(1).uniform(-1, 1, (g.n, 7))
+    for kind in ("combinatorial", "normalized"):
+        assert ctx.spmm(kind, g, X).tobytes() == ref.spmm(kind, g, X).tobytes()
+
+
+def test_spmm_csr_matches_spmv_block(ctx, ref):
+    L = ref.build_laplacian("combinatorial", gen.stencil3d(9, 9, 9, 27))
+    X = np.random.default_rng(2).uniform(-1, 1, (729, 5))
+    a = ctx.spmm_csr(L["row_offsets"], L["col_indices"], L["values"], X)
+    b = ref.spmm_csr(L["row_offsets"], L["col_indices"], L["values"], X)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_cut_identity_exact(ctx):
+    # acceptance c2 (acceptance.cpp:99-122): x^T L_C x / 4 == cutsize, exactly
+    for s in range(20):
+        g = gen.random_connected_graph(10 + s, 2 * (10 + s), seed=100 + s)
+        part = np.random.default_rng(s).integers(0, 2, g.n).astype(np.int32)
+        if part.min() == part.max():
+            part[0] = 1 - part[0]
+        x = np.where(part == 0, 1.0, -1.0)
+        Lx = ctx.spmm("combinatorial", g, x[:, None])[:, 0]
+        p = ctx.make_partition(g, part, 2)
+        assert float(x @ Lx) / 4.0 == p.cutsize
+
+
+def test_gram_matches_and_is_deterministic(ctx, ref):
+    rng = np.random.default_rng(3)
+    U = rng.uniform(-1, 1, (20000, 4))
+    V = rng.uniform(-1, 1, (20000, 3))
+    a = ctx.gram(U, V)
+    b = ctx.gram(U, V)
+    assert a.tobytes() == b.tobytes()
+    np.testing.assert_allclose(a, U.T @ V, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(a, ref.gram(U, V), rtol=1e-12, atol=1e-12)
+    d = rng.uniform(1, 5, 20000)
+    np.testing.assert_allclose(ctx.gram(U, V, d), U.T @ (d[:, None] * V), rtol=1e-12, atol=1e-11)
+
+
+@pytest.mark.parametrize("mu,mv", [(1, 1), (9, 9), (27, 27), (18, 9), (40, 5)])
+def test_gram_shapes(ctx, mu, mv):
+    rng = np.random.default_rng(mu * 100 + mv)
+    n = 5000 + mu
+    U, V = rng.standard_normal((n, mu)), rng.standard_normal((n, mv))
+    np.testing.assert_allclose(ctx.gram(U, V), U.T @ V, rtol=1e-11, atol=1e-10)
+
+
+@pytest.mark.parametrize("init,n,d,seed", [("random", 1000, 3, 42), ("random", 777, 7, 5), ("piecewise", 1001, 4, 0),
+                                           ("piecewise", 10, 9, 0)])
+def test_initial_guess_bit_identical(ctx, ref, init, n, d, seed):
+    assert ctx.initial_guess(init, n, d, seed).tobytes() == ref.initial_guess(init, n, d, seed).tobytes()
+
+
+def test_mj_identical_to_reference(ctx, ref):
+    rng = np.random.default_rng(15)
+    for trial in range(25):
+        n = int(rng.integers(1, 300))
+        k = int(rng.integers(1, n + 1))
+        dims = int(rng.integers(1, 5))
+        coords = rng.uniform(-1, 1, (n, dims))
+        a = ctx.mj_partition(coords, None, k)
+        b = ref.mj_partition(coords, None, k)
+        assert np.array_equal(a.assignment, b.assignment), (n, k, dims)
+        assert np.array_equal(a.part_weights, b.part_weights)
+
+
+def test_mj_ties_weights_and_zero_sign(ctx, ref):
+    # partitioner_test.cpp:213-236
+    assert list(ctx.mj_partition(np.ones((4, 1)), None, 2).assignment) == [0, 0, 1, 1]
+    p = ctx.mj_partition(np.array([[0.0], [1.0], [2.0], [3.0]]), [3.0, 1.0, 1.0, 1.0], 2)
+    assert list(p.assignment) == [0, 1, 1, 1]
+    # -0.0 == +0.0 ties break by id
+    c = np.array([[0.0], [-0.0], [0.0], [-0.0], [1.0], [-1.0]])
+    assert np.array_equal(ctx.mj_partition(c, None, 3).assignment, ref.mj_partition(c, None, 3).assignment)
+    rng = np.random.default_rng(4)
+    for trial in range(10):
+        n = 200
+        coords = np.round(rng.uniform(-1, 1, (n, 3)), 1)  # many ties
+        w = rng.uniform(0.1, 2.0, n)
+        for K in (2, 5, 8, 13):
+            a = ctx.mj_partition(coords, w, K)
+            b = ref.mj_partition(coords, w, K)
+            assert np.array_equal(a.assignment, b.assignment)
+    with pytest.raises(InfeasibleError):
+        ctx.mj_partition(np.array([[0.0], [1.0]]), None, 3)
+
+
+def test_mj_large_identical(ctx, ref):
+    rng = np.random.default_rng(7)
+    coords = rng.standard_normal((200000, 6))
+    for K in (64, 100):
+        a = ctx.mj_partition(coords, None, K)
+        b = ref.mj_partition(coords, None, K)
+        assert np.array_equal(a.assignment, b.assignment)
+
+
+def test_make_partition_exact(ctx, ref):
+    g = gen.stencil3d(12, 11, 10, 27)
+    rng = np.random.default_rng(8)
+    for K in (2, 7, 64):
+        a = rng.integers(0, K, g.n).astype(np.int32)
+        a[:K] = np.arange(K)
+        for doubled in (False, True):
+            p, q = ctx.make_partition(g, a, K, doubled), ref.make_partition(g, a, K, doubled)
+            assert p.cutsize == q.cutsize and p.imbalance == q.imbalance
+            assert np.array_equal(p.part_weights, q.part_weights)
+    # KATs: graph_test.cpp:225-255
+    tri = gen.graph_from_edges(3, [(0, 1), (1, 2), (0, 2)])
+    assert ctx.make_partition(tri, [0, 1, 1], 2).cutsize == 2.0
+    assert ctx.make_partition(tri, [0, 1, 1], 2, True).cutsize == 4.0
+    with pytest.raises(InvalidArgument):
+        ctx.make_partition(tri, [0, 0, 0], 2)  # empty part
+    with pytest.raises(InvalidArgument):
+        ctx.make_partition(tri, [0, 1, 2], 2)  # out of range
