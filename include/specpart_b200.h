@@ -172,6 +172,17 @@ sp_status sp_context_set_timing(sp_context* ctx, int on);
 sp_status sp_partition(sp_context* ctx, const sp_graph* g, const sp_config* cfg,
                        int32_t* assignment_out, sp_report* report, const double* x0_colmajor);
 
+/* ---- device-resident graphs ------------------------------------------------
+ * sp_graph_upload copies the graph arrays into HBM (no computation);
+ * sp_partition_resident then runs the whole pipeline of sp_partition on them
+ * (degree scan and assembly included) and leaves the assignment in HBM,
+ * optionally copying it to assignment_out (host, may be NULL). */
+typedef struct sp_device_graph sp_device_graph;
+sp_status sp_graph_upload(sp_context* ctx, const sp_graph* g, sp_device_graph** out);
+void sp_graph_free(sp_device_graph* dg);
+sp_status sp_partition_resident(sp_context* ctx, sp_device_graph* dg, const sp_config* cfg,
+                                int32_t* assignment_out, sp_report* report, const double* x0_colmajor);
+
 /* ---- kernel-level entry points (parity seams) ------------------------------ */
 
 /* Laplacian assembly (laplacian.cpp:53-144): writes the CSR of L (offsets n+1,

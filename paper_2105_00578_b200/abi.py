@@ -116,6 +116,9 @@ SIGNATURES = {
     "sp_last_error": (C.c_char_p, [P]),
     "sp_context_set_timing": (I32, [P, C.c_int]),
     "sp_partition": (I32, [P, C.POINTER(SpGraph), C.POINTER(SpConfig), P, C.POINTER(SpReport), P]),
+    "sp_graph_upload": (I32, [P, C.POINTER(SpGraph), C.POINTER(P)]),
+    "sp_graph_free": (None, [P]),
+    "sp_partition_resident": (I32, [P, P, C.POINTER(SpConfig), P, C.POINTER(SpReport), P]),
     "sp_build_laplacian": (I32, [P, I32, C.POINTER(SpGraph), P, P, P, P, C.POINTER(F64), C.POINTER(I32)]),
     "sp_spmm": (I32, [P, I32, C.POINTER(SpGraph), P, I32, P]),
     "sp_spmm_csr": (I32, [P, I64, I64, P, P, P, P, I32, P]),

@@ -271,6 +271,27 @@ class Context:
         part = Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance)
         return RunResult(part, report)
 
+    def upload(self, g: Graph) -> "DeviceGraph":
+        """Copies the graph arrays into HBM (sp_graph_upload)."""
+        h = C.c_void_p()
+        gc = g.as_c()
+        self._check(self.lib.sp_graph_upload(self._h, C.byref(gc), C.byref(h)))
+        return DeviceGraph(self, h, g.n)
+
+    def partition_resident(self, dg: "DeviceGraph", cfg: RunConfig, copy_assignment: bool = True,
+                           x0=None) -> RunResult:
+        """partition_graph on an HBM-resident graph (sp_partition_resident)."""
+        assignment = np.empty(dg.n, dtype=np.int32) if copy_assignment else None
+        pw = np.zeros(max(int(cfg.num_parts), 1), dtype=np.float64)
+        rep = abi.SpReport()
+        rep.part_weights = pw.ctypes.data_as(C.POINTER(C.c_double))
+        x0b = _colmajor(x0) if x0 is not None else None
+        cc = cfg.as_c()
+        self._check(self.lib.sp_partition_resident(self._h, dg.handle, C.byref(cc), _ptr(assignment),
+                                                   C.byref(rep), _ptr(x0b)))
+        report = report_from_c(rep, pw, None)
+        return RunResult(Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance), report)
+
     # laplacian.cpp:53-144 (explicit CSR, bit-exact)
     def build_laplacian(self, kind: str, g: Graph):
         k = abi.LAP[kind]
@@ -370,6 +391,22 @@ class Context:
         self._check(self.lib.sp_cut_imbalance(self._h, C.byref(gc), a.ctypes.data, num_parts,
                                               int(doubled_cut), C.byref(cut), C.byref(imb), pw.ctypes.data))
         return Partition(a, num_parts, pw, cut.value, imb.value)
+
+
+class DeviceGraph:
+    def __init__(self, ctx: Context, handle: C.c_void_p, n: int):
+        self.ctx, self.handle, self.n = ctx, handle, n
+
+    def free(self):
+        if self.handle:
+            self.ctx.lib.sp_graph_free(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 _default: dict[int, Context] = {}

@@ -16,6 +16,11 @@
 
 namespace spb {
 
+long long& launch_counter() {
+    thread_local long long c = 0;
+    return c;
+}
+
 int device_sm_count() {
     static int sms = [] {
         int dev = 0, v = 0;
@@ -41,8 +46,8 @@ template <class T> void h2d(T* dst, const T* src, size_t count, cudaStream_t s) 
     if (count) SPB_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
 }
 
-// Uploads the local row block of the caller's host graph.
-void upload_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
+// H2D of the local row block of the caller's host graph (no computation).
+void copy_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
     if (!hg || hg->n < 0 || (hg->n > 0 && (!hg->row_offsets || !hg->col_indices)))
         throw_invalid("graph: null arrays");
     Comm& cm = ctx->comm;
@@ -71,18 +76,52 @@ void upload_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
     } else {
         g.vals.release();
     }
-    g.unit_weights = true;
     if (hg->vertex_weights) {
-        bool unit = true;
-        for (int64_t i = 0; i < hg->n && unit; ++i) unit = hg->vertex_weights[i] == 1.0;
-        g.unit_weights = unit;
-        if (!unit) {
+        // MJ and the part tallies need every vertex's weight
+        g.vw_all.alloc(std::max<int64_t>(hg->n, 1));
+        h2d(g.vw_all.p, hg->vertex_weights, hg->n, s);
+    } else {
+        g.vw_all.release();
+    }
+    g.prepared = false;
+}
+
+__global__ void weight_flags_kernel(int64_t n, const double* w, int* flags) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = w[i];
+        if (v != 1.0) atomicOr(flags, 1);
+        if (!(v > 0.0)) atomicOr(flags, 2);
+    }
+}
+
+// Degrees, unit-cost / unit-weight detection, max degree; multi-GPU: global
+// max degree and all-vertex degrees.
+void prepare_graph(sp_context* ctx, DevGraph& g) {
+    if (g.prepared) return;
+    Comm& cm = ctx->comm;
+    cudaStream_t s = ctx->stream;
+    g.unit_weights = true;
+    g.positive_weights = true;
+    if (g.vw_all.p) {
+        DBuf<int> f(1);
+        SPB_CUDA(cudaMemsetAsync(f.p, 0, sizeof(int), s));
+        weight_flags_kernel<<<grid_for(g.n_global, 256, 8), 256, 0, s>>>(g.n_global, g.vw_all.p, f.p);
+        SPB_LAUNCH_CHECK();
+        int hf = 0;
+        SPB_CUDA(cudaMemcpyAsync(&hf, f.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        g.unit_weights = (hf & 1) == 0;
+        g.positive_weights = (hf & 2) == 0;
+        if (!g.unit_weights) {
             g.vw.alloc(std::max<int64_t>(g.n_local, 1));
-            h2d(g.vw.p, hg->vertex_weights + g.row0, g.n_local, s);
+            SPB_CUDA(cudaMemcpyAsync(g.vw.p, g.vw_all.p + g.row0, sizeof(double) * g.n_local,
+                                     cudaMemcpyDeviceToDevice, s));
         }
     }
     graph_degrees(g, s);
     g.max_degree_global = g.max_degree_local;
+    g.positive_degrees = g.positive_degrees_local;
     if (cm.active()) {
         DBuf<int64_t> t(cm.world), one(1);
         int64_t v = g.max_degree_local;
@@ -90,20 +129,27 @@ void upload_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
         SPB_NCCL(ncclAllGather(one.p, t.p, 1, ncclInt64, cm.nccl, s));
         std::vector<int64_t> h(cm.world);
         SPB_CUDA(cudaMemcpyAsync(h.data(), t.p, sizeof(int64_t) * cm.world, cudaMemcpyDeviceToHost, s));
-        int64_t unit_flag = g.unit_values ? 0 : 1;
-        h2d(one.p, &unit_flag, 1, s);
-        cm.sum_i64(one.p, 1, s);
-        SPB_CUDA(cudaMemcpyAsync(&unit_flag, one.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        int64_t flags[2] = {g.unit_values ? 0 : 1, g.positive_degrees_local ? 0 : 1};
+        DBuf<int64_t> fl(2);
+        h2d(fl.p, flags, 2, s);
+        cm.sum_i64(fl.p, 2, s);
+        SPB_CUDA(cudaMemcpyAsync(flags, fl.p, sizeof(flags), cudaMemcpyDeviceToHost, s));
         SPB_CUDA(cudaStreamSynchronize(s));
         g.max_degree_global = *std::max_element(h.begin(), h.end());
-        g.unit_values = unit_flag == 0;
-        // all-vertex degrees (isd of halo columns for L_N)
+        g.unit_values = flags[0] == 0;
+        g.positive_degrees = flags[1] == 0;
         DBuf<double> padded(cm.n_pad);
         SPB_CUDA(cudaMemsetAsync(padded.p, 0, sizeof(double) * cm.n_pad, s));
         SPB_CUDA(cudaMemcpyAsync(padded.p, g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToDevice, s));
         g.deg_all.alloc(static_cast<size_t>(cm.n_pad) * cm.world);
         cm.gather_f64(padded.p, g.deg_all.p, s);
     }
+    g.prepared = true;
+}
+
+void upload_graph(sp_context* ctx, const sp_graph* hg, DevGraph& g) {
+    copy_graph(ctx, hg, g);
+    prepare_graph(ctx, g);
 }
 
 struct GraphKindInfo {
@@ -201,6 +247,156 @@ View gather_block(sp_context* ctx, const View& local, int m, DBuf<double>& keep)
     return rowmajor(keep.p, m, m);
 }
 
+void validate_config(int64_t n, const sp_config* cfg) {
+    const int64_t K = cfg->num_parts;
+    if (K < 2) throw_infeasible("partition_graph: K must be >= 2");
+    if (K > n)
+        throw_infeasible("partition_graph: K exceeds vertex count (K=" + std::to_string(K) + ", n=" +
+                         std::to_string(n) + ")");
+    if (cfg->epsilon < 0.0) throw_infeasible("partition_graph: epsilon < 0");
+}
+
+// partition_graph (pipeline.cpp:47-167) on a graph whose arrays are on the
+// device. Writes all n part ids to asg (device) and fills the report.
+void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const double* x0, DBuf<int32_t>& asg,
+                    sp_report* rep, Clock::time_point t_total) {
+    cudaStream_t s = ctx->stream;
+    const int64_t K = cfg->num_parts;
+    const int64_t n = g.n_global;
+    ctx->timers = Timers{};
+    ctx->ev_used = 0;
+    ctx->comm.bytes_moved = 0;
+    const long long launches0 = launch_counter();
+    sp_report R{};
+    double* pw_out = rep ? rep->part_weights : nullptr;
+    sp_trace_record* tr_out = rep ? rep->trace : nullptr;
+    const int32_t tr_cap = rep ? rep->trace_capacity : 0;
+
+    // Stage 1: degrees, classification, operators (the copy, if any, is already queued)
+    const auto t_lap = Clock::now();
+    prepare_graph(ctx, g);
+    const GraphKindInfo kind = classify(g);
+    R.n = n;
+    R.edges = g.nnz_global / 2;
+    R.graph_regular = kind.regular;
+    R.max_degree = kind.max_degree;
+    R.avg_degree = kind.avg;
+    R.degree_ratio = kind.ratio;
+    R.num_parts = K;
+    R.seed = cfg->seed;
+    R.max_iters = cfg->max_iters;
+    R.epsilon = cfg->epsilon;
+    R.doubled_cut = cfg->doubled_cut;
+    // resolution order: classify -> precond -> (problem, tol) -> init (pipeline.cpp:66-82)
+    R.precond = cfg->precond == SP_PRECOND_AUTO ? (kind.regular ? SP_PRECOND_AMG : SP_PRECOND_POLYNOMIAL)
+                                                : cfg->precond;
+    if (R.precond == SP_PRECOND_AMG)
+        throw SpError(SP_ERROR, "AMG preconditioner is outside this build's hot path (SURVEY §8(f) rank 1); "
+                                "pass precond=jacobi or polynomial");
+    const auto [auto_problem, auto_tol] = select_defaults(kind.regular, R.precond);
+    R.problem = cfg->problem == SP_PROBLEM_AUTO ? auto_problem : cfg->problem;
+    R.tol = cfg->tol > 0.0 ? cfg->tol : auto_tol;
+    R.init = cfg->init == SP_INIT_AUTO ? (kind.regular ? SP_INIT_RANDOM : SP_INIT_PIECEWISE) : cfg->init;
+    R.eigenvectors = eigenvector_count(K);
+    const int d = R.eigenvectors;
+    if (d > n)
+        throw_infeasible("partition_graph: needs d=" + std::to_string(d) + " eigenvectors but n=" +
+                         std::to_string(n));
+    if (d > 32) throw_dimension("partition_graph: d > 32 eigenvectors is not supported");
+
+    DevLaplacian A;
+    build_laplacian(operator_kind(R.problem), g, false, A, s);
+    if (!kind.regular) collect_long_rows(g, A, 4096, s);
+    const double* bdiag = nullptr;
+    if (R.problem == SP_PROBLEM_GENERALIZED) {
+        // B = D must be positive (laplacian.cpp:169-173)
+        if (!g.positive_degrees) throw_degenerate("generalized problem requires positive degrees");
+        bdiag = g.deg.p;
+    }
+    SPB_CUDA(cudaStreamSynchronize(s));
+    R.laplacian_s = since(t_lap);
+
+    // Stage 2: preconditioner + eigensolve
+    const auto t_eig = Clock::now();
+    Solver solver(ctx, A.op, bdiag, d);
+    DBuf<double> inv;
+    if (R.precond == SP_PRECOND_JACOBI) {
+        inverse_diagonal(A, inv, s);
+        solver.set_jacobi(inv.p);
+    } else if (R.precond == SP_PRECOND_POLYNOMIAL) {
+        solver.build_poly(cfg->seed ^ 0x706f6c79ULL, 25);
+        R.poly_degree = static_cast<int32_t>(solver.roots().size());
+    } else {
+        solver.set_none();
+    }
+    const int64_t nloc = g.n_local;
+    DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
+    const View X = rowmajor(Xb.p, d, d);
+    if (x0) upload_block(x0, n, g.row0, nloc, d, X, s);
+    else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X, s);
+    else initial_block_piecewise(n, d, g.row0, nloc, X, s);
+    SolveOpts so;
+    so.nev = d;
+    so.tol = R.tol;
+    so.max_iters = cfg->max_iters;
+    so.record_trace = cfg->record_trace != 0;
+    SolveResult er = solver.lobpcg(X, so, X);
+    SPB_CUDA(cudaStreamSynchronize(s));
+    R.eigensolve_s = since(t_eig);
+    R.iterations = er.iterations;
+    R.breakdown_retries = er.retries;
+    for (int j = 0; j < d; ++j) {
+        R.theta[j] = er.theta[j];
+        R.residual_norms[j] = er.residual_norms[j];
+        R.converged[j] = er.converged[j];
+    }
+    if (er.retries > 0) R.warnings |= SP_WARN_BREAKDOWN_RECOVERED;
+    if (!er.all_converged()) R.warnings |= SP_WARN_UNCONVERGED;
+
+    // Stage 3: embed (drop column 0) + multi-jagged on the whole embedding
+    const auto t_mj = Clock::now();
+    DBuf<double> Xall;
+    const View Xg = gather_block(ctx, X, d, Xall);
+    asg.alloc(static_cast<size_t>(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : n, 1)));
+    if (!g.positive_weights) throw_infeasible("mj_partition: weights must be positive");
+    mj_partition_dev(n, d - 1, Xg.sub(1, d - 1), g.vw_all.p, g.unit_weights, K, asg.p, s);
+    R.partition_s = since(t_mj);
+
+    // metrics (make_partition, graph.cpp:209-230)
+    PartitionMetrics pm = make_partition_dev(ctx, g, asg.p, K, cfg->doubled_cut != 0);
+    R.cutsize = pm.cut;
+    R.imbalance = pm.imbalance;
+    if (R.imbalance > 1.0 + cfg->epsilon) R.warnings |= SP_WARN_IMBALANCE;
+    SPB_CUDA(cudaStreamSynchronize(s));
+    ctx->collect_spmm_times();
+    R.total_s = since(t_total);
+    R.spmm_launches = ctx->timers.spmm_launches;
+    R.spmm_bytes = ctx->timers.spmm_bytes;
+    R.spmm_ms = ctx->timers.spmm_ms;
+    R.kernel_launches = static_cast<int32_t>(launch_counter() - launches0 + ctx->timers.kernel_launches);
+    R.n_gpus = ctx->comm.world;
+    if (rep) {
+        R.part_weights = pw_out;
+        R.trace = tr_out;
+        R.trace_capacity = tr_cap;
+        if (pw_out) std::memcpy(pw_out, pm.part_weights.data(), sizeof(double) * K);
+        if (tr_out) {
+            int k = 0;
+            for (const TraceRec& t : er.trace) {
+                if (k >= tr_cap) break;
+                tr_out[k].iter = t.iter;
+                tr_out[k].ntheta = static_cast<int32_t>(t.theta.size());
+                tr_out[k].min_residual = t.min_residual;
+                tr_out[k].max_residual = t.max_residual;
+                for (size_t j = 0; j < t.theta.size() && j < SP_MAX_EIG; ++j) tr_out[k].theta[j] = t.theta[j];
+                ++k;
+            }
+            R.trace_len = k;
+        }
+        *rep = R;
+    }
+}
+
 } // namespace
 
 } // namespace spb
@@ -280,160 +476,51 @@ sp_status sp_context_set_timing(sp_context* c, int on) {
 sp_status sp_partition(sp_context* ctx, const sp_graph* hg, const sp_config* cfg, int32_t* assignment_out,
                        sp_report* rep, const double* x0) {
     return guarded(ctx, [&] {
-        if (!cfg || !assignment_out) throw_invalid("sp_partition: null argument");
-        const int64_t K = cfg->num_parts;
-        if (K < 2) throw_infeasible("partition_graph: K must be >= 2");
-        if (K > hg->n)
-            throw_infeasible("partition_graph: K exceeds vertex count (K=" + std::to_string(K) +
-                             ", n=" + std::to_string(hg->n) + ")");
-        if (cfg->epsilon < 0.0) throw_infeasible("partition_graph: epsilon < 0");
+        if (!cfg || !assignment_out || !hg) throw_invalid("sp_partition: null argument");
+        validate_config(hg->n, cfg);
         const auto t_total = Clock::now();
-        cudaStream_t s = ctx->stream;
-        ctx->timers = Timers{};
-        ctx->comm.bytes_moved = 0;
-
-        sp_report R{};
-        double* pw_out = rep ? rep->part_weights : nullptr;
-        sp_trace_record* tr_out = rep ? rep->trace : nullptr;
-        const int32_t tr_cap = rep ? rep->trace_capacity : 0;
-
-        // Stage 1: graph upload + operators
-        const auto t_lap = Clock::now();
         DevGraph g;
-        upload_graph(ctx, hg, g);
-        const GraphKindInfo kind = classify(g);
-        R.n = hg->n;
-        R.edges = g.nnz_global / 2;
-        R.graph_regular = kind.regular;
-        R.max_degree = kind.max_degree;
-        R.avg_degree = kind.avg;
-        R.degree_ratio = kind.ratio;
-        R.num_parts = K;
-        R.seed = cfg->seed;
-        R.max_iters = cfg->max_iters;
-        R.epsilon = cfg->epsilon;
-        R.doubled_cut = cfg->doubled_cut;
-        // resolution order: classify -> precond -> (problem, tol) -> init (pipeline.cpp:66-82)
-        R.precond = cfg->precond == SP_PRECOND_AUTO ? (kind.regular ? SP_PRECOND_AMG : SP_PRECOND_POLYNOMIAL)
-                                                    : cfg->precond;
-        if (R.precond == SP_PRECOND_AMG)
-            throw SpError(SP_ERROR, "AMG preconditioner is outside this build's hot path (SURVEY §8(f) rank 1); "
-                                    "pass precond=jacobi or polynomial");
-        const auto [auto_problem, auto_tol] = select_defaults(kind.regular, R.precond);
-        R.problem = cfg->problem == SP_PROBLEM_AUTO ? auto_problem : cfg->problem;
-        R.tol = cfg->tol > 0.0 ? cfg->tol : auto_tol;
-        R.init = cfg->init == SP_INIT_AUTO ? (kind.regular ? SP_INIT_RANDOM : SP_INIT_PIECEWISE) : cfg->init;
-        R.eigenvectors = eigenvector_count(K);
-        const int d = R.eigenvectors;
-        if (d > hg->n)
-            throw_infeasible("partition_graph: needs d=" + std::to_string(d) + " eigenvectors but n=" +
-                             std::to_string(hg->n));
-        if (d > 32) throw_dimension("partition_graph: d > 32 eigenvectors is not supported");
+        copy_graph(ctx, hg, g);
+        DBuf<int32_t> asg;
+        partition_core(ctx, g, cfg, x0, asg, rep, t_total);
+        SPB_CUDA(cudaMemcpyAsync(assignment_out, asg.p, sizeof(int32_t) * hg->n, cudaMemcpyDeviceToHost, ctx->stream));
+        SPB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (rep) rep->total_s = since(t_total);
+    });
+}
 
-        DevLaplacian A;
-        build_laplacian(operator_kind(R.problem), g, false, A, s);
-        if (!kind.regular) collect_long_rows(g, A, 4096, s);
-        const double* bdiag = nullptr;
-        if (R.problem == SP_PROBLEM_GENERALIZED) {
-            // B = D must be positive (laplacian.cpp:169-173); degrees are integers >= 0 for unit costs
-            std::vector<double> hd(g.n_local);
-            if (g.n_local) SPB_CUDA(cudaMemcpyAsync(hd.data(), g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToHost, s));
-            SPB_CUDA(cudaStreamSynchronize(s));
-            for (double v : hd)
-                if (!(v > 0.0)) throw_degenerate("generalized problem requires positive degrees");
-            bdiag = g.deg.p;
-        }
-        SPB_CUDA(cudaStreamSynchronize(s));
-        R.laplacian_s = since(t_lap);
+sp_status sp_graph_upload(sp_context* ctx, const sp_graph* hg, sp_device_graph** out) {
+    return guarded(ctx, [&] {
+        if (!out) throw_invalid("sp_graph_upload: null out");
+        *out = nullptr;
+        auto h = std::make_unique<sp_device_graph>();
+        h->ctx = ctx;
+        copy_graph(ctx, hg, h->g);
+        SPB_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = h.release();
+    });
+}
 
-        // Stage 2: preconditioner + eigensolve
-        const auto t_eig = Clock::now();
-        Solver solver(ctx, A.op, bdiag, d);
-        DBuf<double> inv;
-        if (R.precond == SP_PRECOND_JACOBI) {
-            inverse_diagonal(A, inv, s);
-            solver.set_jacobi(inv.p);
-        } else if (R.precond == SP_PRECOND_POLYNOMIAL) {
-            solver.build_poly(cfg->seed ^ 0x706f6c79ULL, 25);
-            R.poly_degree = static_cast<int32_t>(solver.roots().size());
-        } else {
-            solver.set_none();
-        }
-        const int64_t nloc = g.n_local;
-        DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
-        const View X = rowmajor(Xb.p, d, d);
-        if (x0) upload_block(x0, hg->n, g.row0, nloc, d, X, s);
-        else if (R.init == SP_INIT_RANDOM) initial_block_random(hg->n, d, cfg->seed, g.row0, nloc, X, s);
-        else initial_block_piecewise(hg->n, d, g.row0, nloc, X, s);
-        SolveOpts so;
-        so.nev = d;
-        so.tol = R.tol;
-        so.max_iters = cfg->max_iters;
-        so.record_trace = cfg->record_trace != 0;
-        SolveResult er = solver.lobpcg(X, so, X);
-        SPB_CUDA(cudaStreamSynchronize(s));
-        R.eigensolve_s = since(t_eig);
-        R.iterations = er.iterations;
-        R.breakdown_retries = er.retries;
-        for (int j = 0; j < d; ++j) {
-            R.theta[j] = er.theta[j];
-            R.residual_norms[j] = er.residual_norms[j];
-            R.converged[j] = er.converged[j];
-        }
-        if (er.retries > 0) R.warnings |= SP_WARN_BREAKDOWN_RECOVERED;
-        if (!er.all_converged()) R.warnings |= SP_WARN_UNCONVERGED;
+void sp_graph_free(sp_device_graph* h) {
+    if (!h) return;
+    cudaSetDevice(h->ctx->device);
+    delete h;
+}
 
-        // Stage 3: embed (drop column 0) + multi-jagged
-        const auto t_mj = Clock::now();
-        DBuf<double> Xall;
-        const View Xg = gather_block(ctx, X, d, Xall);
-        DBuf<int32_t> asg(static_cast<size_t>(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : hg->n, 1)));
-        DBuf<double> wall;
-        const double* wdev = nullptr;
-        if (!g.unit_weights) {
-            wall.alloc(hg->n);
-            h2d(wall.p, hg->vertex_weights, hg->n, s);
-            wdev = wall.p;
-            for (int64_t i = 0; i < hg->n; ++i)
-                if (!(hg->vertex_weights[i] > 0.0)) throw_infeasible("mj_partition: weights must be positive");
+sp_status sp_partition_resident(sp_context* ctx, sp_device_graph* h, const sp_config* cfg,
+                                int32_t* assignment_out, sp_report* rep, const double* x0) {
+    return guarded(ctx, [&] {
+        if (!h || !cfg) throw_invalid("sp_partition_resident: null argument");
+        validate_config(h->g.n_global, cfg);
+        const auto t_total = Clock::now();
+        h->g.prepared = false;  // degree scan etc. belong to the timed pipeline
+        partition_core(ctx, h->g, cfg, x0, h->assignment, rep, t_total);
+        if (assignment_out) {
+            SPB_CUDA(cudaMemcpyAsync(assignment_out, h->assignment.p, sizeof(int32_t) * h->g.n_global,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+            SPB_CUDA(cudaStreamSynchronize(ctx->stream));
         }
-        mj_partition_dev(hg->n, d - 1, Xg.sub(1, d - 1), wdev, g.unit_weights, K, asg.p, s);
-        R.partition_s = since(t_mj);
-
-        // metrics (make_partition, graph.cpp:209-230)
-        PartitionMetrics pm = make_partition_dev(ctx, g, asg.p, K, cfg->doubled_cut != 0);
-        R.cutsize = pm.cut;
-        R.imbalance = pm.imbalance;
-        if (R.imbalance > 1.0 + cfg->epsilon) R.warnings |= SP_WARN_IMBALANCE;
-        SPB_CUDA(cudaMemcpyAsync(assignment_out, asg.p, sizeof(int32_t) * hg->n, cudaMemcpyDeviceToHost, s));
-        SPB_CUDA(cudaStreamSynchronize(s));
-        R.total_s = since(t_total);
-
-        R.spmm_launches = ctx->timers.spmm_launches;
-        R.spmm_bytes = ctx->timers.spmm_bytes;
-        R.spmm_ms = ctx->timers.spmm_ms;
-        R.kernel_launches = static_cast<int32_t>(ctx->timers.kernel_launches);
-        R.n_gpus = ctx->comm.world;
-        if (rep) {
-            R.part_weights = pw_out;
-            R.trace = tr_out;
-            R.trace_capacity = tr_cap;
-            if (pw_out) std::memcpy(pw_out, pm.part_weights.data(), sizeof(double) * K);
-            if (tr_out) {
-                int k = 0;
-                for (const TraceRec& t : er.trace) {
-                    if (k >= tr_cap) break;
-                    tr_out[k].iter = t.iter;
-                    tr_out[k].ntheta = static_cast<int32_t>(t.theta.size());
-                    tr_out[k].min_residual = t.min_residual;
-                    tr_out[k].max_residual = t.max_residual;
-                    for (size_t j = 0; j < t.theta.size() && j < SP_MAX_EIG; ++j) tr_out[k].theta[j] = t.theta[j];
-                    ++k;
-                }
-                R.trace_len = k;
-            }
-            *rep = R;
-        }
+        if (rep) rep->total_s = since(t_total);
     });
 }
 
@@ -569,11 +656,7 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
         build_laplacian(operator_kind(problem), g, false, A, s);
         const double* bdiag = nullptr;
         if (problem == SP_PROBLEM_GENERALIZED) {
-            std::vector<double> hd(g.n_local);
-            if (g.n_local) SPB_CUDA(cudaMemcpyAsync(hd.data(), g.deg.p, sizeof(double) * g.n_local, cudaMemcpyDeviceToHost, s));
-            SPB_CUDA(cudaStreamSynchronize(s));
-            for (double v : hd)
-                if (!(v > 0.0)) throw_degenerate("generalized problem requires positive degrees");
+            if (!g.positive_degrees) throw_degenerate("generalized problem requires positive degrees");
             bdiag = g.deg.p;
         }
         Solver solver(ctx, A.op, bdiag, nev);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -36,7 +37,14 @@ inline void throw_invalid(const std::string& m) { throw SpError(7, m); }
                                         __FILE__ + ":" + std::to_string(__LINE__));          \
     } while (0)
 
-#define SPB_LAUNCH_CHECK() SPB_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by SPB_LAUNCH_CHECK, which
+// also counts it (reported as gpu_launches).
+long long& launch_counter();
+#define SPB_LAUNCH_CHECK()                      \
+    do {                                        \
+        ++::spb::launch_counter();              \
+        SPB_CUDA(cudaGetLastError());           \
+    } while (0)
 
 // ---- device buffers ----
 template <class T> struct DBuf {

@@ -7,6 +7,8 @@
 #include <nccl.h>
 
 #include <string>
+#include <utility>
+#include <vector>
 
 namespace spb {
 
@@ -73,4 +75,34 @@ struct sp_context {
     spb::Timers timers;
     bool time_spmm = false;   // record CUDA events around every SpMM (bench/diagnostics)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // event pairs recorded around SpMM launches; resolved without extra syncs
+    // once the pipeline has synchronized (collect_spmm_times)
+    std::vector<cudaEvent_t> evpool;
+    size_t ev_used = 0;
+
+    std::pair<cudaEvent_t, cudaEvent_t> next_event_pair() {
+        while (evpool.size() < ev_used + 2) {
+            cudaEvent_t e;
+            SPB_CUDA(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        auto p = std::make_pair(evpool[ev_used], evpool[ev_used + 1]);
+        ev_used += 2;
+        return p;
+    }
+    // after a stream sync: accumulate recorded pairs into timers.spmm_ms
+    void collect_spmm_times() {
+        for (size_t i = 0; i + 1 < ev_used; i += 2) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, evpool[i], evpool[i + 1]) == cudaSuccess) timers.spmm_ms += ms;
+        }
+        ev_used = 0;
+    }
+};
+
+// Device-resident graph handle (sp_graph_upload)
+struct sp_device_graph {
+    sp_context* ctx = nullptr;
+    spb::DevGraph g;
+    spb::DBuf<int32_t> assignment;  // last partition result (device)
 };

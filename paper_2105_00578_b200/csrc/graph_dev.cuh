@@ -22,10 +22,15 @@ struct DevGraph {
     DBuf<int32_t> cols;   // nnz_local
     DBuf<double> vals;    // nnz_local, empty = unit costs
     DBuf<double> vw;      // n_local vertex weights, empty = unit
+    DBuf<double> vw_all;  // n_global vertex weights as given (empty = unit)
     DBuf<double> deg;     // n_local weighted degrees (Graph::weighted_degree)
     DBuf<double> deg_all; // n_global degrees (multi-GPU); empty on one GPU
     bool unit_values = true;
     bool unit_weights = true;
+    bool positive_weights = true;
+    bool prepared = false;
+    bool positive_degrees_local = true;
+    bool positive_degrees = true;   // all vertices (the generalized problem needs B = D > 0)
     int64_t max_degree_local = 0;
     int64_t max_degree_global = 0;
 

@@ -23,6 +23,7 @@ __global__ void degree_kernel(int64_t n, const int64_t* offs, const double* vals
         const int64_t k0 = offs[i], k1 = offs[i + 1];
         if (!vals) {
             deg[i] = static_cast<double>(k1 - k0);  // sum of 1.0s is exact
+            if (k1 == k0) atomicOr(nonunit, 2);
             continue;
         }
         double s = 0.0;
@@ -34,6 +35,7 @@ __global__ void degree_kernel(int64_t n, const int64_t* offs, const double* vals
         }
         deg[i] = s;
         if (!unit) atomicOr(nonunit, 1);
+        if (!(s > 0.0)) atomicOr(nonunit, 2);
     }
 }
 
@@ -189,7 +191,8 @@ void graph_degrees(DevGraph& g, cudaStream_t s) {
     SPB_CUDA(cudaMemcpyAsync(&nonunit, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     SPB_CUDA(cudaMemcpyAsync(&maxdeg, md.p, sizeof(maxdeg), cudaMemcpyDeviceToHost, s));
     SPB_CUDA(cudaStreamSynchronize(s));
-    g.unit_values = (g.vals.p == nullptr) || nonunit == 0;
+    g.unit_values = (g.vals.p == nullptr) || (nonunit & 1) == 0;
+    g.positive_degrees_local = (nonunit & 2) == 0;
     g.max_degree_local = static_cast<int64_t>(maxdeg);
 }
 

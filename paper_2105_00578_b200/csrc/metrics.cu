@@ -137,6 +137,7 @@ PartitionMetrics make_partition_dev(sp_context* ctx, const DevGraph& g, const in
             SPB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, a_local, kout.p, vin.p, vout.p, n, 0, 32, s));
             DBuf<char> tmp(need);
             SPB_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, need, a_local, kout.p, vin.p, vout.p, n, 0, 32, s));
+            launch_counter() += 6;
             part_sum_kernel<<<ceil_div(K, 128), 128, 0, s>>>(n, kout.p, vout.p, g.vw.p, K, pw.p);
             SPB_LAUNCH_CHECK();
         }

@@ -213,6 +213,7 @@ void mj_partition_dev(int64_t n, int dims, const View& coords, const double* wei
         }
         SPB_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, need, kin.p, kout.p, n, MjDecomposer{}, 0,
                                                 end_bit, s));
+        launch_counter() += (end_bit + 7) / 8 + 2;  // CUB onesweep: histogram + one pass per digit
         keys_to_ids_kernel<<<g1(n), 256, 0, s>>>(n, kout.p, ids.p);
         SPB_LAUNCH_CHECK();
 

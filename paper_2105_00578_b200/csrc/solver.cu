@@ -62,7 +62,7 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
     cmat_.alloc(static_cast<size_t>(m3) * m3 + 64);
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
-    partial_.alloc(static_cast<size_t>(device_sm_count()) * 8 * 64 + (1u << 20) * 0 + 65536 * 64);
+    partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 + A.n_long + 64) * 64);
     norms_.alloc(64);
     R_.alloc(rows * max_cols);
     H_.alloc(rows * max_cols);
@@ -88,7 +88,6 @@ void Solver::gram_dev(const TsSpec& spec, int& P, int& Q) {
     Q = rq;
     if (n_ <= 0) SPB_CUDA(cudaMemsetAsync(gram_.p, 0, sizeof(double) * P * Q, s_));
     ctx_->comm.sum_small(gram_.p, P * Q, s_);
-    ctx_->timers.kernel_launches += 2;
 }
 
 std::vector<double> Solver::gram_to_host(const TsSpec& spec, int& P, int& Q) {
@@ -103,17 +102,14 @@ std::vector<double> Solver::gram_to_host(const TsSpec& spec, int& P, int& Q) {
 void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     const View Xg = ctx_->comm.gather_rows(Xlocal, m, s_);
     const bool timed = ctx_->time_spmm;
-    if (timed) SPB_CUDA(cudaEventRecord(ctx_->ev0, s_));
-    const int rows = spmm_launch(A_, Xg, m, ea, s_);
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
     if (timed) {
-        SPB_CUDA(cudaEventRecord(ctx_->ev1, s_));
-        SPB_CUDA(cudaEventSynchronize(ctx_->ev1));
-        float ms = 0.f;
-        SPB_CUDA(cudaEventElapsedTime(&ms, ctx_->ev0, ctx_->ev1));
-        ctx_->timers.spmm_ms += ms;
+        ev = ctx_->next_event_pair();
+        SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
+    const int rows = spmm_launch(A_, Xg, m, ea, s_);
+    if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;
-    ctx_->timers.kernel_launches += 1 + (A_.n_long > 0 ? 1 : 0);
     // algorithmic bytes of this launch: index stream,
     // offsets, X read once per referenced row, Y written once, epilogue blocks
     const double idx_b = A_.mode == OP_EXPLICIT ? 12.0 : (A_.mode == OP_DIAGONAL ? 0.0 : 4.0);
@@ -135,10 +131,6 @@ void Solver::spmm_store(const View& X, int m, const View& Y) {
     EpiArgs ea;
     ea.mode = EPI_STORE;
     ea.Y = Y;
-    for (int c0 = 0; c0 < m; c0 += 64) {
-        // the gather handles all columns; the kernel chunks columns internally
-        (void)c0;
-    }
     spmm(X, m, ea);
 }
 
@@ -572,7 +564,6 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         cb.transform = TS_COMBINE;
         cb.n = n_;
         ts_run(cb, nullptr, scratch_.p, scratch_.n, s_);
-        ctx_->timers.kernel_launches += 1;
     };
     auto record = [&](int it) {
         if (!o.record_trace) return;
