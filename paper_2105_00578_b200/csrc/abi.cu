@@ -267,6 +267,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     ctx->ev_used = 0;
     ctx->comm.bytes_moved = 0;
     const long long launches0 = launch_counter();
+    ctx->prof.on = std::getenv("SPB_PROFILE") != nullptr;
+    ctx->prof.start(s);
     sp_report R{};
     double* pw_out = rep ? rep->part_weights : nullptr;
     sp_trace_record* tr_out = rep ? rep->trace : nullptr;
@@ -315,6 +317,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     }
     SPB_CUDA(cudaStreamSynchronize(s));
     R.laplacian_s = since(t_lap);
+    ctx->prof.mark(s, "laplacian");
 
     // Stage 2: preconditioner + eigensolve
     const auto t_eig = Clock::now();
@@ -329,12 +332,14 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     } else {
         solver.set_none();
     }
+    ctx->prof.mark(s, "precond_build");
     const int64_t nloc = g.n_local;
     DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
     const View X = rowmajor(Xb.p, d, d);
     if (x0) upload_block(x0, n, g.row0, nloc, d, X, s);
     else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X, s);
     else initial_block_piecewise(n, d, g.row0, nloc, X, s);
+    ctx->prof.mark(s, "initial_block");
     SolveOpts so;
     so.nev = d;
     so.tol = R.tol;
@@ -361,6 +366,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     if (!g.positive_weights) throw_infeasible("mj_partition: weights must be positive");
     mj_partition_dev(n, d - 1, Xg.sub(1, d - 1), g.vw_all.p, g.unit_weights, K, asg.p, s);
     R.partition_s = since(t_mj);
+    ctx->prof.mark(s, "mj");
 
     // metrics (make_partition, graph.cpp:209-230)
     PartitionMetrics pm = make_partition_dev(ctx, g, asg.p, K, cfg->doubled_cut != 0);
@@ -368,6 +374,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     R.imbalance = pm.imbalance;
     if (R.imbalance > 1.0 + cfg->epsilon) R.warnings |= SP_WARN_IMBALANCE;
     SPB_CUDA(cudaStreamSynchronize(s));
+    ctx->prof.mark(s, "metrics");
+    ctx->prof.dump("partition_core");
     ctx->collect_spmm_times();
     R.total_s = since(t_total);
     R.spmm_launches = ctx->timers.spmm_launches;

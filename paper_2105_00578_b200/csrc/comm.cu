@@ -8,6 +8,9 @@
 // and run to run at a fixed GPU count.
 #include "context.hpp"
 
+#include <chrono>
+#include <cstdio>
+
 namespace spb {
 
 namespace {
@@ -39,6 +42,36 @@ __global__ void ordered_sum_i64_kernel(const int64_t* parts, int world, int coun
 }
 
 } // namespace
+
+double PhaseProf::now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void PhaseProf::start(cudaStream_t s) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    acc.clear();
+    last = now();
+}
+void PhaseProf::mark(cudaStream_t s, const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double t = now();
+    for (auto& kv : acc)
+        if (kv.first == name) {
+            kv.second += t - last;
+            last = t;
+            return;
+        }
+    acc.emplace_back(name, t - last);
+    last = t;
+}
+void PhaseProf::dump(const char* title) {
+    if (!on) return;
+    double tot = 0.0;
+    for (auto& kv : acc) tot += kv.second;
+    std::fprintf(stderr, "[spb-profile] %s total %.3f ms\n", title, tot * 1e3);
+    for (auto& kv : acc) std::fprintf(stderr, "[spb-profile]   %-22s %9.3f ms\n", kv.first.c_str(), kv.second * 1e3);
+}
 
 View Comm::gather_rows(const View& local, int m, cudaStream_t s) {
     if (!active()) return local;

@@ -58,6 +58,18 @@ struct Comm {
     void gather_f64(const double* local, double* global, cudaStream_t s);
 };
 
+// Phase profiler (SPB_PROFILE=1): stream-synchronizes at every mark and
+// accumulates host wall time per phase name; printed to stderr per partition.
+struct PhaseProf {
+    bool on = false;
+    std::vector<std::pair<std::string, double>> acc;
+    double last = 0.0;
+    static double now();
+    void start(cudaStream_t s);
+    void mark(cudaStream_t s, const char* name);
+    void dump(const char* title);
+};
+
 struct Timers {
     double spmm_ms = 0.0;
     int64_t spmm_launches = 0;
@@ -79,6 +91,7 @@ struct sp_context {
     // once the pipeline has synchronized (collect_spmm_times)
     std::vector<cudaEvent_t> evpool;
     size_t ev_used = 0;
+    spb::PhaseProf prof;
 
     std::pair<cudaEvent_t, cudaEvent_t> next_event_pair() {
         while (evpool.size() < ev_used + 2) {

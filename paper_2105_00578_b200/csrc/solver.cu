@@ -535,6 +535,7 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         ea.mode = EPI_STORE;
         ea.Y = AS.sub(0, m);
         spmm(S.sub(0, m), m, ea);
+        ctx_->prof.mark(s_, "rr_spmm");
         TsSpec g;
         g.U0 = S.sub(0, m);
         g.V = AS.sub(0, m);
@@ -611,7 +612,9 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
             RI = rowmajor(work_.p, na, na);
         }
         const View HI = rowmajor(H_.p, na, na);
+        ctx_->prof.mark(s_, "lobpcg_misc");
         apply_precond(RI, na, HI);
+        ctx_->prof.mark(s_, "precond_apply");
 
         int nx = 0, nh = 0, np = 0;
         for (;;) {
@@ -638,10 +641,14 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         }
         const int m = nx + nh + np;
         const int hp = nx;
+        ctx_->prof.mark(s_, "orth");
         std::vector<double> Y;
         projected_eig(m, theta, Y);
+        ctx_->prof.mark(s_, "rayleigh_ritz");
         combine_into(S, m, Y, nev, Xv);
+        ctx_->prof.mark(s_, "combine");
         residuals(Xv, theta, res, thr);
+        ctx_->prof.mark(s_, "residual");
 
         std::vector<int> next;
         for (int j = 0; j < nev; ++j)
@@ -658,6 +665,7 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         } else {
             p_cols = 0;
         }
+        ctx_->prof.mark(s_, "combine");
         record(iter);
     }
     (void)Pv;
