@@ -16,11 +16,13 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "obj"
+GEN = ROOT / "build" / "gen"
+TOOLS = PKG / "tools"
 LIB = PKG / "libspecpart_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
-          "-I", str(ROOT / "include"), "-I", str(CSRC), "--expt-relaxed-constexpr"]
+          "-I", str(ROOT / "include"), "-I", str(CSRC), "-I", str(GEN), "--expt-relaxed-constexpr"]
 
 
 def _sources():
@@ -47,9 +49,25 @@ def _compile(src: Path, hdr_mtime: float, verbose: bool) -> Path:
     return obj
 
 
+def _gen_tables(verbose: bool) -> None:
+    """MT19937-64 jump polynomials (tools/mt_jump_gen.cpp) -> build/gen/mt_jump_table.inc."""
+    GEN.mkdir(parents=True, exist_ok=True)
+    inc = GEN / "mt_jump_table.inc"
+    src = TOOLS / "mt_jump_gen.cpp"
+    if inc.exists() and inc.stat().st_mtime >= src.stat().st_mtime:
+        return
+    exe = GEN / "mt_jump_gen"
+    subprocess.run(["g++", "-O2", "-std=c++20", "-o", str(exe), str(src)], check=True)
+    # chunk of 2^18 draws, jumps for chunk indices < 2^16 (17 G draws)
+    subprocess.run([str(exe), str(inc), "18", "16"], check=True)
+    if verbose:
+        print(f"generated {inc}")
+
+
 def build(verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
-    hm = _headers_mtime()
+    _gen_tables(verbose)
+    hm = max(_headers_mtime(), (GEN / "mt_jump_table.inc").stat().st_mtime)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, hm, verbose), srcs))

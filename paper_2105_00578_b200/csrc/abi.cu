@@ -599,6 +599,9 @@ sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64
         op.cols = c.p;
         op.vals = v.p;
         op.long_threshold = int64_t(1) << 40;
+        int64_t mr = 0;
+        for (int64_t i = 0; i < nrows; ++i) mr = std::max(mr, offsets[i + 1] - offsets[i]);
+        op.max_row = static_cast<int>(std::min<int64_t>(mr, 1 << 30));
         DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(ncols, 1)) * m), yd(static_cast<size_t>(std::max<int64_t>(nrows, 1)) * m);
         upload_block(X, ncols, 0, ncols, m, rowmajor(xd.p, m, m), s);
         EpiArgs ea;

@@ -36,17 +36,30 @@ struct TsDev {
     double* partial;
 };
 
-__device__ __forceinline__ void load_tile(double* dst, const View& v, int64_t r0, int rows, int cols) {
+constexpr int kStages = 3;
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// cp.async copy of rows [r0, r0+rows) x cols of view v into dst[r*ld + c0 + c]
+__device__ __forceinline__ void issue_view(double* dst, int ld, int c0, const View& v, int64_t r0, int rows,
+                                           int cols) {
     const int total = rows * cols;
     if (v.cs == 1) {
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
             const int r = idx / cols, c = idx - r * cols;
-            dst[r * cols + c] = v.ptr[(r0 + r) * v.rs + c];
+            cp_async8(dst + r * ld + c0 + c, v.ptr + (r0 + r) * v.rs + c);
         }
     } else {
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
             const int c = idx / rows, r = idx - c * rows;
-            dst[r * cols + c] = v.ptr[(r0 + r) * v.rs + c * v.cs];
+            cp_async8(dst + r * ld + c0 + c, v.ptr + (r0 + r) * v.rs + static_cast<int64_t>(c) * v.cs);
         }
     }
 }
@@ -68,79 +81,82 @@ __device__ __forceinline__ void store_tile(const View& v, const double* src, int
     }
 }
 
+// Row tiles stream through a kStages-deep cp.async ring (tile i+2 in flight while
+// tile i is transformed / reduced), so every CTA keeps ~2 tiles of loads outstanding.
 template <int MAXB>
 __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
     extern __shared__ double smem[];
     const int u = a.u0 + a.u1;
-    double* Ut = smem;                       // kTR x u
-    double* Vt = Ut + kTR * u;               // kTR x kv
-    double* Wt = Vt + kTR * a.kv;            // kTR x kw
-    double* Bt = Wt + kTR * a.kw;            // kTR
-    double* Cs = Bt + kTR;                   // inner x kw
+    const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
+    const int su = need_u ? u : 0;
+    const int stage_elems = kTR * (su + a.kv + 1);
+    double* Wt = smem + kStages * stage_elems;  // kTR x kw
+    double* Cs = Wt + kTR * a.kw;               // inner x kw
 
     const int inner = a.transform == TS_UPDATE ? u : a.kv;
-    const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
     if (a.transform != TS_NONE)
         for (int i = threadIdx.x; i < inner * a.kw; i += blockDim.x) {
             const int c = i / inner, q = i - c * inner;
             Cs[i] = a.C[q + static_cast<int64_t>(c) * a.ldc];
         }
-
-    const double* right = (a.transform == TS_NONE) ? Vt : Wt;
     const int rq = (a.transform == TS_NONE) ? a.kv : a.kw;
 
-    // gram thread assignment
     double acc[MAXB][4];
 #pragma unroll
     for (int i = 0; i < MAXB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
     const int nbi = (a.P + 1) / 2;
 
     const int64_t ntiles = (a.n + kTR - 1) / kTR;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t nt = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    auto issue = [&](int64_t i) {
+        const int64_t t = blockIdx.x + i * gridDim.x;
         const int64_t r0 = t * kTR;
         const int rows = static_cast<int>(min(static_cast<int64_t>(kTR), a.n - r0));
-        __syncthreads();
+        double* base = smem + (i % kStages) * stage_elems;
+        double* Ut = base;
+        double* Vt = base + kTR * su;
+        double* Bt = Vt + kTR * a.kv;
         if (need_u) {
-            if (a.u0) {
-                // U0 occupies columns [0, u0) of Ut, U1 [u0, u)
-                const int total = rows * a.u0;
-                for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-                    int r, c;
-                    if (a.U0.cs == 1) { r = idx / a.u0; c = idx - r * a.u0; }
-                    else { c = idx / rows; r = idx - c * rows; }
-                    Ut[r * u + c] = a.U0.ptr[(r0 + r) * a.U0.rs + c * a.U0.cs];
-                }
-            }
-            if (a.u1) {
-                const int total = rows * a.u1;
-                for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-                    int r, c;
-                    if (a.U1.cs == 1) { r = idx / a.u1; c = idx - r * a.u1; }
-                    else { c = idx / rows; r = idx - c * rows; }
-                    Ut[r * u + a.u0 + c] = a.U1.ptr[(r0 + r) * a.U1.rs + c * a.U1.cs];
-                }
-            }
+            if (a.u0) issue_view(Ut, u, 0, a.U0, r0, rows, a.u0);
+            if (a.u1) issue_view(Ut, u, a.u0, a.U1, r0, rows, a.u1);
         }
-        load_tile(Vt, a.V, r0, rows, a.kv);
+        issue_view(Vt, a.kv, 0, a.V, r0, rows, a.kv);
         if (a.gram && a.b)
-            for (int r = threadIdx.x; r < rows; r += blockDim.x) Bt[r] = a.b[r0 + r];
+            for (int r = threadIdx.x; r < rows; r += blockDim.x) cp_async8(Bt + r, a.b + r0 + r);
+    };
+
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nt) issue(s);
+        cp_commit();
+    }
+    for (int64_t i = 0; i < nt; ++i) {
+        if (i + kStages - 1 < nt) issue(i + kStages - 1);
+        cp_commit();
+        cp_wait<kStages - 1>();
         __syncthreads();
+        const int64_t t = blockIdx.x + i * gridDim.x;
+        const int64_t r0 = t * kTR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(kTR), a.n - r0));
+        const double* Ut = smem + (i % kStages) * stage_elems;
+        const double* Vt = Ut + kTR * su;
+        const double* Bt = Vt + kTR * a.kv;
 
         if (a.transform == TS_UPDATE) {
             const int total = rows * a.kw;
             for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
                 const int r = idx / a.kw, c = idx - r * a.kw;
-                double s = 0.0;
-                for (int q = 0; q < u; ++q) s = fma(Ut[r * u + q], Cs[q + c * u], s);
-                Wt[r * a.kw + c] = Vt[r * a.kv + c] - s;
+                double sacc = 0.0;
+                for (int q = 0; q < u; ++q) sacc = fma(Ut[r * u + q], Cs[q + c * u], sacc);
+                Wt[r * a.kw + c] = Vt[r * a.kv + c] - sacc;
             }
         } else if (a.transform == TS_COMBINE) {
             const int total = rows * a.kw;
             for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
                 const int r = idx / a.kw, c = idx - r * a.kw;
-                double s = 0.0;
-                for (int q = 0; q < a.kv; ++q) s = fma(Vt[r * a.kv + q], Cs[q + c * a.kv], s);
-                Wt[r * a.kw + c] = s;
+                double sacc = 0.0;
+                for (int q = 0; q < a.kv; ++q) sacc = fma(Vt[r * a.kv + q], Cs[q + c * a.kv], sacc);
+                Wt[r * a.kw + c] = sacc;
             }
         }
         if (a.transform != TS_NONE) {
@@ -149,6 +165,7 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
             if (w1 > 0) store_tile(a.W, Wt, r0, rows, 0, w1, a.kw);
             if (a.kw > w1) store_tile(a.W2, Wt, r0, rows, w1, a.kw - w1, a.kw);
         }
+        const double* right = (a.transform == TS_NONE) ? Vt : Wt;
 
         if (a.gram) {
             // left column i: i < uL -> Ut[:, i]; else right[:, i - uL]
@@ -162,13 +179,16 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
                 const int i0 = 2 * bi, j0 = 2 * bj;
                 const bool i1ok = i0 + 1 < a.P, j1ok = j0 + 1 < a.Q;
                 for (int r = sl; r < rows; r += a.slices) {
-                    const double bw = a.b ? Bt[r] : 1.0;
                     double l0, l1 = 0.0;
                     l0 = (i0 < uL) ? Ut[r * u + i0] : right[r * rq + (i0 - uL)];
                     if (i1ok) l1 = (i0 + 1 < uL) ? Ut[r * u + i0 + 1] : right[r * rq + (i0 + 1 - uL)];
                     double q0 = right[r * rq + j0];
                     double q1 = j1ok ? right[r * rq + j0 + 1] : 0.0;
-                    if (a.b) { q0 *= bw; q1 *= bw; }
+                    if (a.b) {
+                        const double bw = Bt[r];
+                        q0 *= bw;
+                        q1 *= bw;
+                    }
                     acc[bb][0] = fma(l0, q0, acc[bb][0]);
                     acc[bb][1] = fma(l1, q0, acc[bb][1]);
                     acc[bb][2] = fma(l0, q1, acc[bb][2]);
@@ -176,7 +196,9 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
                 }
             }
         }
+        __syncthreads();
     }
+    cp_wait<0>();
 
     if (!a.gram) return;
     double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
@@ -189,14 +211,14 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
         if (threadIdx.x < a.nb) {
             const int blk = threadIdx.x;
             const int bi = blk % nbi, bj = blk / nbi;
-            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            double sred[4] = {0.0, 0.0, 0.0, 0.0};
             for (int sl = 0; sl < a.slices; ++sl)
-                for (int k = 0; k < 4; ++k) s[k] += red[k * blockDim.x + sl * a.nb + blk];
+                for (int k = 0; k < 4; ++k) sred[k] += red[k * blockDim.x + sl * a.nb + blk];
             const int i0 = 2 * bi, j0 = 2 * bj;
-            part[i0 + j0 * a.P] = s[0];
-            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = s[1];
-            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = s[2];
-            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = s[3];
+            part[i0 + j0 * a.P] = sred[0];
+            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = sred[1];
+            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = sred[2];
+            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = sred[3];
         }
     } else {
 #pragma unroll
@@ -344,8 +366,17 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
         a.nb = 1;
         a.slices = 1;
     }
+    const int u = a.u0 + a.u1;
+    const int inner = s.transform == TS_UPDATE ? u : a.kv;
+    a.ldc = s.ldc > 0 ? s.ldc : inner;
+    const bool need_u = (s.transform == TS_UPDATE) || (s.gram && s.gram_left_u);
+    size_t sm = sizeof(double) *
+                (static_cast<size_t>(kStages) * kTR * ((need_u ? u : 0) + a.kv + 1) +
+                 static_cast<size_t>(kTR) * a.kw + (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
+    sm = std::max(sm, sizeof(double) * 4 * kTsThreads);
+    const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / sm)));
     const int64_t ntiles = (s.n + kTR - 1) / kTR;
-    int grid = grid_for(ntiles, 1, 4);
+    int grid = grid_for(ntiles, 1, per_sm);
     const size_t PQ = static_cast<size_t>(a.P) * a.Q;
     if (a.gram) {
         // shrink the grid if the partial scratch is too small (keeps determinism: grid is a
@@ -355,13 +386,6 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
             throw SpError(1, "ts_run: gram scratch too small");
     }
     a.partial = scratch;
-    const int u = a.u0 + a.u1;
-    const int inner = s.transform == TS_UPDATE ? u : a.kv;
-    a.ldc = s.ldc > 0 ? s.ldc : inner;
-    size_t sm = sizeof(double) *
-                (static_cast<size_t>(kTR) * (u + a.kv + a.kw) + kTR +
-                 (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
-    sm = std::max(sm, sizeof(double) * 4 * kTsThreads);
     auto launch = [&](auto kern) {
         if (sm > 48 * 1024) SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         kern<<<grid, kTsThreads, sm, st>>>(a);

@@ -237,6 +237,7 @@ void build_laplacian(int kind, const DevGraph& g, bool materialize, DevLaplacian
         L.op.diag = L.diag.p;
         L.op.is_diagonal = true;
         L.op.nnz = n;
+        L.op.max_row = 1;
         if (materialize) {
             // the diagonal CSR: offsets i, cols i, vals deg (laplacian.cpp:134-143)
             L.offs_L.alloc(n + 1);
@@ -297,11 +298,13 @@ void build_laplacian(int kind, const DevGraph& g, bool materialize, DevLaplacian
         L.op.cols = L.cols_L.p;
         L.op.vals = L.vals_L.p;
         L.op.nnz = nnzL;
+        L.op.max_row = static_cast<int>(std::min<int64_t>(g.max_degree_local + 1, 1 << 30));
     }
     if (pattern_ok) {
         L.op.offs = g.offs.p;
         L.op.cols = g.cols.p;
         L.op.nnz = g.nnz_local;
+        L.op.max_row = static_cast<int>(std::min<int64_t>(g.max_degree_local, 1 << 30));
         if (kind == 0) {
             L.op.mode = OP_LAPLACE_UNIT;
             SPB_CUDA(cudaMemcpyAsync(L.diag.p, g.deg.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));

@@ -34,6 +34,7 @@ struct DevOp {
     const int32_t* long_rows = nullptr;
     int64_t n_long = 0;
     int64_t long_threshold = 1 << 30;
+    int max_row = 1 << 30;      // max stored entries in a row (selects the tiled kernel when <= 32)
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -92,6 +93,11 @@ int ts_run(const TsSpec& spec, double* gram_out, double* scratch, size_t scratch
 
 // Deterministic per-CTA column sums; returns the number of partial rows.
 int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s);
+
+// std::mt19937_64(seed) draws [0, n*d) as uniform(-1,1), column-major order;
+// rows [row0, row0+nloc) written to out (rng.cu).
+void mt_uniform_block(uint64_t seed, int64_t n, int d, int64_t row0, int64_t nloc, const View& out,
+                      cudaStream_t s);
 
 // Elementwise helpers
 void scale_cols(View V, const double* colscale_dev, cudaStream_t s, int64_t n);  // V(:,j) *= s[j]

@@ -404,14 +404,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
     // v0: seeded uniform(-1,1) (preconditioners.cpp:82-87), minus its mean, normalized
     DBuf<double> Vb(static_cast<size_t>(std::max<int64_t>(n_, 1)) * (k_req + 1));
     auto vcol = [&](int j) { return colmajor(Vb.p + static_cast<size_t>(j) * std::max<int64_t>(n_, 1), std::max<int64_t>(n_, 1), 1); };
-    {
-        std::mt19937_64 rng(seed);
-        std::vector<double> v(n_);
-        for (int64_t i = 0; i < row0; ++i) rng();
-        for (int64_t i = 0; i < n_; ++i) v[i] = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
-        if (n_ > 0) SPB_CUDA(cudaMemcpyAsync(Vb.p, v.data(), sizeof(double) * n_, cudaMemcpyHostToDevice, s_));
-        SPB_CUDA(cudaStreamSynchronize(s_));
-    }
+    mt_uniform_block(seed, n_glob, 1, row0, n_, vcol(0), s_);
     const int rows = colsum_partials(n_, vcol(0), scratch_.p, s_);
     reduce_partials(scratch_.p, rows, 1, norms_.p, s_);
     cm.sum_small(norms_.p, 1, s_);
@@ -682,22 +675,7 @@ void initial_block_random(int64_t n, int d, uint64_t seed, int64_t row0, int64_t
                           const View& X, cudaStream_t s) {
     if (d > n) throw_infeasible("initial_guess_random: d > n");
     if (d < 1) throw_infeasible("initial_guess_random: d < 1");
-    std::mt19937_64 rng(seed);
-    std::vector<double> h(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
-    for (int j = 0; j < d; ++j) {
-        for (int64_t i = 0; i < n; ++i) {
-            const uint64_t r = rng();
-            if (i >= row0 && i < row0 + nloc) {
-                const double u = static_cast<double>(r >> 11) * 0x1.0p-53;
-                h[static_cast<size_t>(j) * nloc + (i - row0)] = 2.0 * u - 1.0;
-            }
-        }
-    }
-    if (nloc <= 0) return;
-    DBuf<double> tmp(h.size());
-    SPB_CUDA(cudaMemcpyAsync(tmp.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
-    copy_view(nloc, colmajor(tmp.p, nloc, d), X.sub(0, d), s);
-    SPB_CUDA(cudaStreamSynchronize(s));
+    mt_uniform_block(seed, n, d, row0, nloc, X.sub(0, d), s);
 }
 
 void initial_block_piecewise(int64_t n, int d, int64_t row0, int64_t nloc, const View& X, cudaStream_t s) {

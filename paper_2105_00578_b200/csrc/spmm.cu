@@ -141,6 +141,100 @@ __global__ void __launch_bounds__(kThreads) spmm_group_kernel(const DevOp op, co
     }
 }
 
+
+// Warp-tiled kernel for short rows (max_row <= 32: meshes). A warp owns 32
+// consecutive rows: it loads their 33 offsets and the contiguous column-index
+// segment (<= 32*32 entries) with coalesced loads into shared memory, then its
+// 32/G groups walk the rows. The diagonal slot is located before accumulating,
+// so the inner loops are branch-free and their gathers independent.
+constexpr int kTileRows = 32;
+constexpr int kTileCap = 32 * 32;
+
+template <int G, int MODE, int EPI>
+__global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, const View X, const EpiArgs ea,
+                                                             const int m) {
+    constexpr int GPW = 32 / G;
+    extern __shared__ int32_t s_cols_all[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    int32_t* sc = s_cols_all + warp * kTileCap;
+    double* sv = reinterpret_cast<double*>(s_cols_all + (kThreads / 32) * kTileCap) + warp * kTileCap;
+    const int gl = lane & (G - 1);
+    const int gw = lane / G;
+    double sq = 0.0;
+    const int64_t ntiles = (op.n + kTileRows - 1) / kTileRows;
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+        const int64_t r0 = tile * kTileRows;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), op.n - r0));
+        const int64_t ko = op.offs[r0 + min(lane, nr)];
+        const int64_t kbeg = __shfl_sync(0xffffffffu, ko, 0);
+        const int64_t kend = __shfl_sync(0xffffffffu, ko, nr);
+        const int total = static_cast<int>(kend - kbeg);
+        __syncwarp();
+        for (int e = lane; e < total; e += 32) {
+            sc[e] = __ldg(op.cols + kbeg + e);
+            if (MODE == OP_EXPLICIT) sv[e] = __ldg(op.vals + kbeg + e);
+        }
+        __syncwarp();
+        const int rows_per_group = (nr + GPW - 1) / GPW;
+        for (int it = 0; it < rows_per_group; ++it) {
+            const int rr = it * GPW + gw;
+            const int rclamp = min(rr, nr - 1);
+            const int k0 = static_cast<int>(__shfl_sync(0xffffffffu, ko, rclamp) - kbeg);
+            const int k1 = static_cast<int>(__shfl_sync(0xffffffffu, ko, rclamp + 1) - kbeg);
+            if (rr >= nr) continue;
+            const int64_t row = r0 + rr;
+            const int64_t grow = op.row0 + row;
+            for (int c0 = 0; c0 < m; c0 += G) {
+                const int c = c0 + gl;
+                if (c >= m) continue;
+                const double xi = X.at(grow, c);
+                double acc = 0.0;
+                if (MODE == OP_EXPLICIT) {
+                    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, __dmul_rn(sv[k], X.at(sc[k], c)));
+                } else {
+                    // storage position of the diagonal: before the first column > grow
+                    int kd = k0;
+                    while (kd < k1 && sc[kd] < grow) ++kd;
+                    if (MODE == OP_LAPLACE_UNIT) {
+#pragma unroll 4
+                        for (int k = k0; k < kd; ++k) acc = __dsub_rn(acc, X.at(sc[k], c));
+                        acc = __dadd_rn(acc, __dmul_rn(op.diag[row], xi));
+#pragma unroll 4
+                        for (int k = kd; k < k1; ++k) acc = __dsub_rn(acc, X.at(sc[k], c));
+                    } else {
+                        const double nisdi = -op.isd[grow];
+#pragma unroll 4
+                        for (int k = k0; k < kd; ++k) {
+                            const int j = sc[k];
+                            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(nisdi, op.isd[j]), X.at(j, c)));
+                        }
+                        acc = __dadd_rn(acc, xi);
+#pragma unroll 4
+                        for (int k = kd; k < k1; ++k) {
+                            const int j = sc[k];
+                            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(nisdi, op.isd[j]), X.at(j, c)));
+                        }
+                    }
+                }
+                epilogue<EPI>(ea, row, c, acc, xi, sq);
+            }
+        }
+    }
+    if (EPI == EPI_RESIDUAL) {
+        __shared__ double red[kThreads];
+        red[threadIdx.x] = sq;
+        __syncthreads();
+        if (threadIdx.x < m) {
+            double s = 0.0;
+            for (int g = 0; g < kThreads / G; ++g) s += red[g * G + threadIdx.x];
+            ea.partial[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = s;
+        }
+    }
+}
+
 // One CTA per long row (power-law hubs). Thread t accumulates entries
 // k0+t, k0+t+256, ... for every column; fixed-order warp butterfly + smem tree.
 template <int MODE, int EPI>
@@ -205,6 +299,29 @@ template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
     int G = 1;
     while (G < m && G < 32) G <<= 1;
+    if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0) {
+        const int64_t ntiles = (op.n + kTileRows - 1) / kTileRows;
+        const int grid = grid_for(ntiles, kThreads / 32, 8);
+        const size_t smem = (kThreads / 32) * kTileCap * (sizeof(int32_t) + (MODE == OP_EXPLICIT ? sizeof(double) : 0));
+        auto go = [&](auto kern) {
+            static bool attr = false;
+            if (!attr) {
+                SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                attr = true;
+            }
+            kern<<<grid, kThreads, smem, s>>>(op, X, ea, m);
+        };
+        switch (G) {
+        case 1: go(spmm_tile_kernel<1, MODE, EPI>); break;
+        case 2: go(spmm_tile_kernel<2, MODE, EPI>); break;
+        case 4: go(spmm_tile_kernel<4, MODE, EPI>); break;
+        case 8: go(spmm_tile_kernel<8, MODE, EPI>); break;
+        case 16: go(spmm_tile_kernel<16, MODE, EPI>); break;
+        default: go(spmm_tile_kernel<32, MODE, EPI>); break;
+        }
+        SPB_LAUNCH_CHECK();
+        return grid;
+    }
     const int groups_per_block = kThreads / G;
     const int grid = grid_for(op.n, groups_per_block, 8);
     switch (G) {
