@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
         const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), op.n - r0));
         const int64_t ko = op.offs[r0 + min(lane, nr)];
         const int64_t kbeg = __shfl_sync(0xffffffffu, ko, 0);
-        const int64_t kend = __shfl_sync(0xffffffffu, ko, nr);
+        const int64_t kend = op.offs[r0 + nr];
         const int total = static_cast<int>(kend - kbeg);
         __syncwarp();
         for (int e = lane; e < total; e += 32) {
@@ -182,8 +182,10 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
         for (int it = 0; it < rows_per_group; ++it) {
             const int rr = it * GPW + gw;
             const int rclamp = min(rr, nr - 1);
-            const int k0 = static_cast<int>(__shfl_sync(0xffffffffu, ko, rclamp) - kbeg);
-            const int k1 = static_cast<int>(__shfl_sync(0xffffffffu, ko, rclamp + 1) - kbeg);
+            const int64_t o_lo = __shfl_sync(0xffffffffu, ko, rclamp);
+            const int64_t o_hi = __shfl_sync(0xffffffffu, ko, min(rclamp + 1, 31));
+            const int k0 = static_cast<int>(o_lo - kbeg);
+            const int k1 = static_cast<int>((rclamp + 1 >= nr ? kend : o_hi) - kbeg);
             if (rr >= nr) continue;
             const int64_t row = r0 + rr;
             const int64_t grow = op.row0 + row;
