@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
 #include <random>
 
 namespace spb {
@@ -665,6 +666,9 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     (void)Hv;
     res.iterations = iter;
     res.theta = theta;
+    if (ctx_->prof.on)
+        std::fprintf(stderr, "[spb-profile] lobpcg: %d iterations, %d slow orthonormalizations, %d CholQR fix-ups\n",
+                     iter, res.slow_orth, res.cholqr_fixups);
     return res;
 }
 
