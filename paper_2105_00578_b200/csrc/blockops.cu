@@ -235,12 +235,17 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
     }
 }
 
+// One warp per Gram entry: lane l sums partial rows l, l+32, ... then a fixed
+// butterfly — deterministic for a fixed grid.
 __global__ void reduce_gram_kernel(const double* partial, int rows, int PQ, double* out) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (e >= PQ) return;
     double s = 0.0;
-    for (int r = 0; r < rows; ++r) s += partial[static_cast<int64_t>(r) * PQ + e];
-    out[e] = s;
+    for (int r = lane; r < rows; r += 32) s += partial[static_cast<int64_t>(r) * PQ + e];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) out[e] = s;
 }
 
 __global__ void scale_cols_kernel(View v, const double* sc, int64_t n) {
@@ -398,7 +403,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     else throw_dimension("ts_run: gram too large");
     SPB_LAUNCH_CHECK();
     if (a.gram) {
-        reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 128), 128, 0, st>>>(
+        reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 4), 128, 0, st>>>(
             scratch, grid, static_cast<int>(PQ), gram_out);
         SPB_LAUNCH_CHECK();
     }

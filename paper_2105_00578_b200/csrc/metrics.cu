@@ -25,10 +25,24 @@ __global__ void validate_kernel(int64_t n, const int32_t* a, int64_t K, int* bad
         if (a[i] < 0 || a[i] >= K) atomicOr(bad, 1);
 }
 
-__global__ void count_kernel(int64_t n, const int32_t* a, unsigned long long* cnt) {
+// per-CTA shared histogram (K <= 4096) then one global atomic per bin (exact)
+__global__ void count_kernel(int64_t n, const int32_t* a, int64_t K, unsigned long long* cnt) {
+    extern __shared__ unsigned int hist[];
+    const bool local = K <= 4096;
+    if (local) {
+        for (int64_t k = threadIdx.x; k < K; k += blockDim.x) hist[k] = 0;
+        __syncthreads();
+    }
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        atomicAdd(cnt + a[i], 1ull);
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (local) atomicAdd(hist + a[i], 1u);
+        else atomicAdd(cnt + a[i], 1ull);
+    }
+    if (local) {
+        __syncthreads();
+        for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+            if (hist[k]) atomicAdd(cnt + k, static_cast<unsigned long long>(hist[k]));
+    }
 }
 
 __global__ void iota32_kernel(int64_t n, int32_t* v) {
@@ -119,7 +133,7 @@ PartitionMetrics make_partition_dev(sp_context* ctx, const DevGraph& g, const in
         DBuf<unsigned long long> cnt(K);
         SPB_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * K, s));
         if (n > 0) {
-            count_kernel<<<grid_for(n, kT, 8), kT, 0, s>>>(n, a_local, cnt.p);
+            count_kernel<<<grid_for(n, kT, 2), kT, K <= 4096 ? sizeof(unsigned int) * K : 0, s>>>(n, a_local, K, cnt.p);
             SPB_LAUNCH_CHECK();
         }
         cm.sum_i64(reinterpret_cast<int64_t*>(cnt.p), static_cast<int>(K), s);

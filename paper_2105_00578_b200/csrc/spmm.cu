@@ -143,24 +143,126 @@ __global__ void __launch_bounds__(kThreads) spmm_group_kernel(const DevOp op, co
 
 
 // Warp-tiled kernel for short rows (max_row <= 32: meshes). A warp owns 32
-// consecutive rows: it loads their 33 offsets and the contiguous column-index
-// segment (<= 32*32 entries) with coalesced loads into shared memory, then its
-// 32/G groups walk the rows. The diagonal slot is located before accumulating,
-// so the inner loops are branch-free and their gathers independent.
+// consecutive rows: it loads their offsets and the contiguous column-index
+// segment (<= 32*32 entries) with coalesced loads into shared memory, computes
+// each row's length and diagonal slot once (lane = row), then its 32/G groups
+// walk (row, column-chunk) items. Each item issues all its gathers before
+// accumulating (fully unrolled, predicated, 32-bit index math), and short rows
+// are processed two items per group iteration to keep more loads in flight.
+// X, Y and H are row-major (cs == 1) with 32-bit row*ld products.
 constexpr int kTileRows = 32;
 constexpr int kTileCap = 32 * 32;
 
-template <int G, int MODE, int EPI>
-__global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, const View X, const EpiArgs ea,
-                                                             const int m) {
+struct TileArgs {
+    const double* X;
+    int ldx;
+    double* Y;
+    int ldy;
+    double* H;
+    int ldh;
+    int m;
+};
+
+template <int MAXR, int MODE>
+struct ItemLoad {
+    double xv[MAXR];
+    double vv[MAXR];  // explicit values / normalized coefficients
+    double xi, h;
+    int len, kd, c;
+    int64_t row;
+    bool act;
+};
+
+template <int G, int MAXR, int MODE, int EPI>
+__device__ __forceinline__ void tile_item_load(ItemLoad<MAXR, MODE>& it, const DevOp& op, const TileArgs& ta,
+                                               const EpiArgs& ea, const int32_t* sc, const double* sv,
+                                               const int* s_start, const int* s_len, const int* s_kd,
+                                               int64_t r0, int rr, int ch, int gl) {
+    it.c = ch * G + gl;
+    it.act = it.c < ta.m;
+    it.row = r0 + rr;
+    const int st = s_start[rr];
+    it.len = s_len[rr];
+    it.kd = s_kd[rr];
+    const int64_t grow = op.row0 + it.row;
+    const double* xc = ta.X + it.c;
+    it.xi = it.act ? xc[static_cast<int64_t>(static_cast<int>(grow) * ta.ldx)] : 0.0;
+    it.h = 0.0;
+    if (EPI == EPI_POLY && !ea.first && it.act) it.h = ta.H[static_cast<int>(it.row) * ta.ldh + it.c];
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+        if (k < it.len && it.act) {
+            const int j = sc[st + k];
+            it.xv[k] = xc[j * ta.ldx];
+            if (MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) it.vv[k] = sv[st + k];
+        }
+    }
+}
+
+template <int MAXR, int MODE, int EPI>
+__device__ __forceinline__ void tile_item_finish(const ItemLoad<MAXR, MODE>& it, const DevOp& op,
+                                                 const TileArgs& ta, const EpiArgs& ea, const double* s_theta,
+                                                 double& sq) {
+    if (!it.act) return;
+    double acc = 0.0;
+    double dterm = 0.0;
+    if (MODE == OP_LAPLACE_UNIT) dterm = __dmul_rn(op.diag[it.row], it.xi);
+    if (MODE == OP_NORMAL_UNIT) dterm = it.xi;
+#pragma unroll
+    for (int k = 0; k < MAXR; ++k) {
+        if (k < it.len) {
+            if (MODE == OP_LAPLACE_UNIT) {
+                if (k == it.kd) acc = __dadd_rn(acc, dterm);
+                acc = __dsub_rn(acc, it.xv[k]);
+            } else if (MODE == OP_NORMAL_UNIT) {
+                if (k == it.kd) acc = __dadd_rn(acc, dterm);
+                acc = __dadd_rn(acc, __dmul_rn(it.vv[k], it.xv[k]));
+            } else {
+                acc = __dadd_rn(acc, __dmul_rn(it.vv[k], it.xv[k]));
+            }
+        }
+    }
+    if ((MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) && it.kd >= it.len) acc = __dadd_rn(acc, dterm);
+    const int yoff = static_cast<int>(it.row) * ta.ldy + it.c;
+    if (EPI == EPI_STORE) {
+        ta.Y[yoff] = acc;
+    } else if (EPI == EPI_RESIDUAL) {
+        const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[it.row], it.xi) : it.xi;
+        const double r = __dsub_rn(acc, __dmul_rn(s_theta[it.c], bx));
+        ta.Y[yoff] = r;
+        sq = fma(r, r, sq);
+    } else {
+        const double pn = __dsub_rn(it.xi, __dmul_rn(ea.inv_cur, acc));
+        ta.Y[yoff] = pn;
+        double h = ea.first ? __dmul_rn(ea.inv_cur, it.xi) : it.h;
+        h = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
+        ta.H[static_cast<int>(it.row) * ta.ldh + it.c] = h;
+    }
+}
+
+template <int G, int MAXR, int RPI, int MODE, int EPI>
+__global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
     constexpr int GPW = 32 / G;
-    extern __shared__ int32_t s_cols_all[];
+    constexpr bool kVals = (MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT);
+    extern __shared__ int32_t s_dyn[];
+    __shared__ int s_start_all[kThreads / 32][kTileRows + 1];
+    __shared__ int s_len_all[kThreads / 32][kTileRows];
+    __shared__ int s_kd_all[kThreads / 32][kTileRows];
+    __shared__ double s_theta[kMaxCols];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    int32_t* sc = s_cols_all + warp * kTileCap;
-    double* sv = reinterpret_cast<double*>(s_cols_all + (kThreads / 32) * kTileCap) + warp * kTileCap;
+    int32_t* sc = s_dyn + warp * kTileCap;
+    double* sv = reinterpret_cast<double*>(s_dyn + (kThreads / 32) * kTileCap) + warp * kTileCap;
+    int* s_start = s_start_all[warp];
+    int* s_len = s_len_all[warp];
+    int* s_kd = s_kd_all[warp];
+    if (EPI == EPI_RESIDUAL) {
+        for (int c = threadIdx.x; c < ta.m; c += kThreads) s_theta[c] = ea.theta[c];
+        __syncthreads();
+    }
     const int gl = lane & (G - 1);
     const int gw = lane / G;
+    const int nch = (ta.m + G - 1) / G;
     double sq = 0.0;
     const int64_t ntiles = (op.n + kTileRows - 1) / kTileRows;
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
@@ -170,69 +272,61 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
         const int nr = static_cast<int>(min(static_cast<int64_t>(kTileRows), op.n - r0));
         const int64_t ko = op.offs[r0 + min(lane, nr)];
         const int64_t kbeg = __shfl_sync(0xffffffffu, ko, 0);
+        const int64_t kn = __shfl_down_sync(0xffffffffu, ko, 1);
         const int64_t kend = op.offs[r0 + nr];
         const int total = static_cast<int>(kend - kbeg);
         __syncwarp();
         for (int e = lane; e < total; e += 32) {
-            sc[e] = __ldg(op.cols + kbeg + e);
+            const int j = __ldg(op.cols + kbeg + e);
+            sc[e] = j;
             if (MODE == OP_EXPLICIT) sv[e] = __ldg(op.vals + kbeg + e);
+            if (MODE == OP_NORMAL_UNIT) sv[e] = __ldg(op.isd + j);
         }
         __syncwarp();
-        const int rows_per_group = (nr + GPW - 1) / GPW;
-        for (int it = 0; it < rows_per_group; ++it) {
-            const int rr = it * GPW + gw;
-            const int rclamp = min(rr, nr - 1);
-            const int64_t o_lo = __shfl_sync(0xffffffffu, ko, rclamp);
-            const int64_t o_hi = __shfl_sync(0xffffffffu, ko, min(rclamp + 1, 31));
-            const int k0 = static_cast<int>(o_lo - kbeg);
-            const int k1 = static_cast<int>((rclamp + 1 >= nr ? kend : o_hi) - kbeg);
-            if (rr >= nr) continue;
-            const int64_t row = r0 + rr;
-            const int64_t grow = op.row0 + row;
-            for (int c0 = 0; c0 < m; c0 += G) {
-                const int c = c0 + gl;
-                if (c >= m) continue;
-                const double xi = X.at(grow, c);
-                double acc = 0.0;
-                if (MODE == OP_EXPLICIT) {
-                    for (int k = k0; k < k1; ++k) acc = __dadd_rn(acc, __dmul_rn(sv[k], X.at(sc[k], c)));
-                } else {
-                    // storage position of the diagonal: before the first column > grow
-                    int kd = k0;
-                    while (kd < k1 && sc[kd] < grow) ++kd;
-                    if (MODE == OP_LAPLACE_UNIT) {
-#pragma unroll 4
-                        for (int k = k0; k < kd; ++k) acc = __dsub_rn(acc, X.at(sc[k], c));
-                        acc = __dadd_rn(acc, __dmul_rn(op.diag[row], xi));
-#pragma unroll 4
-                        for (int k = kd; k < k1; ++k) acc = __dsub_rn(acc, X.at(sc[k], c));
-                    } else {
-                        const double nisdi = -op.isd[grow];
-#pragma unroll 4
-                        for (int k = k0; k < kd; ++k) {
-                            const int j = sc[k];
-                            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(nisdi, op.isd[j]), X.at(j, c)));
-                        }
-                        acc = __dadd_rn(acc, xi);
-#pragma unroll 4
-                        for (int k = kd; k < k1; ++k) {
-                            const int j = sc[k];
-                            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(nisdi, op.isd[j]), X.at(j, c)));
-                        }
-                    }
+        if (lane < nr) {
+            const int st = static_cast<int>(ko - kbeg);
+            const int len = static_cast<int>((lane + 1 < nr ? kn : kend) - ko);
+            const int64_t grow = op.row0 + r0 + lane;
+            int kd = 0;
+            if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) {
+                while (kd < len && sc[st + kd] < grow) ++kd;
+                if (MODE == OP_NORMAL_UNIT) {
+                    const double nisdi = -op.isd[grow];
+                    for (int k = 0; k < len; ++k) sv[st + k] = __dmul_rn(nisdi, sv[st + k]);
                 }
-                epilogue<EPI>(ea, row, c, acc, xi, sq);
+            }
+            s_start[lane] = st;
+            s_len[lane] = len;
+            s_kd[lane] = kd;
+        }
+        __syncwarp();
+        const int items = nr * nch;
+        for (int it0 = gw; it0 < items; it0 += GPW * RPI) {
+            ItemLoad<MAXR, MODE> A;
+            tile_item_load<G, MAXR, MODE, EPI>(A, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, it0 / nch,
+                                               it0 % nch, gl);
+            if (RPI == 2) {
+                const int it1 = it0 + GPW;
+                ItemLoad<MAXR, MODE> B;
+                if (it1 < items)
+                    tile_item_load<G, MAXR, MODE, EPI>(B, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, it1 / nch,
+                                                       it1 % nch, gl);
+                tile_item_finish<MAXR, MODE, EPI>(A, op, ta, ea, s_theta, sq);
+                if (it1 < items) tile_item_finish<MAXR, MODE, EPI>(B, op, ta, ea, s_theta, sq);
+            } else {
+                tile_item_finish<MAXR, MODE, EPI>(A, op, ta, ea, s_theta, sq);
             }
         }
+        __syncwarp();
     }
     if (EPI == EPI_RESIDUAL) {
         __shared__ double red[kThreads];
         red[threadIdx.x] = sq;
         __syncthreads();
-        if (threadIdx.x < m) {
+        if (threadIdx.x < ta.m) {
             double s = 0.0;
             for (int g = 0; g < kThreads / G; ++g) s += red[g * G + threadIdx.x];
-            ea.partial[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = s;
+            ea.partial[static_cast<int64_t>(blockIdx.x) * ta.m + threadIdx.x] = s;
         }
     }
 }
@@ -301,26 +395,50 @@ template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
     int G = 1;
     while (G < m && G < 32) G <<= 1;
-    if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0) {
+    const bool rowmajor_ok = (m == 1 || X.cs == 1) && (ea.mode == EPI_STORE || ea.Y.cs == 1) &&
+                             (ea.mode != EPI_POLY || ea.H.cs == 1) &&
+                             (op.row0 + op.n) * (m == 1 ? X.rs : X.rs) < (int64_t(1) << 31) &&
+                             op.n * ea.Y.rs < (int64_t(1) << 31);
+    if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && rowmajor_ok) {
+        // row-major addressing: element (r, c) at r*ld + c (m == 1 column views use ld = rs)
+        TileArgs ta;
+        ta.X = X.ptr;
+        ta.ldx = static_cast<int>(X.rs);
+        ta.Y = ea.Y.ptr;
+        ta.ldy = static_cast<int>(ea.Y.rs);
+        ta.H = ea.H.ptr;
+        ta.ldh = static_cast<int>(ea.H.rs);
+        ta.m = m;
+        // STORE: 8-wide column chunks keep 4 rows per warp for wide blocks; fused
+        // epilogues need one chunk per row (column = lane)
+        int Gt = G;
+        if (ea.mode == EPI_STORE && m > 8) Gt = 8;
         const int64_t ntiles = (op.n + kTileRows - 1) / kTileRows;
         const int grid = grid_for(ntiles, kThreads / 32, 8);
-        const size_t smem = (kThreads / 32) * kTileCap * (sizeof(int32_t) + (MODE == OP_EXPLICIT ? sizeof(double) : 0));
+        const size_t smem = (kThreads / 32) * kTileCap *
+                            (sizeof(int32_t) + ((MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) ? sizeof(double) : 0));
         auto go = [&](auto kern) {
             static bool attr = false;
             if (!attr) {
                 SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
                 attr = true;
             }
-            kern<<<grid, kThreads, smem, s>>>(op, X, ea, m);
+            kern<<<grid, kThreads, smem, s>>>(op, ta, ea);
         };
-        switch (G) {
-        case 1: go(spmm_tile_kernel<1, MODE, EPI>); break;
-        case 2: go(spmm_tile_kernel<2, MODE, EPI>); break;
-        case 4: go(spmm_tile_kernel<4, MODE, EPI>); break;
-        case 8: go(spmm_tile_kernel<8, MODE, EPI>); break;
-        case 16: go(spmm_tile_kernel<16, MODE, EPI>); break;
-        default: go(spmm_tile_kernel<32, MODE, EPI>); break;
+        const int mr = op.max_row;
+#define SPB_TILE_CASES(GG)                                                                     \
+    if (mr <= 8) go(spmm_tile_kernel<GG, 8, 2, MODE, EPI>);                                    \
+    else if (mr <= 16) go(spmm_tile_kernel<GG, 16, 1, MODE, EPI>);                            \
+    else go(spmm_tile_kernel<GG, 32, 1, MODE, EPI>);
+        switch (Gt) {
+        case 1: SPB_TILE_CASES(1) break;
+        case 2: SPB_TILE_CASES(2) break;
+        case 4: SPB_TILE_CASES(4) break;
+        case 8: SPB_TILE_CASES(8) break;
+        case 16: SPB_TILE_CASES(16) break;
+        default: SPB_TILE_CASES(32) break;
         }
+#undef SPB_TILE_CASES
         SPB_LAUNCH_CHECK();
         return grid;
     }
@@ -354,11 +472,14 @@ int launch_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t 
 }
 
 __global__ void reduce_partials_kernel(const double* partial, int rows, int m, double* out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (c >= m) return;
     double s = 0.0;
-    for (int r = 0; r < rows; ++r) s += partial[static_cast<int64_t>(r) * m + c];
-    out[c] = s;
+    for (int r = lane; r < rows; r += 32) s += partial[static_cast<int64_t>(r) * m + c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) out[c] = s;
 }
 
 } // namespace
@@ -375,7 +496,7 @@ int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t
 }
 
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s) {
-    reduce_partials_kernel<<<1, 64, 0, s>>>(partial, rows, m, out);
+    reduce_partials_kernel<<<ceil_div(m, 4), 128, 0, s>>>(partial, rows, m, out);
     SPB_LAUNCH_CHECK();
 }
 
