@@ -15,6 +15,9 @@
 // bit-identical to the sequential sum).
 #include "ops.cuh"
 
+#include <algorithm>
+#include <vector>
+
 namespace spb {
 
 namespace {
@@ -418,10 +421,13 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
         const size_t smem = (kThreads / 32) * kTileCap *
                             (sizeof(int32_t) + ((MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) ? sizeof(double) : 0));
         auto go = [&](auto kern) {
-            static bool attr = false;
-            if (!attr) {
+            // every instantiation has the same function-pointer type: key the
+            // one-time attribute call by address
+            static std::vector<const void*> done;
+            const void* key = reinterpret_cast<const void*>(kern);
+            if (std::find(done.begin(), done.end(), key) == done.end()) {
                 SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                attr = true;
+                done.push_back(key);
             }
             kern<<<grid, kThreads, smem, s>>>(op, ta, ea);
         };
