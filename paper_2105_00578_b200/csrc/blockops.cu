@@ -20,7 +20,7 @@ namespace spb {
 namespace {
 
 constexpr int kTsThreads = 256;
-constexpr int kTR = 32;  // rows per tile
+constexpr int kTR = 64;  // rows per tile
 
 struct TsDev {
     int64_t n;
@@ -47,87 +47,96 @@ template <int N> __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// cp.async copy of rows [r0, r0+rows) x cols of view v into dst[r*ld + c0 + c]
-__device__ __forceinline__ void issue_view(double* dst, int ld, int c0, const View& v, int64_t r0, int rows,
+// Tile rows [r0, r0+rows) of view v -> smem columns [c0, c0+cols) of a row-major
+// tile with row stride ldt. Warp w copies rows w, w+8, ...; lane = column.
+__device__ __forceinline__ void issue_view(double* tile, int ldt, int c0, const View& v, int64_t r0, int rows,
                                            int cols) {
-    const int total = rows * cols;
-    if (v.cs == 1) {
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int r = idx / cols, c = idx - r * cols;
-            cp_async8(dst + r * ld + c0 + c, v.ptr + (r0 + r) * v.rs + c);
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int c = idx / rows, r = idx - c * rows;
-            cp_async8(dst + r * ld + c0 + c, v.ptr + (r0 + r) * v.rs + static_cast<int64_t>(c) * v.cs);
-        }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < rows; r += kTsThreads / 32) {
+        const double* src = v.ptr + (r0 + r) * v.rs;
+        double* dst = tile + r * ldt + c0;
+        for (int c = lane; c < cols; c += 32) cp_async8(dst + c, src + static_cast<int64_t>(c) * v.cs);
     }
 }
 
-__device__ __forceinline__ void store_tile(const View& v, const double* src, int64_t r0, int rows,
-                                           int c_begin, int cols, int src_ld) {
-    // writes src[:, c_begin : c_begin+cols] into view columns 0..cols-1
-    const int total = rows * cols;
-    if (v.cs == 1) {
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int r = idx / cols, c = idx - r * cols;
-            v.ptr[(r0 + r) * v.rs + c] = src[r * src_ld + c_begin + c];
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int c = idx / rows, r = idx - c * rows;
-            v.ptr[(r0 + r) * v.rs + c * v.cs] = src[r * src_ld + c_begin + c];
-        }
+__device__ __forceinline__ void store_view(const View& v, const double* tile, int ldt, int c0, int64_t r0,
+                                           int rows, int cols) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < rows; r += kTsThreads / 32) {
+        double* dst = v.ptr + (r0 + r) * v.rs;
+        const double* src = tile + r * ldt + c0;
+        for (int c = lane; c < cols; c += 32) dst[static_cast<int64_t>(c) * v.cs] = src[c];
     }
 }
 
-// Row tiles stream through a kStages-deep cp.async ring (tile i+2 in flight while
-// tile i is transformed / reduced), so every CTA keeps ~2 tiles of loads outstanding.
+// One smem row layout per stage: [ U (u) | V (kv) | W (kw) | b ], row stride LDT.
+// A Gram operand column is then a fixed column offset inside the row, and the
+// per-row inner loops are 4 LDS + 4 DFMA per 2x2 register block.
 template <int MAXB>
 __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
     extern __shared__ double smem[];
+    constexpr int TR = kTR;
     const int u = a.u0 + a.u1;
     const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
-    const int su = need_u ? u : 0;
-    const int stage_elems = kTR * (su + a.kv + 1);
-    double* Wt = smem + kStages * stage_elems;  // kTR x kw
-    double* Cs = Wt + kTR * a.kw;               // inner x kw
-
+    const int cu = need_u ? u : 0;
+    const int cv = cu, cw = cu + a.kv, cb = cw + a.kw;
+    const int LDT = cb + 1;
+    const int stage_elems = TR * LDT;
     const int inner = a.transform == TS_UPDATE ? u : a.kv;
+    double* Cs = smem + kStages * stage_elems;  // inner x kw, column-major
     if (a.transform != TS_NONE)
         for (int i = threadIdx.x; i < inner * a.kw; i += blockDim.x) {
             const int c = i / inner, q = i - c * inner;
             Cs[i] = a.C[q + static_cast<int64_t>(c) * a.ldc];
         }
-    const int rq = (a.transform == TS_NONE) ? a.kv : a.kw;
 
+    // transform mapping: thread -> (fixed output column, row slice)
+    const int kwp = a.kw > 0 ? a.kw : 1;
+    const int t_col = threadIdx.x % kwp;
+    const int t_r0 = threadIdx.x / kwp;
+    const int t_rstep = max(1, kTsThreads / kwp);
+    const bool t_on = t_r0 < t_rstep && a.transform != TS_NONE;
+    const int a_off = a.transform == TS_UPDATE ? 0 : cv;      // transform operand columns
+    const double* Ccol = Cs + t_col * inner;
+
+    // gram mapping: left col i -> [U | right], right col j -> right block
+    const int right_off = (a.transform == TS_NONE) ? cv : cw;
+    const int uL = a.left_u ? u : 0;
     double acc[MAXB][4];
-#pragma unroll
-    for (int i = 0; i < MAXB; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.0;
+    int lc0[MAXB], lc1[MAXB], rc0[MAXB], rc1[MAXB];
+    bool on[MAXB];
     const int nbi = (a.P + 1) / 2;
+    const int sl = (MAXB == 1) ? threadIdx.x / max(a.nb, 1) : 0;
+#pragma unroll
+    for (int bb = 0; bb < MAXB; ++bb) {
+        acc[bb][0] = acc[bb][1] = acc[bb][2] = acc[bb][3] = 0.0;
+        const int blk = (MAXB == 1) ? (threadIdx.x % max(a.nb, 1)) : (threadIdx.x + bb * blockDim.x);
+        on[bb] = a.gram && blk < a.nb && sl < a.slices;
+        const int i0 = 2 * (blk % nbi), j0 = 2 * (blk / nbi);
+        const int i1 = min(i0 + 1, a.P - 1), j1 = min(j0 + 1, a.Q - 1);
+        lc0[bb] = i0 < uL ? i0 : right_off + (i0 - uL);
+        lc1[bb] = i1 < uL ? i1 : right_off + (i1 - uL);
+        rc0[bb] = right_off + j0;
+        rc1[bb] = right_off + j1;
+    }
 
-    const int64_t ntiles = (a.n + kTR - 1) / kTR;
+    const int64_t ntiles = (a.n + TR - 1) / TR;
     const int64_t nt = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-
     auto issue = [&](int64_t i) {
-        const int64_t t = blockIdx.x + i * gridDim.x;
-        const int64_t r0 = t * kTR;
-        const int rows = static_cast<int>(min(static_cast<int64_t>(kTR), a.n - r0));
-        double* base = smem + (i % kStages) * stage_elems;
-        double* Ut = base;
-        double* Vt = base + kTR * su;
-        double* Bt = Vt + kTR * a.kv;
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        double* T = smem + (i % kStages) * stage_elems;
         if (need_u) {
-            if (a.u0) issue_view(Ut, u, 0, a.U0, r0, rows, a.u0);
-            if (a.u1) issue_view(Ut, u, a.u0, a.U1, r0, rows, a.u1);
+            if (a.u0) issue_view(T, LDT, 0, a.U0, r0, rows, a.u0);
+            if (a.u1) issue_view(T, LDT, a.u0, a.U1, r0, rows, a.u1);
         }
-        issue_view(Vt, a.kv, 0, a.V, r0, rows, a.kv);
+        issue_view(T, LDT, cv, a.V, r0, rows, a.kv);
         if (a.gram && a.b)
-            for (int r = threadIdx.x; r < rows; r += blockDim.x) cp_async8(Bt + r, a.b + r0 + r);
+            for (int r = threadIdx.x; r < rows; r += blockDim.x) cp_async8(T + r * LDT + cb, a.b + r0 + r);
     };
 
-    for (int s = 0; s < kStages - 1; ++s) {
-        if (s < nt) issue(s);
+    for (int st = 0; st < kStages - 1; ++st) {
+        if (st < nt) issue(st);
         cp_commit();
     }
     for (int64_t i = 0; i < nt; ++i) {
@@ -135,65 +144,49 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
         cp_commit();
         cp_wait<kStages - 1>();
         __syncthreads();
-        const int64_t t = blockIdx.x + i * gridDim.x;
-        const int64_t r0 = t * kTR;
-        const int rows = static_cast<int>(min(static_cast<int64_t>(kTR), a.n - r0));
-        const double* Ut = smem + (i % kStages) * stage_elems;
-        const double* Vt = Ut + kTR * su;
-        const double* Bt = Vt + kTR * a.kv;
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        double* T = smem + (i % kStages) * stage_elems;
 
-        if (a.transform == TS_UPDATE) {
-            const int total = rows * a.kw;
-            for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-                const int r = idx / a.kw, c = idx - r * a.kw;
-                double sacc = 0.0;
-                for (int q = 0; q < u; ++q) sacc = fma(Ut[r * u + q], Cs[q + c * u], sacc);
-                Wt[r * a.kw + c] = Vt[r * a.kv + c] - sacc;
-            }
-        } else if (a.transform == TS_COMBINE) {
-            const int total = rows * a.kw;
-            for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-                const int r = idx / a.kw, c = idx - r * a.kw;
-                double sacc = 0.0;
-                for (int q = 0; q < a.kv; ++q) sacc = fma(Vt[r * a.kv + q], Cs[q + c * a.kv], sacc);
-                Wt[r * a.kw + c] = sacc;
-            }
-        }
         if (a.transform != TS_NONE) {
+            if (t_on) {
+                for (int r = t_r0; r < rows; r += t_rstep) {
+                    const double* ar = T + r * LDT + a_off;
+                    double sacc = 0.0;
+                    for (int q = 0; q < inner; ++q) sacc = fma(ar[q], Ccol[q], sacc);
+                    T[r * LDT + cw + t_col] = (a.transform == TS_UPDATE) ? T[r * LDT + cv + t_col] - sacc : sacc;
+                }
+            }
             __syncthreads();
             const int w1 = min(a.kw, a.W.cols);
-            if (w1 > 0) store_tile(a.W, Wt, r0, rows, 0, w1, a.kw);
-            if (a.kw > w1) store_tile(a.W2, Wt, r0, rows, w1, a.kw - w1, a.kw);
+            if (w1 > 0) store_view(a.W, T, LDT, cw, r0, rows, w1);
+            if (a.kw > w1) store_view(a.W2, T, LDT, cw + w1, r0, rows, a.kw - w1);
         }
-        const double* right = (a.transform == TS_NONE) ? Vt : Wt;
-
         if (a.gram) {
-            // left column i: i < uL -> Ut[:, i]; else right[:, i - uL]
-            const int uL = a.left_u ? u : 0;
 #pragma unroll
             for (int bb = 0; bb < MAXB; ++bb) {
-                const int blk = (MAXB == 1) ? (threadIdx.x % a.nb) : (threadIdx.x + bb * blockDim.x);
-                const int sl = (MAXB == 1) ? (threadIdx.x / a.nb) : 0;
-                if (blk >= a.nb || sl >= a.slices) continue;
-                const int bi = blk % nbi, bj = blk / nbi;
-                const int i0 = 2 * bi, j0 = 2 * bj;
-                const bool i1ok = i0 + 1 < a.P, j1ok = j0 + 1 < a.Q;
-                for (int r = sl; r < rows; r += a.slices) {
-                    double l0, l1 = 0.0;
-                    l0 = (i0 < uL) ? Ut[r * u + i0] : right[r * rq + (i0 - uL)];
-                    if (i1ok) l1 = (i0 + 1 < uL) ? Ut[r * u + i0 + 1] : right[r * rq + (i0 + 1 - uL)];
-                    double q0 = right[r * rq + j0];
-                    double q1 = j1ok ? right[r * rq + j0 + 1] : 0.0;
+                if (!on[bb]) continue;
+                const int step = (MAXB == 1) ? a.slices : 1;
+                const int rstart = (MAXB == 1) ? sl : 0;
+                const double* row = T + rstart * LDT;
+                double a0 = acc[bb][0], a1 = acc[bb][1], a2 = acc[bb][2], a3 = acc[bb][3];
+                for (int r = rstart; r < rows; r += step, row += step * LDT) {
+                    const double l0 = row[lc0[bb]], l1 = row[lc1[bb]];
+                    double q0 = row[rc0[bb]], q1 = row[rc1[bb]];
                     if (a.b) {
-                        const double bw = Bt[r];
+                        const double bw = row[cb];
                         q0 *= bw;
                         q1 *= bw;
                     }
-                    acc[bb][0] = fma(l0, q0, acc[bb][0]);
-                    acc[bb][1] = fma(l1, q0, acc[bb][1]);
-                    acc[bb][2] = fma(l0, q1, acc[bb][2]);
-                    acc[bb][3] = fma(l1, q1, acc[bb][3]);
+                    a0 = fma(l0, q0, a0);
+                    a1 = fma(l1, q0, a1);
+                    a2 = fma(l0, q1, a2);
+                    a3 = fma(l1, q1, a3);
                 }
+                acc[bb][0] = a0;
+                acc[bb][1] = a1;
+                acc[bb][2] = a2;
+                acc[bb][3] = a3;
             }
         }
         __syncthreads();
@@ -202,6 +195,13 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
 
     if (!a.gram) return;
     double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
+    auto put = [&](int blk, const double* v) {
+        const int i0 = 2 * (blk % nbi), j0 = 2 * (blk / nbi);
+        part[i0 + j0 * a.P] = v[0];
+        if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = v[1];
+        if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = v[2];
+        if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = v[3];
+    };
     if (MAXB == 1) {
         // reduce row slices in fixed order through shared memory
         __syncthreads();
@@ -210,27 +210,16 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
         __syncthreads();
         if (threadIdx.x < a.nb) {
             const int blk = threadIdx.x;
-            const int bi = blk % nbi, bj = blk / nbi;
             double sred[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int sl = 0; sl < a.slices; ++sl)
-                for (int k = 0; k < 4; ++k) sred[k] += red[k * blockDim.x + sl * a.nb + blk];
-            const int i0 = 2 * bi, j0 = 2 * bj;
-            part[i0 + j0 * a.P] = sred[0];
-            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = sred[1];
-            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = sred[2];
-            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = sred[3];
+            for (int s2 = 0; s2 < a.slices; ++s2)
+                for (int k = 0; k < 4; ++k) sred[k] += red[k * blockDim.x + s2 * a.nb + blk];
+            put(blk, sred);
         }
     } else {
 #pragma unroll
         for (int bb = 0; bb < MAXB; ++bb) {
             const int blk = threadIdx.x + bb * blockDim.x;
-            if (blk >= a.nb) continue;
-            const int bi = blk % nbi, bj = blk / nbi;
-            const int i0 = 2 * bi, j0 = 2 * bj;
-            part[i0 + j0 * a.P] = acc[bb][0];
-            if (i0 + 1 < a.P) part[i0 + 1 + j0 * a.P] = acc[bb][1];
-            if (j0 + 1 < a.Q) part[i0 + (j0 + 1) * a.P] = acc[bb][2];
-            if (i0 + 1 < a.P && j0 + 1 < a.Q) part[i0 + 1 + (j0 + 1) * a.P] = acc[bb][3];
+            if (blk < a.nb) put(blk, acc[bb]);
         }
     }
 }
@@ -375,9 +364,9 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     const int inner = s.transform == TS_UPDATE ? u : a.kv;
     a.ldc = s.ldc > 0 ? s.ldc : inner;
     const bool need_u = (s.transform == TS_UPDATE) || (s.gram && s.gram_left_u);
-    size_t sm = sizeof(double) *
-                (static_cast<size_t>(kStages) * kTR * ((need_u ? u : 0) + a.kv + 1) +
-                 static_cast<size_t>(kTR) * a.kw + (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
+    const int LDT = (need_u ? u : 0) + a.kv + a.kw + 1;
+    size_t sm = sizeof(double) * (static_cast<size_t>(kStages) * kTR * LDT +
+                                  (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
     sm = std::max(sm, sizeof(double) * 4 * kTsThreads);
     const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / sm)));
     const int64_t ntiles = (s.n + kTR - 1) / kTR;

@@ -180,23 +180,24 @@ template <int G, int MAXR, int MODE, int EPI>
 __device__ __forceinline__ void tile_item_load(ItemLoad<MAXR, MODE>& it, const DevOp& op, const TileArgs& ta,
                                                const EpiArgs& ea, const int32_t* sc, const double* sv,
                                                const int* s_start, const int* s_len, const int* s_kd,
-                                               int64_t r0, int rr, int ch, int gl) {
+                                               int64_t r0, int rr, int ch, int gl, const char* xbase,
+                                               uint32_t ld8) {
     it.c = ch * G + gl;
     it.act = it.c < ta.m;
     it.row = r0 + rr;
     const int st = s_start[rr];
-    it.len = s_len[rr];
+    it.len = it.act ? s_len[rr] : 0;
     it.kd = s_kd[rr];
-    const int64_t grow = op.row0 + it.row;
-    const double* xc = ta.X + it.c;
-    it.xi = it.act ? xc[static_cast<int64_t>(static_cast<int>(grow) * ta.ldx)] : 0.0;
+    const char* xc = xbase + 8u * static_cast<uint32_t>(it.c);
+    const uint32_t grow = static_cast<uint32_t>(op.row0 + it.row);
+    it.xi = it.act ? *reinterpret_cast<const double*>(xc + static_cast<uint64_t>(grow) * ld8) : 0.0;
     it.h = 0.0;
     if (EPI == EPI_POLY && !ea.first && it.act) it.h = ta.H[static_cast<int>(it.row) * ta.ldh + it.c];
 #pragma unroll
     for (int k = 0; k < MAXR; ++k) {
-        if (k < it.len && it.act) {
-            const int j = sc[st + k];
-            it.xv[k] = xc[j * ta.ldx];
+        if (k < it.len) {
+            const uint32_t j = static_cast<uint32_t>(sc[st + k]);
+            it.xv[k] = __ldg(reinterpret_cast<const double*>(xc + static_cast<uint64_t>(j) * ld8));
             if (MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) it.vv[k] = sv[st + k];
         }
     }
@@ -266,6 +267,8 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
     const int gl = lane & (G - 1);
     const int gw = lane / G;
     const int nch = (ta.m + G - 1) / G;
+    const char* xbase = reinterpret_cast<const char*>(ta.X);
+    const uint32_t ld8 = 8u * static_cast<uint32_t>(ta.ldx);
     double sq = 0.0;
     const int64_t ntiles = (op.n + kTileRows - 1) / kTileRows;
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
@@ -306,14 +309,16 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
         const int items = nr * nch;
         for (int it0 = gw; it0 < items; it0 += GPW * RPI) {
             ItemLoad<MAXR, MODE> A;
-            tile_item_load<G, MAXR, MODE, EPI>(A, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, it0 / nch,
-                                               it0 % nch, gl);
+            const int rA = nch == 1 ? it0 : it0 / nch;
+            tile_item_load<G, MAXR, MODE, EPI>(A, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, rA,
+                                               it0 - rA * nch, gl, xbase, ld8);
             if (RPI == 2) {
                 const int it1 = it0 + GPW;
                 ItemLoad<MAXR, MODE> B;
+                const int rB = nch == 1 ? it1 : it1 / nch;
                 if (it1 < items)
-                    tile_item_load<G, MAXR, MODE, EPI>(B, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, it1 / nch,
-                                                       it1 % nch, gl);
+                    tile_item_load<G, MAXR, MODE, EPI>(B, op, ta, ea, sc, sv, s_start, s_len, s_kd, r0, rB,
+                                                       it1 - rB * nch, gl, xbase, ld8);
                 tile_item_finish<MAXR, MODE, EPI>(A, op, ta, ea, s_theta, sq);
                 if (it1 < items) tile_item_finish<MAXR, MODE, EPI>(B, op, ta, ea, s_theta, sq);
             } else {
@@ -398,9 +403,8 @@ template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
     int G = 1;
     while (G < m && G < 32) G <<= 1;
-    const bool rowmajor_ok = (m == 1 || X.cs == 1) && (ea.mode == EPI_STORE || ea.Y.cs == 1) &&
-                             (ea.mode != EPI_POLY || ea.H.cs == 1) &&
-                             (op.row0 + op.n) * (m == 1 ? X.rs : X.rs) < (int64_t(1) << 31) &&
+    const bool rowmajor_ok = (m == 1 || (X.cs == 1 && ea.Y.cs == 1 && (ea.mode != EPI_POLY || ea.H.cs == 1))) &&
+                             X.rs * 8 < (int64_t(1) << 32) && (op.row0 + op.n) < (int64_t(1) << 32) &&
                              op.n * ea.Y.rs < (int64_t(1) << 31);
     if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && rowmajor_ok) {
         // row-major addressing: element (r, c) at r*ld + c (m == 1 column views use ld = rs)
