@@ -334,8 +334,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     }
     ctx->prof.mark(s, "precond_build");
     const int64_t nloc = g.n_local;
-    DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d);
-    const View X = rowmajor(Xb.p, d, d);
+    DBuf<double> Xb(solver.block_elems(d));
+    const View X = solver.block(Xb.p, d);
     if (x0) upload_block(x0, n, g.row0, nloc, d, X, s);
     else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X, s);
     else initial_block_piecewise(n, d, g.row0, nloc, X, s);
@@ -568,13 +568,14 @@ sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* hg, const doubl
         DevLaplacian L;
         build_laplacian(kind, g, false, L, s);
         const int64_t n = g.n_local;
-        DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m), yd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m);
-        upload_block(X, n, 0, n, m, rowmajor(xd.p, m, m), s);
+        Solver solver(ctx, L.op, nullptr, 1);  // only for its block layout choice
+        DBuf<double> xd(solver.block_elems(m)), yd(solver.block_elems(m));
+        upload_block(X, n, 0, n, m, solver.block(xd.p, m), s);
         EpiArgs ea;
         ea.mode = EPI_STORE;
-        ea.Y = rowmajor(yd.p, m, m);
-        spmm_launch(L.op, rowmajor(xd.p, m, m), m, ea, s);
-        download_block(rowmajor(yd.p, m, m), n, m, Y, s);
+        ea.Y = solver.block(yd.p, m);
+        spmm_launch(L.op, solver.block(xd.p, m), m, ea, s);
+        download_block(solver.block(yd.p, m), n, m, Y, s);
     });
 }
 
@@ -679,8 +680,8 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
             solver.build_poly(poly_seed, poly_degree > 0 ? poly_degree : 25);
         }
         const int64_t nloc = g.n_local;
-        DBuf<double> Xb(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * nev);
-        const View X = rowmajor(Xb.p, nev, nev);
+        DBuf<double> Xb(solver.block_elems(nev));
+        const View X = solver.block(Xb.p, nev);
         upload_block(X0, hg->n, g.row0, nloc, nev, X, s);
         SolveOpts so;
         so.nev = nev;
@@ -716,10 +717,10 @@ sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* hg, uint6
         Solver solver(ctx, A.op, nullptr, m);
         solver.build_poly(seed, degree > 0 ? degree : 25);
         const int64_t n = g.n_local;
-        DBuf<double> rd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m), hd(static_cast<size_t>(std::max<int64_t>(n, 1)) * m);
-        upload_block(Rh, n, 0, n, m, rowmajor(rd.p, m, m), s);
-        solver.apply_precond(rowmajor(rd.p, m, m), m, rowmajor(hd.p, m, m));
-        download_block(rowmajor(hd.p, m, m), n, m, H_out, s);
+        DBuf<double> rd(solver.block_elems(m)), hd(solver.block_elems(m));
+        upload_block(Rh, n, 0, n, m, solver.block(rd.p, m), s);
+        solver.apply_precond(solver.block(rd.p, m), m, solver.block(hd.p, m));
+        download_block(solver.block(hd.p, m), n, m, H_out, s);
         const std::vector<double>& rt = solver.roots();
         if (roots_out) std::memcpy(roots_out, rt.data(), sizeof(double) * rt.size());
         if (achieved_out) *achieved_out = static_cast<int32_t>(rt.size());

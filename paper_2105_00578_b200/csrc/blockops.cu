@@ -48,24 +48,56 @@ template <int N> __device__ __forceinline__ void cp_wait() {
 }
 
 // Tile rows [r0, r0+rows) of view v -> smem columns [c0, c0+cols) of a row-major
-// tile with row stride ldt. Warp w copies rows w, w+8, ...; lane = column.
+// tile with row stride ldt. Column-major views (rs == 1): warp per column, lane
+// per row (coalesced 256 B per warp request). Row-major views: a flat walk over
+// the rows x cols elements with an incremental (r, c) cursor (no divisions).
 __device__ __forceinline__ void issue_view(double* tile, int ldt, int c0, const View& v, int64_t r0, int rows,
                                            int cols) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < rows; r += kTsThreads / 32) {
-        const double* src = v.ptr + (r0 + r) * v.rs;
-        double* dst = tile + r * ldt + c0;
-        for (int c = lane; c < cols; c += 32) cp_async8(dst + c, src + static_cast<int64_t>(c) * v.cs);
+    if (v.rs == 1 && cols > 1) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int c = warp; c < cols; c += kTsThreads / 32) {
+            const double* src = v.ptr + static_cast<int64_t>(c) * v.cs + r0;
+            double* dst = tile + c0 + c;
+            for (int r = lane; r < rows; r += 32) cp_async8(dst + r * ldt, src + r);
+        }
+        return;
+    }
+    const int total = rows * cols;
+    int r = threadIdx.x / cols, c = threadIdx.x - (threadIdx.x / cols) * cols;
+    const int dr = kTsThreads / cols, dc = kTsThreads - dr * cols;
+    for (int e = threadIdx.x; e < total; e += kTsThreads) {
+        cp_async8(tile + r * ldt + c0 + c, v.ptr + (r0 + r) * v.rs + static_cast<int64_t>(c) * v.cs);
+        r += dr;
+        c += dc;
+        if (c >= cols) {
+            c -= cols;
+            ++r;
+        }
     }
 }
 
 __device__ __forceinline__ void store_view(const View& v, const double* tile, int ldt, int c0, int64_t r0,
                                            int rows, int cols) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < rows; r += kTsThreads / 32) {
-        double* dst = v.ptr + (r0 + r) * v.rs;
-        const double* src = tile + r * ldt + c0;
-        for (int c = lane; c < cols; c += 32) dst[static_cast<int64_t>(c) * v.cs] = src[c];
+    if (v.rs == 1 && cols > 1) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int c = warp; c < cols; c += kTsThreads / 32) {
+            double* dst = v.ptr + static_cast<int64_t>(c) * v.cs + r0;
+            const double* src = tile + c0 + c;
+            for (int r = lane; r < rows; r += 32) dst[r] = src[r * ldt];
+        }
+        return;
+    }
+    const int total = rows * cols;
+    int r = threadIdx.x / cols, c = threadIdx.x - (threadIdx.x / cols) * cols;
+    const int dr = kTsThreads / cols, dc = kTsThreads - dr * cols;
+    for (int e = threadIdx.x; e < total; e += kTsThreads) {
+        v.ptr[(r0 + r) * v.rs + static_cast<int64_t>(c) * v.cs] = tile[r * ldt + c0 + c];
+        r += dr;
+        c += dc;
+        if (c >= cols) {
+            c -= cols;
+            ++r;
+        }
     }
 }
 
@@ -80,7 +112,7 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
     const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
     const int cu = need_u ? u : 0;
     const int cv = cu, cw = cu + a.kv, cb = cw + a.kw;
-    const int LDT = cb + 1;
+    const int LDT = (cb + 1) | 1;  // odd row stride: conflict-free column-wise smem access
     const int stage_elems = TR * LDT;
     const int inner = a.transform == TS_UPDATE ? u : a.kv;
     double* Cs = smem + kStages * stage_elems;  // inner x kw, column-major
@@ -364,7 +396,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     const int inner = s.transform == TS_UPDATE ? u : a.kv;
     a.ldc = s.ldc > 0 ? s.ldc : inner;
     const bool need_u = (s.transform == TS_UPDATE) || (s.gram && s.gram_left_u);
-    const int LDT = (need_u ? u : 0) + a.kv + a.kw + 1;
+    const int LDT = ((need_u ? u : 0) + a.kv + a.kw + 1) | 1;
     size_t sm = sizeof(double) * (static_cast<size_t>(kStages) * kTR * LDT +
                                   (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
     sm = std::max(sm, sizeof(double) * 4 * kTsThreads);

@@ -57,19 +57,20 @@ __global__ void unit_vec_kernel(int64_t n, int64_t row0, View v) {
 
 Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_cols)
     : ctx_(ctx), s_(ctx->stream), A_(A), bdiag_(bdiag), n_(A.n), max_cols_(max_cols) {
+    colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0 && !ctx->comm.active();
+    ld_ = colmajor_ ? ((std::max<int64_t>(n_, 1) + 63) / 64) * 64 : max_cols;
     const int m3 = 3 * max_cols;
-    const size_t rows = static_cast<size_t>(std::max<int64_t>(n_, 1));
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
     cmat_.alloc(static_cast<size_t>(m3) * m3 + 64);
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
     partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 + A.n_long + 64) * 64);
     norms_.alloc(64);
-    R_.alloc(rows * max_cols);
-    H_.alloc(rows * max_cols);
-    P_.alloc(rows * max_cols);
-    S_.alloc(rows * m3);
-    AS_.alloc(rows * m3);
+    R_.alloc(block_elems(max_cols));
+    H_.alloc(block_elems(max_cols));
+    P_.alloc(block_elems(max_cols));
+    S_.alloc(block_elems(m3));
+    AS_.alloc(block_elems(m3));
 }
 
 void Solver::upload(const std::vector<double>& h, DBuf<double>& d) {
@@ -139,7 +140,7 @@ void Solver::residuals(const View& X, const std::vector<double>& theta, SolveRes
     const int nev = static_cast<int>(theta.size());
     EpiArgs ea;
     ea.mode = EPI_RESIDUAL;
-    ea.Y = rowmajor(R_.p, nev, nev);
+    ea.Y = block(R_.p, nev);
     ea.bdiag = bdiag_;
     for (int j = 0; j < nev; ++j) ea.theta[j] = theta[j];
     ea.partial = partial_.p;
@@ -376,12 +377,11 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         poly_first_only(n_, 1.0 / roots_[0], R.sub(0, k), H.sub(0, k), s_);
         return;
     }
-    const size_t rows = static_cast<size_t>(std::max<int64_t>(n_, 1));
-    prodA_.alloc(rows * max_cols_);
-    prodB_.alloc(rows * max_cols_);
+    prodA_.alloc(block_elems(max_cols_));
+    prodB_.alloc(block_elems(max_cols_));
     View cur = R.sub(0, k);
     for (int i = 0; i + 1 < deg; ++i) {
-        const View nxt = rowmajor((i % 2 == 0) ? prodA_.p : prodB_.p, k, k);
+        const View nxt = block((i % 2 == 0) ? prodA_.p : prodB_.p, k);
         EpiArgs ea;
         ea.mode = EPI_POLY;
         ea.Y = nxt;
@@ -510,12 +510,12 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     res.residual_norms.assign(nev, 0.0);
 
     const int m3 = 3 * nev;
-    const View S = rowmajor(S_.p, m3, m3);
-    const View AS = rowmajor(AS_.p, m3, m3);
+    const View S = colmajor_ ? colmajor(S_.p, ld_, m3) : rowmajor(S_.p, m3, m3);
+    const View AS = colmajor_ ? colmajor(AS_.p, ld_, m3) : rowmajor(AS_.p, m3, m3);
     const View Xv = X.sub(0, nev);
-    const View Rv = rowmajor(R_.p, nev, nev);
-    const View Hv = rowmajor(H_.p, nev, nev);
-    const View Pv = rowmajor(P_.p, nev, nev);
+    const View Rv = block(R_.p, nev);
+    const View Hv = block(H_.p, nev);
+    const View Pv = block(P_.p, nev);
     int p_cols = 0;
     std::vector<double> theta;
     int iter = 0;
@@ -597,15 +597,12 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         // H_I = M(R_I)
         View RI = Rv;
         if (na != nev) {
-            gather_cols(n_, Rv, active.data(), na, rowmajor(prodB_.p ? prodB_.p : H_.p, na, na), s_);
-        }
-        if (na != nev) {
             // compact R_I into work_, then precondition into H
-            work_.alloc(static_cast<size_t>(std::max<int64_t>(n_, 1)) * nev);
-            gather_cols(n_, Rv, active.data(), na, rowmajor(work_.p, na, na), s_);
-            RI = rowmajor(work_.p, na, na);
+            work_.alloc(block_elems(nev));
+            gather_cols(n_, Rv, active.data(), na, block(work_.p, na), s_);
+            RI = block(work_.p, na);
         }
-        const View HI = rowmajor(H_.p, na, na);
+        const View HI = block(H_.p, na);
         ctx_->prof.mark(s_, "lobpcg_misc");
         apply_precond(RI, na, HI);
         ctx_->prof.mark(s_, "precond_apply");
@@ -622,7 +619,7 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
                 nh = oh.kept;
                 np = 0;
                 if (p_cols > 0) {
-                    Orth op = b_orth(rowmajor(P_.p, p_cols, p_cols), p_cols, S, nx + nh,
+                    Orth op = b_orth(block(P_.p, p_cols), p_cols, S, nx + nh,
                                      S.sub(nx + nh, m3 - nx - nh), res);
                     np = op.kept;
                 }
@@ -654,7 +651,7 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
             for (int c = 0; c < nn; ++c)
                 for (int r = 0; r < hpc; ++r)
                     Yhp[static_cast<size_t>(c) * hpc + r] = Y[static_cast<size_t>(next[c]) * m + hp + r];
-            combine_into(S.sub(hp, hpc), hpc, Yhp, nn, rowmajor(P_.p, nn, nn));
+            combine_into(S.sub(hp, hpc), hpc, Yhp, nn, block(P_.p, nn));
             p_cols = nn;
         } else {
             p_cols = 0;

@@ -4,6 +4,7 @@
 #include "context.hpp"
 #include "dense_host.hpp"
 
+#include <algorithm>
 #include <vector>
 
 namespace spb {
@@ -61,6 +62,13 @@ public:
     // Y = A X (local rows, X local block) — exposed for the kernel-level ABI.
     void spmm_store(const View& X, int m, const View& Y);
 
+    // Block layout used by this solver: column-major (ld = padded rows) for
+    // short-row operators (meshes: row-per-lane SpMM), row-major otherwise.
+    bool colmajor_blocks() const { return colmajor_; }
+    int64_t ld() const { return ld_; }
+    View block(double* p, int cols) const { return colmajor_ ? colmajor(p, ld_, cols) : rowmajor(p, cols, cols); }
+    size_t block_elems(int cols) const { return static_cast<size_t>(colmajor_ ? ld_ : std::max<int64_t>(n_, 1)) * cols; }
+
 private:
     struct Orth {
         int kept = 0;
@@ -82,6 +90,8 @@ private:
     const double* bdiag_;
     int64_t n_;       // local rows
     int max_cols_;
+    bool colmajor_ = false;
+    int64_t ld_ = 1;
     PrecKind prec_ = PREC_NONE;
     const double* inv_diag_ = nullptr;
     std::vector<double> roots_;

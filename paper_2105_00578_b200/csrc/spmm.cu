@@ -339,6 +339,116 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
     }
 }
 
+
+// Column-major "row per lane" kernel for short rows (max_row <= 32, meshes).
+// X, Y, H column-major: element (r, c) at c*ld + r. A warp owns 32 consecutive
+// rows (one per lane); each lane loads its row's column ids once, finds the
+// diagonal slot, then for every column c accumulates the row sequentially in
+// storage order (bit-identical to spmv_block). For mesh orderings the 32 lanes
+// gather 32 consecutive addresses per (entry, column): coalesced, and every
+// warp instruction serves 32 rows.
+template <int MAXR, int MODE, int EPI>
+__global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
+    __shared__ double s_sq[kThreads / 32][kMaxCols];
+    __shared__ double s_theta[kMaxCols];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int m = ta.m;
+    if (EPI == EPI_RESIDUAL) {
+        for (int c = threadIdx.x; c < m; c += kThreads) s_theta[c] = ea.theta[c];
+        for (int c = lane; c < m; c += 32) s_sq[warp][c] = 0.0;
+        __syncthreads();
+    }
+    const int64_t ntiles = (op.n + 31) / 32;
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    const uint64_t ldx8 = 8ull * static_cast<uint32_t>(ta.ldx);
+    const char* xbase = reinterpret_cast<const char*>(ta.X);
+    for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+        const int64_t row = tile * 32 + lane;
+        const bool live = row < op.n;
+        const int64_t grow = op.row0 + row;
+        int64_t k0 = 0;
+        int len = 0;
+        if (live) {
+            k0 = op.offs[row];
+            len = static_cast<int>(op.offs[row + 1] - k0);
+        }
+        uint32_t j8[MAXR];  // byte offsets of the gathered rows within a column
+        double vv[MAXR];
+        int kd = 0;
+        const double nisdi = (MODE == OP_NORMAL_UNIT && live) ? -op.isd[grow] : 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXR; ++k) {
+            j8[k] = 0;
+            vv[k] = 0.0;
+            if (k < len) {
+                const int j = __ldg(op.cols + k0 + k);
+                j8[k] = 8u * static_cast<uint32_t>(j);
+                if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) kd += (j < grow) ? 1 : 0;
+                if (MODE == OP_EXPLICIT) vv[k] = __ldg(op.vals + k0 + k);
+                if (MODE == OP_NORMAL_UNIT) vv[k] = __dmul_rn(nisdi, __ldg(op.isd + j));
+            }
+        }
+        const double dval = (MODE == OP_LAPLACE_UNIT && live) ? op.diag[row] : 0.0;
+        const uint32_t grow8 = 8u * static_cast<uint32_t>(grow);
+        for (int c = 0; c < m; ++c) {
+            const char* xc = xbase + static_cast<uint64_t>(c) * ldx8;
+            double xi = 0.0, acc = 0.0;
+            if (live) {
+                xi = *reinterpret_cast<const double*>(xc + grow8);
+                double xv[MAXR];
+#pragma unroll
+                for (int k = 0; k < MAXR; ++k)
+                    xv[k] = (k < len) ? __ldg(reinterpret_cast<const double*>(xc + j8[k])) : 0.0;
+                const double dterm = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xi) : xi;
+#pragma unroll
+                for (int k = 0; k < MAXR; ++k) {
+                    if (k < len) {
+                        if (MODE != OP_EXPLICIT && k == kd) acc = __dadd_rn(acc, dterm);
+                        if (MODE == OP_LAPLACE_UNIT) acc = __dsub_rn(acc, xv[k]);
+                        else acc = __dadd_rn(acc, __dmul_rn(vv[k], xv[k]));
+                    }
+                }
+                if (MODE != OP_EXPLICIT && kd >= len) acc = __dadd_rn(acc, dterm);
+            }
+            double sqv = 0.0;
+            if (live) {
+                const int64_t yo = static_cast<int64_t>(c) * ta.ldy + row;
+                if (EPI == EPI_STORE) {
+                    ta.Y[yo] = acc;
+                } else if (EPI == EPI_RESIDUAL) {
+                    const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[row], xi) : xi;
+                    const double r = __dsub_rn(acc, __dmul_rn(s_theta[c], bx));
+                    ta.Y[yo] = r;
+                    sqv = r * r;
+                } else {
+                    const int64_t ho = static_cast<int64_t>(c) * ta.ldh + row;
+                    const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
+                    ta.Y[yo] = pn;
+                    double h = ea.first ? __dmul_rn(ea.inv_cur, xi) : ta.H[ho];
+                    h = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
+                    ta.H[ho] = h;
+                }
+            }
+            if (EPI == EPI_RESIDUAL) {
+                // fixed-order warp tree, one lane accumulates per (warp, column)
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sqv += __shfl_xor_sync(0xffffffffu, sqv, off);
+                if (lane == 0) s_sq[warp][c] += sqv;
+            }
+        }
+    }
+    if (EPI == EPI_RESIDUAL) {
+        __syncthreads();
+        for (int c = threadIdx.x; c < m; c += kThreads) {
+            double s = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) s += s_sq[w][c];
+            ea.partial[static_cast<int64_t>(blockIdx.x) * m + c] = s;
+        }
+    }
+}
+
 // One CTA per long row (power-law hubs). Thread t accumulates entries
 // k0+t, k0+t+256, ... for every column; fixed-order warp butterfly + smem tree.
 template <int MODE, int EPI>
@@ -403,6 +513,28 @@ template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
     int G = 1;
     while (G < m && G < 32) G <<= 1;
+    // column-major blocks (regular graphs): row per lane
+    const bool colmajor = m > 1 ? (X.rs == 1 && ea.Y.rs == 1 && (ea.mode != EPI_POLY || ea.H.rs == 1))
+                                : (X.rs == 1 && ea.Y.rs == 1);
+    if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && colmajor &&
+        (op.row0 + op.n) * 8 < (int64_t(1) << 32) && m <= kMaxCols) {
+        TileArgs ta;
+        ta.X = X.ptr;
+        ta.ldx = static_cast<int>(m > 1 ? X.cs : 0);
+        ta.Y = ea.Y.ptr;
+        ta.ldy = static_cast<int>(m > 1 ? ea.Y.cs : 0);
+        ta.H = ea.H.ptr;
+        ta.ldh = static_cast<int>(ea.mode == EPI_POLY && m > 1 ? ea.H.cs : 0);
+        ta.m = m;
+        const int64_t ntiles = (op.n + 31) / 32;
+        const int grid = grid_for(ntiles, kThreads / 32, 8);
+        const int mr = op.max_row;
+        if (mr <= 8) spmm_col_kernel<8, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
+        else if (mr <= 16) spmm_col_kernel<16, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
+        else spmm_col_kernel<32, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
+        SPB_LAUNCH_CHECK();
+        return grid;
+    }
     const bool rowmajor_ok = (m == 1 || (X.cs == 1 && ea.Y.cs == 1 && (ea.mode != EPI_POLY || ea.H.cs == 1))) &&
                              X.rs * 8 < (int64_t(1) << 32) && (op.row0 + op.n) < (int64_t(1) << 32) &&
                              op.n * ea.Y.rs < (int64_t(1) << 31);
