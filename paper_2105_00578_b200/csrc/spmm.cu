@@ -374,68 +374,122 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
             k0 = op.offs[row];
             len = static_cast<int>(op.offs[row + 1] - k0);
         }
-        uint32_t j8[MAXR];  // byte offsets of the gathered rows within a column
-        double vv[MAXR];
         int kd = 0;
         const double nisdi = (MODE == OP_NORMAL_UNIT && live) ? -op.isd[grow] : 0.0;
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            j8[k] = 0;
-            vv[k] = 0.0;
-            if (k < len) {
-                const int j = __ldg(op.cols + k0 + k);
-                j8[k] = 8u * static_cast<uint32_t>(j);
-                if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) kd += (j < grow) ? 1 : 0;
-                if (MODE == OP_EXPLICIT) vv[k] = __ldg(op.vals + k0 + k);
-                if (MODE == OP_NORMAL_UNIT) vv[k] = __dmul_rn(nisdi, __ldg(op.isd + j));
-            }
+        if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) {
+            // storage slot of the diagonal: number of stored columns < grow
+            for (int k = 0; k < len; ++k) kd += (__ldg(op.cols + k0 + k) < grow) ? 1 : 0;
         }
         const double dval = (MODE == OP_LAPLACE_UNIT && live) ? op.diag[row] : 0.0;
         const uint32_t grow8 = 8u * static_cast<uint32_t>(grow);
-        for (int c = 0; c < m; ++c) {
-            const char* xc = xbase + static_cast<uint64_t>(c) * ldx8;
-            double xi = 0.0, acc = 0.0;
+        // two columns per pass (two independent accumulation chains); entries in
+        // chunks of 8: all gathers of a chunk are issued before they are summed
+        for (int c0 = 0; c0 < m; c0 += 2) {
+            const bool two = c0 + 1 < m;
+            const char* xa = xbase + static_cast<uint64_t>(c0) * ldx8;
+            const char* xb = two ? xa + ldx8 : xa;
+            double xia = 0.0, xib = 0.0;
             if (live) {
-                xi = *reinterpret_cast<const double*>(xc + grow8);
-                double xv[MAXR];
+                xia = *reinterpret_cast<const double*>(xa + grow8);
+                xib = *reinterpret_cast<const double*>(xb + grow8);
+            }
+            const double da = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xia) : xia;
+            const double db = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xib) : xib;
+            double acca = 0.0, accb = 0.0;
+            double prev_a = -0.0, prev_b = -0.0;  // term of the previous slot (shifted tail)
 #pragma unroll
-                for (int k = 0; k < MAXR; ++k)
-                    xv[k] = (k < len) ? __ldg(reinterpret_cast<const double*>(xc + j8[k])) : 0.0;
-                const double dterm = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xi) : xi;
+            for (int q = 0; q < MAXR / 8; ++q) {
+                if (q * 8 > len) break;  // warp-uniform enough; remaining slots are -0.0
+                double ta[8], tb[8];
 #pragma unroll
-                for (int k = 0; k < MAXR; ++k) {
+                for (int i = 0; i < 8; ++i) {
+                    const int k = q * 8 + i;
+                    ta[i] = -0.0;
+                    tb[i] = -0.0;
                     if (k < len) {
-                        if (MODE != OP_EXPLICIT && k == kd) acc = __dadd_rn(acc, dterm);
-                        if (MODE == OP_LAPLACE_UNIT) acc = __dsub_rn(acc, xv[k]);
-                        else acc = __dadd_rn(acc, __dmul_rn(vv[k], xv[k]));
+                        const int j = __ldg(op.cols + k0 + k);
+                        const uint32_t j8 = 8u * static_cast<uint32_t>(j);
+                        const double xa_k = __ldg(reinterpret_cast<const double*>(xa + j8));
+                        const double xb_k = __ldg(reinterpret_cast<const double*>(xb + j8));
+                        if (MODE == OP_LAPLACE_UNIT) {
+                            ta[i] = -xa_k;
+                            tb[i] = -xb_k;
+                        } else {
+                            double v;
+                            if (MODE == OP_EXPLICIT) v = __ldg(op.vals + k0 + k);
+                            else v = __dmul_rn(nisdi, __ldg(op.isd + j));
+                            ta[i] = __dmul_rn(v, xa_k);
+                            tb[i] = __dmul_rn(v, xb_k);
+                        }
                     }
                 }
-                if (MODE != OP_EXPLICIT && kd >= len) acc = __dadd_rn(acc, dterm);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k = q * 8 + i;
+                    double sa, sb;
+                    if (MODE == OP_EXPLICIT) {
+                        sa = ta[i];
+                        sb = tb[i];
+                    } else {
+                        sa = (k < kd) ? ta[i] : ((k == kd) ? da : prev_a);
+                        sb = (k < kd) ? tb[i] : ((k == kd) ? db : prev_b);
+                        prev_a = ta[i];
+                        prev_b = tb[i];
+                    }
+                    acca = __dadd_rn(acca, sa);  // slots beyond the row hold -0.0
+                    accb = __dadd_rn(accb, sb);
+                }
             }
-            double sqv = 0.0;
+            if (MODE != OP_EXPLICIT) {
+                // slot MAXR: the diagonal when every stored column is < grow, else the
+                // shifted last term (-0.0 unless the row has MAXR entries)
+                acca = __dadd_rn(acca, (kd == MAXR) ? da : prev_a);
+                accb = __dadd_rn(accb, (kd == MAXR) ? db : prev_b);
+            }
+            double sqa = 0.0, sqb = 0.0;
             if (live) {
-                const int64_t yo = static_cast<int64_t>(c) * ta.ldy + row;
+                const int64_t ya = static_cast<int64_t>(c0) * ta.ldy + row;
+                const int64_t yb = ya + ta.ldy;
                 if (EPI == EPI_STORE) {
-                    ta.Y[yo] = acc;
+                    ta.Y[ya] = acca;
+                    if (two) ta.Y[yb] = accb;
                 } else if (EPI == EPI_RESIDUAL) {
-                    const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[row], xi) : xi;
-                    const double r = __dsub_rn(acc, __dmul_rn(s_theta[c], bx));
-                    ta.Y[yo] = r;
-                    sqv = r * r;
+                    const double bd = ea.bdiag ? ea.bdiag[row] : 1.0;
+                    const double bxa = ea.bdiag ? __dmul_rn(bd, xia) : xia;
+                    const double bxb = ea.bdiag ? __dmul_rn(bd, xib) : xib;
+                    const double ra = __dsub_rn(acca, __dmul_rn(s_theta[c0], bxa));
+                    ta.Y[ya] = ra;
+                    sqa = ra * ra;
+                    if (two) {
+                        const double rb = __dsub_rn(accb, __dmul_rn(s_theta[c0 + 1], bxb));
+                        ta.Y[yb] = rb;
+                        sqb = rb * rb;
+                    }
                 } else {
-                    const int64_t ho = static_cast<int64_t>(c) * ta.ldh + row;
-                    const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
-                    ta.Y[yo] = pn;
-                    double h = ea.first ? __dmul_rn(ea.inv_cur, xi) : ta.H[ho];
-                    h = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
-                    ta.H[ho] = h;
+                    const int64_t ha = static_cast<int64_t>(c0) * ta.ldh + row;
+                    const int64_t hb = ha + ta.ldh;
+                    const double pa = __dsub_rn(xia, __dmul_rn(ea.inv_cur, acca));
+                    double h0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : ta.H[ha];
+                    ta.Y[ya] = pa;
+                    ta.H[ha] = __dadd_rn(h0, __dmul_rn(ea.inv_next, pa));
+                    if (two) {
+                        const double pb = __dsub_rn(xib, __dmul_rn(ea.inv_cur, accb));
+                        double h1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : ta.H[hb];
+                        ta.Y[yb] = pb;
+                        ta.H[hb] = __dadd_rn(h1, __dmul_rn(ea.inv_next, pb));
+                    }
                 }
             }
             if (EPI == EPI_RESIDUAL) {
-                // fixed-order warp tree, one lane accumulates per (warp, column)
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) sqv += __shfl_xor_sync(0xffffffffu, sqv, off);
-                if (lane == 0) s_sq[warp][c] += sqv;
+                for (int off = 16; off > 0; off >>= 1) {
+                    sqa += __shfl_xor_sync(0xffffffffu, sqa, off);
+                    sqb += __shfl_xor_sync(0xffffffffu, sqb, off);
+                }
+                if (lane == 0) {
+                    s_sq[warp][c0] += sqa;
+                    if (two) s_sq[warp][c0 + 1] += sqb;
+                }
             }
         }
     }
