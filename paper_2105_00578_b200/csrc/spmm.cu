@@ -342,15 +342,23 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
 
 // Column-major "row per lane" kernel for short rows (max_row <= 32, meshes).
 // X, Y, H column-major: element (r, c) at c*ld + r. A warp owns 32 consecutive
-// rows (one per lane); each lane loads its row's column ids once, finds the
-// diagonal slot, then for every column c accumulates the row sequentially in
-// storage order (bit-identical to spmv_block). For mesh orderings the 32 lanes
-// gather 32 consecutive addresses per (entry, column): coalesced, and every
-// warp instruction serves 32 rows.
+// rows (one per lane). Each lane first turns its row into MAXR slots
+// (byte offset, weight) in the exact storage order of the explicit CSR of L —
+// off-diagonals (offset j, weight -1 / (-isd_i)*isd_j / a_ij) with the diagonal
+// (offset i, weight deg / 1.0) spliced in before the first column > i — then
+// every column is a branch-free chain acc += w_k * X[c][o_k]. The products are
+// the reference's products (spmv_block: acc += a_ik * x_k), so the result is
+// bit-identical; padded slots add +-0, which cannot change an accumulator that
+// starts at +0 (round-to-nearest never produces -0 from +0 by addition).
+// For mesh orderings the 32 lanes gather 32 consecutive addresses per slot.
 template <int MAXR, int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
+    constexpr bool kRegs = MAXR <= 8;       // slots in registers, two columns per pass
+    constexpr int NS = MAXR + 1;            // + the diagonal slot
+    constexpr int NSR = kRegs ? NS : 1;
     __shared__ double s_sq[kThreads / 32][kMaxCols];
     __shared__ double s_theta[kMaxCols];
+    extern __shared__ uint32_t s_slot_dyn[];  // !kRegs: [warp][slot][lane] offsets, then weights
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
@@ -359,6 +367,8 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
         for (int c = lane; c < m; c += 32) s_sq[warp][c] = 0.0;
         __syncthreads();
     }
+    uint32_t* so = s_slot_dyn + warp * NS * 32;
+    double* sw = reinterpret_cast<double*>(s_slot_dyn + (kThreads / 32) * NS * 32) + warp * NS * 32;
     const int64_t ntiles = (op.n + 31) / 32;
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
@@ -368,86 +378,77 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
         const int64_t row = tile * 32 + lane;
         const bool live = row < op.n;
         const int64_t grow = op.row0 + row;
+        const uint32_t grow8 = 8u * static_cast<uint32_t>(live ? grow : op.row0);
         int64_t k0 = 0;
         int len = 0;
         if (live) {
             k0 = op.offs[row];
             len = static_cast<int>(op.offs[row + 1] - k0);
         }
-        int kd = 0;
-        const double nisdi = (MODE == OP_NORMAL_UNIT && live) ? -op.isd[grow] : 0.0;
-        if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) {
-            // storage slot of the diagonal: number of stored columns < grow
-            for (int k = 0; k < len; ++k) kd += (__ldg(op.cols + k0 + k) < grow) ? 1 : 0;
+        // ---- slots of this row
+        uint32_t ro[NSR];
+        double rw[NSR];
+        {
+            double dw = 0.0, nisdi = 0.0;
+            if (MODE == OP_LAPLACE_UNIT && live) dw = op.diag[row];
+            if (MODE == OP_NORMAL_UNIT && live) {
+                dw = 1.0;
+                nisdi = -op.isd[grow];
+            }
+            bool placed = (MODE == OP_EXPLICIT);
+            int k = 0;
+#pragma unroll
+            for (int sidx = 0; sidx < NS; ++sidx) {
+                uint32_t o = grow8;
+                double w = 0.0;
+                if (k < len) {
+                    const int j = __ldg(op.cols + k0 + k);
+                    if (!placed && j > grow) {
+                        w = dw;  // diagonal slot, offset = own row
+                        placed = true;
+                    } else {
+                        o = 8u * static_cast<uint32_t>(j);
+                        if (MODE == OP_LAPLACE_UNIT) w = -1.0;
+                        else if (MODE == OP_NORMAL_UNIT) w = __dmul_rn(nisdi, __ldg(op.isd + j));
+                        else w = __ldg(op.vals + k0 + k);
+                        ++k;
+                    }
+                } else if (!placed && live) {
+                    w = dw;  // diagonal after every stored column
+                    placed = true;
+                }
+                if (kRegs) {
+                    ro[sidx < NSR ? sidx : 0] = o;
+                    rw[sidx < NSR ? sidx : 0] = w;
+                } else {
+                    so[sidx * 32 + lane] = o;
+                    sw[sidx * 32 + lane] = w;
+                }
+            }
         }
-        const double dval = (MODE == OP_LAPLACE_UNIT && live) ? op.diag[row] : 0.0;
-        const uint32_t grow8 = 8u * static_cast<uint32_t>(grow);
-        // two columns per pass (two independent accumulation chains); entries in
-        // chunks of 8: all gathers of a chunk are issued before they are summed
-        for (int c0 = 0; c0 < m; c0 += 2) {
-            const bool two = c0 + 1 < m;
+        if (!kRegs) __syncwarp();
+        // ---- columns
+        constexpr int CB = kRegs ? 2 : 1;
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const bool two = CB == 2 && c0 + 1 < m;
             const char* xa = xbase + static_cast<uint64_t>(c0) * ldx8;
             const char* xb = two ? xa + ldx8 : xa;
-            double xia = 0.0, xib = 0.0;
-            if (live) {
-                xia = *reinterpret_cast<const double*>(xa + grow8);
-                xib = *reinterpret_cast<const double*>(xb + grow8);
-            }
-            const double da = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xia) : xia;
-            const double db = (MODE == OP_LAPLACE_UNIT) ? __dmul_rn(dval, xib) : xib;
             double acca = 0.0, accb = 0.0;
-            double prev_a = -0.0, prev_b = -0.0;  // term of the previous slot (shifted tail)
 #pragma unroll
-            for (int q = 0; q < MAXR / 8; ++q) {
-                if (q * 8 > len) break;  // warp-uniform enough; remaining slots are -0.0
-                double ta[8], tb[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = q * 8 + i;
-                    ta[i] = -0.0;
-                    tb[i] = -0.0;
-                    if (k < len) {
-                        const int j = __ldg(op.cols + k0 + k);
-                        const uint32_t j8 = 8u * static_cast<uint32_t>(j);
-                        const double xa_k = __ldg(reinterpret_cast<const double*>(xa + j8));
-                        const double xb_k = __ldg(reinterpret_cast<const double*>(xb + j8));
-                        if (MODE == OP_LAPLACE_UNIT) {
-                            ta[i] = -xa_k;
-                            tb[i] = -xb_k;
-                        } else {
-                            double v;
-                            if (MODE == OP_EXPLICIT) v = __ldg(op.vals + k0 + k);
-                            else v = __dmul_rn(nisdi, __ldg(op.isd + j));
-                            ta[i] = __dmul_rn(v, xa_k);
-                            tb[i] = __dmul_rn(v, xb_k);
-                        }
-                    }
+            for (int sidx = 0; sidx < NS; ++sidx) {
+                const uint32_t o = kRegs ? ro[sidx < NSR ? sidx : 0] : so[sidx * 32 + lane];
+                const double w = kRegs ? rw[sidx < NSR ? sidx : 0] : sw[sidx * 32 + lane];
+                const double ga = __ldg(reinterpret_cast<const double*>(xa + o));
+                acca = __dadd_rn(acca, __dmul_rn(w, ga));
+                if (CB == 2) {
+                    const double gb = __ldg(reinterpret_cast<const double*>(xb + o));
+                    accb = __dadd_rn(accb, __dmul_rn(w, gb));
                 }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = q * 8 + i;
-                    double sa, sb;
-                    if (MODE == OP_EXPLICIT) {
-                        sa = ta[i];
-                        sb = tb[i];
-                    } else {
-                        sa = (k < kd) ? ta[i] : ((k == kd) ? da : prev_a);
-                        sb = (k < kd) ? tb[i] : ((k == kd) ? db : prev_b);
-                        prev_a = ta[i];
-                        prev_b = tb[i];
-                    }
-                    acca = __dadd_rn(acca, sa);  // slots beyond the row hold -0.0
-                    accb = __dadd_rn(accb, sb);
-                }
-            }
-            if (MODE != OP_EXPLICIT) {
-                // slot MAXR: the diagonal when every stored column is < grow, else the
-                // shifted last term (-0.0 unless the row has MAXR entries)
-                acca = __dadd_rn(acca, (kd == MAXR) ? da : prev_a);
-                accb = __dadd_rn(accb, (kd == MAXR) ? db : prev_b);
             }
             double sqa = 0.0, sqb = 0.0;
             if (live) {
+                const double xia = *reinterpret_cast<const double*>(xa + grow8);
+                const double xib = two ? *reinterpret_cast<const double*>(xb + grow8) : 0.0;
                 const int64_t ya = static_cast<int64_t>(c0) * ta.ldy + row;
                 const int64_t yb = ya + ta.ldy;
                 if (EPI == EPI_STORE) {
@@ -456,11 +457,11 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
                 } else if (EPI == EPI_RESIDUAL) {
                     const double bd = ea.bdiag ? ea.bdiag[row] : 1.0;
                     const double bxa = ea.bdiag ? __dmul_rn(bd, xia) : xia;
-                    const double bxb = ea.bdiag ? __dmul_rn(bd, xib) : xib;
                     const double ra = __dsub_rn(acca, __dmul_rn(s_theta[c0], bxa));
                     ta.Y[ya] = ra;
                     sqa = ra * ra;
                     if (two) {
+                        const double bxb = ea.bdiag ? __dmul_rn(bd, xib) : xib;
                         const double rb = __dsub_rn(accb, __dmul_rn(s_theta[c0 + 1], bxb));
                         ta.Y[yb] = rb;
                         sqb = rb * rb;
@@ -469,12 +470,12 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
                     const int64_t ha = static_cast<int64_t>(c0) * ta.ldh + row;
                     const int64_t hb = ha + ta.ldh;
                     const double pa = __dsub_rn(xia, __dmul_rn(ea.inv_cur, acca));
-                    double h0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : ta.H[ha];
+                    const double h0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : ta.H[ha];
                     ta.Y[ya] = pa;
                     ta.H[ha] = __dadd_rn(h0, __dmul_rn(ea.inv_next, pa));
                     if (two) {
                         const double pb = __dsub_rn(xib, __dmul_rn(ea.inv_cur, accb));
-                        double h1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : ta.H[hb];
+                        const double h1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : ta.H[hb];
                         ta.Y[yb] = pb;
                         ta.H[hb] = __dadd_rn(h1, __dmul_rn(ea.inv_next, pb));
                     }
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) {
                     sqa += __shfl_xor_sync(0xffffffffu, sqa, off);
-                    sqb += __shfl_xor_sync(0xffffffffu, sqb, off);
+                    if (CB == 2) sqb += __shfl_xor_sync(0xffffffffu, sqb, off);
                 }
                 if (lane == 0) {
                     s_sq[warp][c0] += sqa;
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
                 }
             }
         }
+        if (!kRegs) __syncwarp();
     }
     if (EPI == EPI_RESIDUAL) {
         __syncthreads();
@@ -581,11 +583,29 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
         ta.ldh = static_cast<int>(ea.mode == EPI_POLY && m > 1 ? ea.H.cs : 0);
         ta.m = m;
         const int64_t ntiles = (op.n + 31) / 32;
-        const int grid = grid_for(ntiles, kThreads / 32, 8);
         const int mr = op.max_row;
-        if (mr <= 8) spmm_col_kernel<8, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
-        else if (mr <= 16) spmm_col_kernel<16, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
-        else spmm_col_kernel<32, MODE, EPI><<<grid, kThreads, 0, s>>>(op, ta, ea);
+        int grid = 0;
+        auto go = [&](auto kern, int maxr) {
+            const size_t smem = maxr <= 8 ? 0 : (kThreads / 32) * (maxr + 1) * 32 * (sizeof(uint32_t) + sizeof(double));
+            // one wave of co-resident CTAs (grid-stride loop inside)
+            static std::vector<std::pair<const void*, int>> occ;
+            const void* key = reinterpret_cast<const void*>(kern);
+            int per_sm = 0;
+            for (auto& e : occ)
+                if (e.first == key) per_sm = e.second;
+            if (!per_sm) {
+                if (smem > 48 * 1024)
+                    SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+                per_sm = std::max(per_sm, 1);
+                occ.emplace_back(key, per_sm);
+            }
+            grid = grid_for(ntiles, kThreads / 32, per_sm);
+            kern<<<grid, kThreads, smem, s>>>(op, ta, ea);
+        };
+        if (mr <= 8) go(spmm_col_kernel<8, MODE, EPI>, 8);
+        else if (mr <= 16) go(spmm_col_kernel<16, MODE, EPI>, 16);
+        else go(spmm_col_kernel<32, MODE, EPI>, 32);
         SPB_LAUNCH_CHECK();
         return grid;
     }
