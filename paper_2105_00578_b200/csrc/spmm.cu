@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
             k0 = op.offs[row];
             len = static_cast<int>(op.offs[row + 1] - k0);
         }
-        // ---- slots of this row
+        // ---- slots of this row: independent loads first, then the splice
         uint32_t ro[NSR];
         double rw[NSR];
         {
@@ -395,27 +395,40 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
                 dw = 1.0;
                 nisdi = -op.isd[grow];
             }
-            bool placed = (MODE == OP_EXPLICIT);
-            int k = 0;
+            int jv[MAXR];
+            double wv[MAXR];
+#pragma unroll
+            for (int k = 0; k < MAXR; ++k) jv[k] = (k < len) ? __ldg(op.cols + k0 + k) : 0;
+#pragma unroll
+            for (int k = 0; k < MAXR; ++k) {
+                wv[k] = 0.0;
+                if (k < len) {
+                    if (MODE == OP_LAPLACE_UNIT) wv[k] = -1.0;
+                    else if (MODE == OP_NORMAL_UNIT) wv[k] = __dmul_rn(nisdi, __ldg(op.isd + jv[k]));
+                    else wv[k] = __ldg(op.vals + k0 + k);
+                }
+            }
+            int kd = MAXR + 1;  // explicit CSR: the diagonal is a stored entry
+            if (MODE != OP_EXPLICIT) {
+                kd = 0;
+#pragma unroll
+                for (int k = 0; k < MAXR; ++k) kd += (k < len && jv[k] < grow) ? 1 : 0;
+            }
 #pragma unroll
             for (int sidx = 0; sidx < NS; ++sidx) {
+                // slot sidx holds entry sidx before the diagonal, entry sidx-1 after it
                 uint32_t o = grow8;
                 double w = 0.0;
-                if (k < len) {
-                    const int j = __ldg(op.cols + k0 + k);
-                    if (!placed && j > grow) {
-                        w = dw;  // diagonal slot, offset = own row
-                        placed = true;
-                    } else {
-                        o = 8u * static_cast<uint32_t>(j);
-                        if (MODE == OP_LAPLACE_UNIT) w = -1.0;
-                        else if (MODE == OP_NORMAL_UNIT) w = __dmul_rn(nisdi, __ldg(op.isd + j));
-                        else w = __ldg(op.vals + k0 + k);
-                        ++k;
+                if (sidx < kd) {
+                    if (sidx < MAXR && sidx < len) {
+                        o = 8u * static_cast<uint32_t>(jv[sidx < MAXR ? sidx : 0]);
+                        w = wv[sidx < MAXR ? sidx : 0];
                     }
-                } else if (!placed && live) {
-                    w = dw;  // diagonal after every stored column
-                    placed = true;
+                } else if (sidx == kd) {
+                    w = live ? dw : 0.0;
+                } else if (sidx - 1 < len) {
+                    o = 8u * static_cast<uint32_t>(jv[sidx >= 1 ? sidx - 1 : 0]);
+                    w = wv[sidx >= 1 ? sidx - 1 : 0];
                 }
                 if (kRegs) {
                     ro[sidx < NSR ? sidx : 0] = o;
@@ -433,6 +446,14 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
             const bool two = CB == 2 && c0 + 1 < m;
             const char* xa = xbase + static_cast<uint64_t>(c0) * ldx8;
             const char* xb = two ? xa + ldx8 : xa;
+            // own-row values and H issued ahead of the gathers
+            const double xia = *reinterpret_cast<const double*>(xa + grow8);
+            const double xib = two ? *reinterpret_cast<const double*>(xb + grow8) : 0.0;
+            double h0 = 0.0, h1 = 0.0;
+            if (EPI == EPI_POLY && !ea.first && live) {
+                h0 = ta.H[static_cast<int64_t>(c0) * ta.ldh + row];
+                if (two) h1 = ta.H[static_cast<int64_t>(c0 + 1) * ta.ldh + row];
+            }
             double acca = 0.0, accb = 0.0;
 #pragma unroll
             for (int sidx = 0; sidx < NS; ++sidx) {
@@ -447,8 +468,6 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
             }
             double sqa = 0.0, sqb = 0.0;
             if (live) {
-                const double xia = *reinterpret_cast<const double*>(xa + grow8);
-                const double xib = two ? *reinterpret_cast<const double*>(xb + grow8) : 0.0;
                 const int64_t ya = static_cast<int64_t>(c0) * ta.ldy + row;
                 const int64_t yb = ya + ta.ldy;
                 if (EPI == EPI_STORE) {
@@ -470,14 +489,14 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
                     const int64_t ha = static_cast<int64_t>(c0) * ta.ldh + row;
                     const int64_t hb = ha + ta.ldh;
                     const double pa = __dsub_rn(xia, __dmul_rn(ea.inv_cur, acca));
-                    const double h0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : ta.H[ha];
+                    const double ha0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : h0;
                     ta.Y[ya] = pa;
-                    ta.H[ha] = __dadd_rn(h0, __dmul_rn(ea.inv_next, pa));
+                    ta.H[ha] = __dadd_rn(ha0, __dmul_rn(ea.inv_next, pa));
                     if (two) {
                         const double pb = __dsub_rn(xib, __dmul_rn(ea.inv_cur, accb));
-                        const double h1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : ta.H[hb];
+                        const double hb1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : h1;
                         ta.Y[yb] = pb;
-                        ta.H[hb] = __dadd_rn(h1, __dmul_rn(ea.inv_next, pb));
+                        ta.H[hb] = __dadd_rn(hb1, __dmul_rn(ea.inv_next, pb));
                     }
                 }
             }
