@@ -440,75 +440,57 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
             }
         }
         if (!kRegs) __syncwarp();
-        // ---- columns
-        constexpr int CB = kRegs ? 2 : 1;
+        // ---- columns, CB per pass: CB independent accumulation chains with all
+        // CB*NS gathers and the own-row / H loads issued before the chains
+        constexpr int CB = kRegs ? 4 : 1;
         for (int c0 = 0; c0 < m; c0 += CB) {
-            const bool two = CB == 2 && c0 + 1 < m;
-            const char* xa = xbase + static_cast<uint64_t>(c0) * ldx8;
-            const char* xb = two ? xa + ldx8 : xa;
-            // own-row values and H issued ahead of the gathers
-            const double xia = *reinterpret_cast<const double*>(xa + grow8);
-            const double xib = two ? *reinterpret_cast<const double*>(xb + grow8) : 0.0;
-            double h0 = 0.0, h1 = 0.0;
-            if (EPI == EPI_POLY && !ea.first && live) {
-                h0 = ta.H[static_cast<int64_t>(c0) * ta.ldh + row];
-                if (two) h1 = ta.H[static_cast<int64_t>(c0 + 1) * ta.ldh + row];
+            const char* xcol[CB];
+            bool on[CB];
+            double xi[CB], hv[CB], acc[CB];
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                on[q] = c0 + q < m;
+                xcol[q] = xbase + static_cast<uint64_t>(on[q] ? c0 + q : c0) * ldx8;
+                xi[q] = *reinterpret_cast<const double*>(xcol[q] + grow8);
+                hv[q] = 0.0;
+                if (EPI == EPI_POLY && !ea.first && live && on[q])
+                    hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
+                acc[q] = 0.0;
             }
-            double acca = 0.0, accb = 0.0;
 #pragma unroll
             for (int sidx = 0; sidx < NS; ++sidx) {
                 const uint32_t o = kRegs ? ro[sidx < NSR ? sidx : 0] : so[sidx * 32 + lane];
                 const double w = kRegs ? rw[sidx < NSR ? sidx : 0] : sw[sidx * 32 + lane];
-                const double ga = __ldg(reinterpret_cast<const double*>(xa + o));
-                acca = __dadd_rn(acca, __dmul_rn(w, ga));
-                if (CB == 2) {
-                    const double gb = __ldg(reinterpret_cast<const double*>(xb + o));
-                    accb = __dadd_rn(accb, __dmul_rn(w, gb));
-                }
-            }
-            double sqa = 0.0, sqb = 0.0;
-            if (live) {
-                const int64_t ya = static_cast<int64_t>(c0) * ta.ldy + row;
-                const int64_t yb = ya + ta.ldy;
-                if (EPI == EPI_STORE) {
-                    ta.Y[ya] = acca;
-                    if (two) ta.Y[yb] = accb;
-                } else if (EPI == EPI_RESIDUAL) {
-                    const double bd = ea.bdiag ? ea.bdiag[row] : 1.0;
-                    const double bxa = ea.bdiag ? __dmul_rn(bd, xia) : xia;
-                    const double ra = __dsub_rn(acca, __dmul_rn(s_theta[c0], bxa));
-                    ta.Y[ya] = ra;
-                    sqa = ra * ra;
-                    if (two) {
-                        const double bxb = ea.bdiag ? __dmul_rn(bd, xib) : xib;
-                        const double rb = __dsub_rn(accb, __dmul_rn(s_theta[c0 + 1], bxb));
-                        ta.Y[yb] = rb;
-                        sqb = rb * rb;
-                    }
-                } else {
-                    const int64_t ha = static_cast<int64_t>(c0) * ta.ldh + row;
-                    const int64_t hb = ha + ta.ldh;
-                    const double pa = __dsub_rn(xia, __dmul_rn(ea.inv_cur, acca));
-                    const double ha0 = ea.first ? __dmul_rn(ea.inv_cur, xia) : h0;
-                    ta.Y[ya] = pa;
-                    ta.H[ha] = __dadd_rn(ha0, __dmul_rn(ea.inv_next, pa));
-                    if (two) {
-                        const double pb = __dsub_rn(xib, __dmul_rn(ea.inv_cur, accb));
-                        const double hb1 = ea.first ? __dmul_rn(ea.inv_cur, xib) : h1;
-                        ta.Y[yb] = pb;
-                        ta.H[hb] = __dadd_rn(hb1, __dmul_rn(ea.inv_next, pb));
-                    }
-                }
-            }
-            if (EPI == EPI_RESIDUAL) {
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    sqa += __shfl_xor_sync(0xffffffffu, sqa, off);
-                    if (CB == 2) sqb += __shfl_xor_sync(0xffffffffu, sqb, off);
+                for (int q = 0; q < CB; ++q) {
+                    const double g = __ldg(reinterpret_cast<const double*>(xcol[q] + o));
+                    acc[q] = __dadd_rn(acc[q], __dmul_rn(w, g));
                 }
-                if (lane == 0) {
-                    s_sq[warp][c0] += sqa;
-                    if (two) s_sq[warp][c0 + 1] += sqb;
+            }
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                double sq = 0.0;
+                if (live && on[q]) {
+                    const int c = c0 + q;
+                    const int64_t yo = static_cast<int64_t>(c) * ta.ldy + row;
+                    if (EPI == EPI_STORE) {
+                        ta.Y[yo] = acc[q];
+                    } else if (EPI == EPI_RESIDUAL) {
+                        const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[row], xi[q]) : xi[q];
+                        const double r = __dsub_rn(acc[q], __dmul_rn(s_theta[c], bx));
+                        ta.Y[yo] = r;
+                        sq = r * r;
+                    } else {
+                        const double pn = __dsub_rn(xi[q], __dmul_rn(ea.inv_cur, acc[q]));
+                        const double h = ea.first ? __dmul_rn(ea.inv_cur, xi[q]) : hv[q];
+                        ta.Y[yo] = pn;
+                        ta.H[static_cast<int64_t>(c) * ta.ldh + row] = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
+                    }
+                }
+                if (EPI == EPI_RESIDUAL) {
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+                    if (lane == 0 && on[q]) s_sq[warp][c0 + q] += sq;
                 }
             }
         }
