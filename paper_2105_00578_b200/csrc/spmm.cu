@@ -16,6 +16,7 @@
 #include "ops.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace spb {
@@ -351,9 +352,9 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
 // bit-identical; padded slots add +-0, which cannot change an accumulator that
 // starts at +0 (round-to-nearest never produces -0 from +0 by addition).
 // For mesh orderings the 32 lanes gather 32 consecutive addresses per slot.
-template <int MAXR, int MODE, int EPI>
-__global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
-    constexpr bool kRegs = MAXR <= 8;       // slots in registers, two columns per pass
+template <int MAXR, int MODE, int EPI, int CBT = 2, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
+    constexpr bool kRegs = MAXR <= 8;       // slots in registers, several columns per pass
     constexpr int NS = MAXR + 1;            // + the diagonal slot
     constexpr int NSR = kRegs ? NS : 1;
     __shared__ double s_sq[kThreads / 32][kMaxCols];
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(kThreads) spmm_col_kernel(const DevOp op, cons
         if (!kRegs) __syncwarp();
         // ---- columns, CB per pass: CB independent accumulation chains with all
         // CB*NS gathers and the own-row / H loads issued before the chains
-        constexpr int CB = kRegs ? 4 : 1;
+        constexpr int CB = kRegs ? CBT : 1;
         for (int c0 = 0; c0 < m; c0 += CB) {
             const char* xcol[CB];
             bool on[CB];
@@ -604,7 +605,20 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             grid = grid_for(ntiles, kThreads / 32, per_sm);
             kern<<<grid, kThreads, smem, s>>>(op, ta, ea);
         };
-        if (mr <= 8) go(spmm_col_kernel<8, MODE, EPI>, 8);
+        static const int variant = [] {
+            const char* e = std::getenv("SPB_SPMM_VARIANT");
+            return e ? std::atoi(e) : 0;
+        }();
+        if (mr <= 8) {
+            switch (variant) {
+            case 1: go(spmm_col_kernel<8, MODE, EPI, 1, 1>, 8); break;
+            case 2: go(spmm_col_kernel<8, MODE, EPI, 1, 8>, 8); break;
+            case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
+            case 4: go(spmm_col_kernel<8, MODE, EPI, 4, 3>, 8); break;
+            case 5: go(spmm_col_kernel<8, MODE, EPI, 4, 1>, 8); break;
+            default: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
+            }
+        }
         else if (mr <= 16) go(spmm_col_kernel<16, MODE, EPI>, 16);
         else go(spmm_col_kernel<32, MODE, EPI>, 32);
         SPB_LAUNCH_CHECK();
