@@ -56,7 +56,7 @@ struct EpiArgs {
     double inv_cur = 0.0;
     double inv_next = 0.0;
     int first = 0;
-    int last_h_only = 0;     // unused (kept for ABI of the struct)
+    int h_terms = 1;         // 0: H untouched, 1: H += inv_next*p_{i+1}, 2: also inv_cur*p_i first
 };
 
 // Y-block SpMM with epilogue. X is the gathered block (rows = global columns of

@@ -120,7 +120,7 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
                    8.0 * m * nrows /*X (own rows; halo counted by comm)*/ + 8.0 * m * nrows /*Y*/;
     if (A_.mode == OP_NORMAL_UNIT) bytes += 8.0 * nrows;  // isd
     if (ea.mode == EPI_RESIDUAL && ea.bdiag) bytes += 8.0 * nrows;
-    if (ea.mode == EPI_POLY) bytes += (ea.first ? 1.0 : 2.0) * 8.0 * m * nrows;
+    if (ea.mode == EPI_POLY && ea.h_terms) bytes += (ea.first ? 1.0 : 2.0) * 8.0 * m * nrows;
     ctx_->timers.spmm_bytes += bytes;
     (void)rows;
     if (ea.mode == EPI_RESIDUAL) {
@@ -389,6 +389,8 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         ea.inv_cur = 1.0 / roots_[i];
         ea.inv_next = 1.0 / roots_[i + 1];
         ea.first = (i == 0);
+        // H absorbs (p_i, p_{i+1}) on even steps, the trailing p_{deg-1} on a final odd step
+        ea.h_terms = (i % 2 == 0) ? 2 : (i + 2 == deg ? 1 : 0);
         spmm(cur, k, ea);
         cur = nxt;
     }

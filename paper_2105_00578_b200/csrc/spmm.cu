@@ -76,6 +76,15 @@ struct RowAcc {
     }
 };
 
+// H accumulation of the product-form polynomial (preconditioners.cpp:184-185),
+// in the reference's order: h_terms == 2 adds inv_cur*p_i then inv_next*p_{i+1};
+// h_terms == 1 adds inv_next*p_{i+1} only; `first` starts from H = 0.
+__device__ __forceinline__ double poly_h(const EpiArgs& ea, double hold, double xi, double pn) {
+    double h = hold;
+    if (ea.h_terms == 2) h = ea.first ? __dmul_rn(ea.inv_cur, xi) : __dadd_rn(h, __dmul_rn(ea.inv_cur, xi));
+    return __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue(const EpiArgs& ea, int64_t row, int c, double acc,
                                          double xi, double& sq) {
@@ -92,9 +101,7 @@ __device__ __forceinline__ void epilogue(const EpiArgs& ea, int64_t row, int c, 
         // (preconditioners.cpp:183-190, unrolled one step ahead)
         const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
         ea.Y.at(row, c) = pn;
-        double h = ea.first ? __dmul_rn(ea.inv_cur, xi) : ea.H.at(row, c);
-        h = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
-        ea.H.at(row, c) = h;
+        if (ea.h_terms) ea.H.at(row, c) = poly_h(ea, ea.first ? 0.0 : ea.H.at(row, c), xi, pn);
     }
 }
 
@@ -193,7 +200,7 @@ __device__ __forceinline__ void tile_item_load(ItemLoad<MAXR, MODE>& it, const D
     const uint32_t grow = static_cast<uint32_t>(op.row0 + it.row);
     it.xi = it.act ? *reinterpret_cast<const double*>(xc + static_cast<uint64_t>(grow) * ld8) : 0.0;
     it.h = 0.0;
-    if (EPI == EPI_POLY && !ea.first && it.act) it.h = ta.H[static_cast<int>(it.row) * ta.ldh + it.c];
+    if (EPI == EPI_POLY && !ea.first && ea.h_terms && it.act) it.h = ta.H[static_cast<int>(it.row) * ta.ldh + it.c];
 #pragma unroll
     for (int k = 0; k < MAXR; ++k) {
         if (k < it.len) {
@@ -239,9 +246,7 @@ __device__ __forceinline__ void tile_item_finish(const ItemLoad<MAXR, MODE>& it,
     } else {
         const double pn = __dsub_rn(it.xi, __dmul_rn(ea.inv_cur, acc));
         ta.Y[yoff] = pn;
-        double h = ea.first ? __dmul_rn(ea.inv_cur, it.xi) : it.h;
-        h = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
-        ta.H[static_cast<int>(it.row) * ta.ldh + it.c] = h;
+        if (ea.h_terms) ta.H[static_cast<int>(it.row) * ta.ldh + it.c] = poly_h(ea, it.h, it.xi, pn);
     }
 }
 
@@ -454,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
                 xcol[q] = xbase + static_cast<uint64_t>(on[q] ? c0 + q : c0) * ldx8;
                 xi[q] = *reinterpret_cast<const double*>(xcol[q] + grow8);
                 hv[q] = 0.0;
-                if (EPI == EPI_POLY && !ea.first && live && on[q])
+                if (EPI == EPI_POLY && !ea.first && ea.h_terms && live && on[q])
                     hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
                 acc[q] = 0.0;
             }
@@ -483,9 +488,9 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
                         sq = r * r;
                     } else {
                         const double pn = __dsub_rn(xi[q], __dmul_rn(ea.inv_cur, acc[q]));
-                        const double h = ea.first ? __dmul_rn(ea.inv_cur, xi[q]) : hv[q];
                         ta.Y[yo] = pn;
-                        ta.H[static_cast<int64_t>(c) * ta.ldh + row] = __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
+                        if (ea.h_terms)
+                            ta.H[static_cast<int64_t>(c) * ta.ldh + row] = poly_h(ea, hv[q], xi[q], pn);
                     }
                 }
                 if (EPI == EPI_RESIDUAL) {
@@ -613,10 +618,10 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             switch (variant) {
             case 1: go(spmm_col_kernel<8, MODE, EPI, 1, 1>, 8); break;
             case 2: go(spmm_col_kernel<8, MODE, EPI, 1, 8>, 8); break;
-            case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
+            case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
             case 4: go(spmm_col_kernel<8, MODE, EPI, 4, 3>, 8); break;
             case 5: go(spmm_col_kernel<8, MODE, EPI, 4, 1>, 8); break;
-            default: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
+            default: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
             }
         }
         else if (mr <= 16) go(spmm_col_kernel<16, MODE, EPI>, 16);
