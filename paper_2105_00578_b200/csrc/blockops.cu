@@ -14,6 +14,7 @@
 #include "ops.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace spb {
 
@@ -256,6 +257,160 @@ __global__ void __launch_bounds__(kTsThreads) ts_tile_kernel(const TsDev a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core variant (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4). Same
+// staging and smem row layout as ts_tile_kernel; the block transform is a
+// (64 x inner) x (inner x kw) product per tile (warp w owns rows 8w..8w+7) and
+// the Gram is L^T diag(b) R with K = tile rows, 8x8 output blocks spread over
+// warps by (block, k-step group). Per-warp fragments are combined in a fixed
+// order, so results are run-to-run deterministic.
+constexpr int kMaxItems = 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kTsThreads) ts_mma_kernel(const TsDev a) {
+    extern __shared__ double smem[];
+    constexpr int TR = kTR;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int u = a.u0 + a.u1;
+    const bool need_u = (a.transform == TS_UPDATE) || (a.gram && a.left_u);
+    const int cu = need_u ? u : 0;
+    const int cv = cu, cw = cu + a.kv, cb = cw + a.kw;
+    const int LDT = (cb + 1) | 1;
+    const int stage_elems = TR * LDT;
+    const int inner = a.transform == TS_UPDATE ? u : a.kv;
+    double* Cs = smem + kStages * stage_elems;  // inner x kw, column-major
+    if (a.transform != TS_NONE)
+        for (int i = threadIdx.x; i < inner * a.kw; i += blockDim.x) {
+            const int c = i / inner, q = i - c * inner;
+            Cs[i] = a.C[q + static_cast<int64_t>(c) * a.ldc];
+        }
+    const int a_off = a.transform == TS_UPDATE ? 0 : cv;
+    const int right_off = (a.transform == TS_NONE) ? cv : cw;
+    const int uL = a.left_u ? u : 0;
+
+    // gram work items: (8x8 block, k-step group)
+    const int MB = (a.P + 7) / 8, NB = (a.Q + 7) / 8, nblk = MB * NB;
+    const int kgroups = a.gram ? max(1, min(16, 8 / max(nblk, 1))) : 1;
+    const int nitems = nblk * kgroups;
+    double acc0[kMaxItems], acc1[kMaxItems];
+    int lcol[kMaxItems], rcol[kMaxItems], kgi[kMaxItems];
+    bool lok[kMaxItems], rok[kMaxItems], ion[kMaxItems];
+#pragma unroll
+    for (int t = 0; t < kMaxItems; ++t) {
+        const int item = warp + t * (kTsThreads / 32);
+        ion[t] = a.gram && item < nitems;
+        const int blk = item % max(nblk, 1), kg = item / max(nblk, 1);
+        const int mb = blk % max(MB, 1), nb = blk / max(MB, 1);
+        const int mrow = mb * 8 + gid, ncol = nb * 8 + gid;
+        lok[t] = mrow < a.P;
+        rok[t] = ncol < a.Q;
+        lcol[t] = mrow < uL ? mrow : right_off + (mrow - uL);
+        rcol[t] = right_off + ncol;
+        kgi[t] = kg;
+        acc0[t] = acc1[t] = 0.0;
+    }
+
+    const int64_t ntiles = (a.n + TR - 1) / TR;
+    const int64_t nt = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](int64_t i) {
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        double* T = smem + (i % kStages) * stage_elems;
+        if (need_u) {
+            if (a.u0) issue_view(T, LDT, 0, a.U0, r0, rows, a.u0);
+            if (a.u1) issue_view(T, LDT, a.u0, a.U1, r0, rows, a.u1);
+        }
+        issue_view(T, LDT, cv, a.V, r0, rows, a.kv);
+        if (a.gram && a.b)
+            for (int r = threadIdx.x; r < rows; r += blockDim.x) cp_async8(T + r * LDT + cb, a.b + r0 + r);
+        // zero the rows of a short tail tile so the fixed-size MMA steps read zeros
+        for (int e = threadIdx.x; e < (TR - rows) * LDT; e += blockDim.x) T[rows * LDT + e] = 0.0;
+    };
+
+    for (int st = 0; st < kStages - 1; ++st) {
+        if (st < nt) issue(st);
+        cp_commit();
+    }
+    for (int64_t i = 0; i < nt; ++i) {
+        if (i + kStages - 1 < nt) issue(i + kStages - 1);
+        cp_commit();
+        cp_wait<kStages - 1>();
+        __syncthreads();
+        const int64_t r0 = (blockIdx.x + i * gridDim.x) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        double* T = smem + (i % kStages) * stage_elems;
+
+        if (a.transform != TS_NONE) {
+            // rows 8*warp .. 8*warp+7 of W = A_in * C  (UPDATE: W = V - U*C)
+            const double* arow = T + (warp * 8 + gid) * LDT + a_off;
+            for (int nb = 0; nb * 8 < a.kw; ++nb) {
+                double d0 = 0.0, d1 = 0.0;
+                const int n = nb * 8 + gid;
+                const double* ccol = Cs + min(n, a.kw - 1) * inner;
+                for (int k0 = 0; k0 < inner; k0 += 4) {
+                    const int k = k0 + tig;
+                    const double av = k < inner ? arow[k] : 0.0;
+                    const double bv = (k < inner && n < a.kw) ? ccol[k] : 0.0;
+                    dmma(d0, d1, av, bv);
+                }
+                // d0, d1 = W[8*warp + gid][nb*8 + 2*tig + {0,1}]
+                const int r = warp * 8 + gid;
+                const int c0 = nb * 8 + 2 * tig;
+                double* wrow = T + r * LDT;
+                if (c0 < a.kw) wrow[cw + c0] = (a.transform == TS_UPDATE) ? wrow[cv + c0] - d0 : d0;
+                if (c0 + 1 < a.kw) wrow[cw + c0 + 1] = (a.transform == TS_UPDATE) ? wrow[cv + c0 + 1] - d1 : d1;
+            }
+            __syncthreads();
+            const int w1 = min(a.kw, a.W.cols);
+            if (w1 > 0) store_view(a.W, T, LDT, cw, r0, rows, w1);
+            if (a.kw > w1) store_view(a.W2, T, LDT, cw + w1, r0, rows, a.kw - w1);
+        }
+        if (a.gram) {
+#pragma unroll
+            for (int t = 0; t < kMaxItems; ++t) {
+                if (!ion[t]) continue;
+                for (int ks = kgi[t]; ks < TR / 4; ks += kgroups) {
+                    const double* row = T + (ks * 4 + tig) * LDT;
+                    const double av = lok[t] ? row[lcol[t]] : 0.0;
+                    double bv = rok[t] ? row[rcol[t]] : 0.0;
+                    if (a.b) bv *= row[cb];
+                    dmma(acc0[t], acc1[t], av, bv);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+
+    if (!a.gram) return;
+    // fixed-order reduction: fragments -> smem [item][64] -> sum over k-groups per block
+    __syncthreads();
+    double* red = smem;  // nitems x 64
+#pragma unroll
+    for (int t = 0; t < kMaxItems; ++t) {
+        if (!ion[t]) continue;
+        const int item = warp + t * (kTsThreads / 32);
+        red[item * 64 + gid * 8 + 2 * tig] = acc0[t];
+        red[item * 64 + gid * 8 + 2 * tig + 1] = acc1[t];
+    }
+    __syncthreads();
+    double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
+    for (int e = threadIdx.x; e < a.P * a.Q; e += blockDim.x) {
+        const int i = e % a.P, j = e / a.P;
+        const int blk = (i / 8) + (j / 8) * MB;
+        const int off = (i % 8) * 8 + (j % 8);
+        double sum = 0.0;
+        for (int kg = 0; kg < kgroups; ++kg) sum += red[(kg * nblk + blk) * 64 + off];
+        part[i + j * a.P] = sum;
+    }
+}
+
 // One warp per Gram entry: lane l sums partial rows l, l+32, ... then a fixed
 // butterfly — deterministic for a fixed grid.
 __global__ void reduce_gram_kernel(const double* partial, int rows, int PQ, double* out) {
@@ -354,6 +509,11 @@ int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s) {
     return grid;
 }
 
+bool ts_force_cuda_cores() {
+    static const bool v = std::getenv("SPB_TS_NO_MMA") != nullptr;
+    return v;
+}
+
 int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_elems, cudaStream_t st) {
     TsDev a{};
     a.n = s.n;
@@ -416,7 +576,17 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
         if (sm > 48 * 1024) SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         kern<<<grid, kTsThreads, sm, st>>>(a);
     };
-    if (maxb <= 1) launch(ts_tile_kernel<1>);
+    const int nblk = ((a.P + 7) / 8) * ((a.Q + 7) / 8);
+    const bool mma_ok = !ts_force_cuda_cores() && (!a.gram || nblk <= kMaxItems * (kTsThreads / 32));
+    if (mma_ok) {
+        // reduction scratch: nitems x 64 doubles must fit in the staged smem
+        const int kgroups = a.gram ? std::max(1, std::min(16, 8 / std::max(nblk, 1))) : 1;
+        const size_t need = sizeof(double) * 64 * static_cast<size_t>(nblk * kgroups);
+        size_t sm2 = std::max(sm, need);
+        if (sm2 > 48 * 1024)
+            SPB_CUDA(cudaFuncSetAttribute(ts_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
+        ts_mma_kernel<<<grid, kTsThreads, sm2, st>>>(a);
+    } else if (maxb <= 1) launch(ts_tile_kernel<1>);
     else if (maxb <= 2) launch(ts_tile_kernel<2>);
     else if (maxb <= 4) launch(ts_tile_kernel<4>);
     else if (maxb <= 8) launch(ts_tile_kernel<8>);
