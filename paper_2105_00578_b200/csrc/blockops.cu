@@ -714,7 +714,8 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     auto cm = [](const View& v, int cols) { return cols == 0 || v.rs == 1; };
     const bool colmajor_all = cm(s.U0, a.u0) && cm(s.U1, a.u1) && cm(s.V, a.kv) &&
                               (s.transform == TS_NONE || (cm(s.W, s.W.cols) && (!s.W2.ptr || cm(s.W2, s.W2.cols))));
-    if (colmajor_all && !ts_force_cuda_cores() && (s.transform == TS_NONE || (inner <= 32 && a.kw <= 32)) &&
+    static const bool direct = std::getenv("SPB_TS_DIRECT") != nullptr;  // experimental, off by default
+    if (direct && colmajor_all && !ts_force_cuda_cores() && (s.transform == TS_NONE || (inner <= 32 && a.kw <= 32)) &&
         (!a.gram || (a.P <= 40 && a.Q <= 32))) {
         const int KB = (inner + 3) / 4, NBW = (a.kw + 7) / 8;
         const int MBG = a.gram ? (a.P + 7) / 8 : 0, NBG = a.gram ? (a.Q + 7) / 8 : 0;
