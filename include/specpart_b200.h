@@ -139,6 +139,10 @@ typedef struct sp_report {
     double spmm_ms;
     int32_t kernel_launches;
     int32_t n_gpus;
+    /* the GMRES-polynomial step SpMM (the dominant kernel with precond=polynomial) */
+    int64_t poly_launches;
+    double poly_bytes;
+    double poly_ms;
     /* caller-provided outputs (may be NULL) */
     double* part_weights;          /* num_parts */
     sp_trace_record* trace;        /* trace_capacity records */

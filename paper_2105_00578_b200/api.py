@@ -190,7 +190,8 @@ def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> 
                "partition_s": r.partition_s, "total_s": r.total_s},
         cutsize=r.cutsize, imbalance=r.imbalance, part_weights=list(part_weights), trace=trace,
         device={"spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
-                "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus})
+                "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus,
+                "poly_launches": r.poly_launches, "poly_bytes": r.poly_bytes, "poly_ms": r.poly_ms})
 
 
 def _ptr(a):

@@ -381,6 +381,9 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     R.spmm_launches = ctx->timers.spmm_launches;
     R.spmm_bytes = ctx->timers.spmm_bytes;
     R.spmm_ms = ctx->timers.spmm_ms;
+    R.poly_launches = ctx->timers.poly_launches;
+    R.poly_bytes = ctx->timers.poly_bytes;
+    R.poly_ms = ctx->timers.poly_ms;
     R.kernel_launches = static_cast<int32_t>(launch_counter() - launches0 + ctx->timers.kernel_launches);
     R.n_gpus = ctx->comm.world;
     if (rep) {

@@ -75,6 +75,9 @@ struct Timers {
     int64_t spmm_launches = 0;
     double spmm_bytes = 0.0;
     int64_t kernel_launches = 0;
+    double poly_ms = 0.0;
+    int64_t poly_launches = 0;
+    double poly_bytes = 0.0;
 };
 
 } // namespace spb
@@ -90,15 +93,18 @@ struct sp_context {
     // event pairs recorded around SpMM launches; resolved without extra syncs
     // once the pipeline has synchronized (collect_spmm_times)
     std::vector<cudaEvent_t> evpool;
+    std::vector<char> ev_poly;  // per event pair: was it a polynomial-step launch
     size_t ev_used = 0;
     spb::PhaseProf prof;
 
-    std::pair<cudaEvent_t, cudaEvent_t> next_event_pair() {
+    std::pair<cudaEvent_t, cudaEvent_t> next_event_pair(bool poly = false) {
         while (evpool.size() < ev_used + 2) {
             cudaEvent_t e;
             SPB_CUDA(cudaEventCreate(&e));
             evpool.push_back(e);
         }
+        if (ev_poly.size() < ev_used / 2 + 1) ev_poly.resize(ev_used / 2 + 1);
+        ev_poly[ev_used / 2] = poly;
         auto p = std::make_pair(evpool[ev_used], evpool[ev_used + 1]);
         ev_used += 2;
         return p;
@@ -107,7 +113,10 @@ struct sp_context {
     void collect_spmm_times() {
         for (size_t i = 0; i + 1 < ev_used; i += 2) {
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, evpool[i], evpool[i + 1]) == cudaSuccess) timers.spmm_ms += ms;
+            if (cudaEventElapsedTime(&ms, evpool[i], evpool[i + 1]) == cudaSuccess) {
+                timers.spmm_ms += ms;
+                if (ev_poly[i / 2]) timers.poly_ms += ms;
+            }
         }
         ev_used = 0;
     }

@@ -106,7 +106,7 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     const bool timed = ctx_->time_spmm;
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
     if (timed) {
-        ev = ctx_->next_event_pair();
+        ev = ctx_->next_event_pair(ea.mode == EPI_POLY);
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
     const int rows = spmm_launch(A_, Xg, m, ea, s_);
@@ -122,6 +122,10 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     if (ea.mode == EPI_RESIDUAL && ea.bdiag) bytes += 8.0 * nrows;
     if (ea.mode == EPI_POLY && ea.h_terms) bytes += (ea.first ? 1.0 : 2.0) * 8.0 * m * nrows;
     ctx_->timers.spmm_bytes += bytes;
+    if (ea.mode == EPI_POLY) {
+        ctx_->timers.poly_bytes += bytes;
+        ctx_->timers.poly_launches += 1;
+    }
     (void)rows;
     if (ea.mode == EPI_RESIDUAL) {
         reduce_partials(ea.partial, rows, m, norms_.p, s_);
