@@ -73,13 +73,31 @@ def build(verbose: bool = False) -> Path:
         objs = list(ex.map(lambda s: _compile(s, hm, verbose), srcs))
     newest = max(o.stat().st_mtime for o in objs)
     if not LIB.exists() or LIB.stat().st_mtime < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lnccl", "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    _build_shim_test(verbose)
     return LIB
+
+
+def _build_shim_test(verbose: bool) -> None:
+    """tests/cpp/shim_test.cpp against include/specpart_b200.hpp + the library (a reference-style
+    C++ caller that compiles unchanged against the shim)."""
+    src = ROOT / "tests" / "cpp" / "shim_test.cpp"
+    exe = ROOT / "build" / "shim_test"
+    if not src.exists():
+        return
+    if exe.exists() and exe.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime,
+                                                   (ROOT / "include" / "specpart_b200.hpp").stat().st_mtime):
+        return
+    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), str(src), "-L", str(PKG), "-lspecpart_b200",
+           "-Wl,-rpath,$ORIGIN/../paper_2105_00578_b200", "-o", str(exe)]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
 
 
 if __name__ == "__main__":

@@ -126,7 +126,7 @@ void prepare_graph(sp_context* ctx, DevGraph& g) {
         DBuf<int64_t> t(cm.world), one(1);
         int64_t v = g.max_degree_local;
         h2d(one.p, &v, 1, s);
-        SPB_NCCL(ncclAllGather(one.p, t.p, 1, ncclInt64, cm.nccl, s));
+        SPB_NCCL(::spb::nccl().AllGather(one.p, t.p, 1, ncclInt64, cm.nccl, s));
         std::vector<int64_t> h(cm.world);
         SPB_CUDA(cudaMemcpyAsync(h.data(), t.p, sizeof(int64_t) * cm.world, cudaMemcpyDeviceToHost, s));
         int64_t flags[2] = {g.unit_values ? 0 : 1, g.positive_degrees_local ? 0 : 1};
@@ -308,6 +308,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
 
     DevLaplacian A;
     build_laplacian(operator_kind(R.problem), g, false, A, s);
+    A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
     if (!kind.regular) collect_long_rows(g, A, 4096, s);
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {
@@ -440,9 +441,13 @@ sp_status sp_context_create(int device, sp_context** out) {
 sp_status sp_nccl_unique_id(void* out128) {
     if (!out128) return SP_INVALID;
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-    ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) return SP_NCCL;
-    std::memcpy(out128, &id, sizeof(id));
+    try {
+        ncclUniqueId id;
+        if (nccl().GetUniqueId(&id) != ncclSuccess) return SP_NCCL;
+        std::memcpy(out128, &id, sizeof(id));
+    } catch (...) {
+        return SP_NCCL;
+    }
     return SP_OK;
 }
 
@@ -454,7 +459,7 @@ sp_status sp_context_create_dist(int device, int rank, int world, const void* nc
     try {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id128, sizeof(id));
-        SPB_NCCL(ncclCommInitRank(&c->comm.nccl, world, id, rank));
+        SPB_NCCL(nccl().CommInitRank(&c->comm.nccl, world, id, rank));
         c->comm.rank = rank;
         c->comm.world = world;
     } catch (...) {
@@ -469,7 +474,7 @@ sp_status sp_context_create_dist(int device, int rank, int world, const void* nc
 void sp_context_destroy(sp_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->comm.nccl) ncclCommDestroy(c->comm.nccl);
+    if (c->comm.nccl) nccl().CommDestroy(c->comm.nccl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -669,6 +674,7 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
         upload_graph(ctx, hg, g);
         DevLaplacian A;
         build_laplacian(operator_kind(problem), g, false, A, s);
+        A.op.bound = ctx->comm.max_f64(A.op.bound, s);
         const double* bdiag = nullptr;
         if (problem == SP_PROBLEM_GENERALIZED) {
             if (!g.positive_degrees) throw_degenerate("generalized problem requires positive degrees");

@@ -9,6 +9,10 @@
 #include "context.hpp"
 
 #include <chrono>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <vector>
 #include <cstdio>
 
 namespace spb {
@@ -42,6 +46,30 @@ __global__ void ordered_sum_i64_kernel(const int64_t* parts, int world, int coun
 }
 
 } // namespace
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static bool loaded = false;
+    if (loaded) return api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw SpError(9, std::string("NCCL: cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* name) {
+        void* f = dlsym(h, name);
+        if (!f) throw SpError(9, std::string("NCCL: missing symbol ") + name);
+        return f;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+    return api;
+}
 
 double PhaseProf::now() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -82,7 +110,7 @@ View Comm::gather_rows(const View& local, int m, cudaStream_t s) {
         pack_kernel<<<grid_for(nl * m, 256, 8), 256, 0, s>>>(nl, local, stage.p, m);
         SPB_LAUNCH_CHECK();
     }
-    SPB_NCCL(ncclAllGather(stage.p, full.p, static_cast<size_t>(n_pad) * m, ncclDouble, nccl, s));
+    SPB_NCCL(::spb::nccl().AllGather(stage.p, full.p, static_cast<size_t>(n_pad) * m, ncclDouble, nccl, s));
     bytes_moved += static_cast<int64_t>(n_pad) * m * 8 * (world - 1);
     return rowmajor(full.p, m, m);
 }
@@ -90,7 +118,7 @@ View Comm::gather_rows(const View& local, int m, cudaStream_t s) {
 void Comm::sum_small(double* dev, int count, cudaStream_t s) {
     if (!active() || count <= 0) return;
     small.alloc(static_cast<size_t>(count) * world);
-    SPB_NCCL(ncclAllGather(dev, small.p, count, ncclDouble, nccl, s));
+    SPB_NCCL(::spb::nccl().AllGather(dev, small.p, count, ncclDouble, nccl, s));
     ordered_sum_kernel<<<ceil_div(count, 128), 128, 0, s>>>(small.p, world, count, dev);
     SPB_LAUNCH_CHECK();
 }
@@ -98,10 +126,23 @@ void Comm::sum_small(double* dev, int count, cudaStream_t s) {
 void Comm::sum_i64(int64_t* dev, int count, cudaStream_t s) {
     if (!active() || count <= 0) return;
     DBuf<int64_t> tmp(static_cast<size_t>(count) * world);
-    SPB_NCCL(ncclAllGather(dev, tmp.p, count, ncclInt64, nccl, s));
+    SPB_NCCL(::spb::nccl().AllGather(dev, tmp.p, count, ncclInt64, nccl, s));
     ordered_sum_i64_kernel<<<ceil_div(count, 128), 128, 0, s>>>(tmp.p, world, count, dev);
     SPB_LAUNCH_CHECK();
     SPB_CUDA(cudaStreamSynchronize(s));
+}
+
+double Comm::max_f64(double v, cudaStream_t s) {
+    if (!active()) return v;
+    DBuf<double> one(1), all(world);
+    SPB_CUDA(cudaMemcpyAsync(one.p, &v, sizeof(double), cudaMemcpyHostToDevice, s));
+    SPB_NCCL(::spb::nccl().AllGather(one.p, all.p, 1, ncclDouble, nccl, s));
+    std::vector<double> h(world);
+    SPB_CUDA(cudaMemcpyAsync(h.data(), all.p, sizeof(double) * world, cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    double m = h[0];
+    for (double x : h) m = std::max(m, x);
+    return m;
 }
 
 void Comm::gather_i32(const int32_t* local, int32_t* global, cudaStream_t s) {
@@ -110,7 +151,7 @@ void Comm::gather_i32(const int32_t* local, int32_t* global, cudaStream_t s) {
         return;
     }
     // local must hold n_pad entries (the tail beyond nloc() is ignored by readers)
-    SPB_NCCL(ncclAllGather(local, global, n_pad, ncclInt32, nccl, s));
+    SPB_NCCL(::spb::nccl().AllGather(local, global, n_pad, ncclInt32, nccl, s));
 }
 
 void Comm::gather_f64(const double* local, double* global, cudaStream_t s) {
@@ -118,7 +159,7 @@ void Comm::gather_f64(const double* local, double* global, cudaStream_t s) {
         SPB_CUDA(cudaMemcpyAsync(global, local, sizeof(double) * n_global, cudaMemcpyDeviceToDevice, s));
         return;
     }
-    SPB_NCCL(ncclAllGather(local, global, n_pad, ncclDouble, nccl, s));
+    SPB_NCCL(::spb::nccl().AllGather(local, global, n_pad, ncclDouble, nccl, s));
 }
 
 } // namespace spb

@@ -4,7 +4,7 @@
 
 #include "graph_dev.cuh"
 
-#include <nccl.h>
+#include "nccl_dyn.hpp"
 
 #include <string>
 #include <utility>
@@ -16,7 +16,7 @@ namespace spb {
     do {                                                                                 \
         ncclResult_t _r = (call);                                                        \
         if (_r != ncclSuccess)                                                           \
-            throw ::spb::SpError(9, std::string("NCCL: ") + ncclGetErrorString(_r) + " at " + \
+            throw ::spb::SpError(9, std::string("NCCL: ") + ::spb::nccl().GetErrorString(_r) + " at " + \
                                         __FILE__ + ":" + std::to_string(__LINE__));      \
     } while (0)
 
@@ -53,6 +53,8 @@ struct Comm {
     void sum_small(double* dev, int count, cudaStream_t s);
     // Sum of int64 counters (exact).
     void sum_i64(int64_t* dev, int count, cudaStream_t s);
+    // Max over ranks of a host double (Gershgorin bounds of row blocks).
+    double max_f64(double v, cudaStream_t s);
     // Gathers int32 per-row values (n_loc each) into a global array (world*n_pad).
     void gather_i32(const int32_t* local, int32_t* global, cudaStream_t s);
     void gather_f64(const double* local, double* global, cudaStream_t s);
