@@ -201,3 +201,13 @@ def test_pipeline_irregular_normalized(ctx, ref):
     assert a.report.init == "piecewise"
     assert abs(a.report.cutsize - b.report.cutsize) <= 0.02 * b.report.cutsize
     np.testing.assert_allclose(a.report.theta, b.report.theta, rtol=1e-3, atol=1e-2)
+
+
+def test_cpp_shim_caller():
+    # a reference-style C++ caller compiled against include/specpart_b200.hpp
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parent.parent / "build" / "shim_test"
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
