@@ -310,6 +310,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     build_laplacian(operator_kind(R.problem), g, false, A, s);
     A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
     if (!kind.regular) collect_long_rows(g, A, 4096, s);
+    localize_operator(ctx->comm, g, A, s);  // multi-GPU: halo numbering + exchange plan
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {
         // B = D must be positive (laplacian.cpp:169-173)
@@ -568,22 +569,24 @@ sp_status sp_build_laplacian(sp_context* ctx, int32_t kind, const sp_graph* hg, 
 
 sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* hg, const double* X, int32_t m, double* Y) {
     return guarded(ctx, [&] {
-        if (ctx->comm.active()) throw_invalid("sp_spmm: single-GPU entry point");
         if (m < 1 || m > kMaxCols) throw_dimension("sp_spmm: 1 <= m <= 64");
         cudaStream_t s = ctx->stream;
         DevGraph g;
         upload_graph(ctx, hg, g);
         DevLaplacian L;
         build_laplacian(kind, g, false, L, s);
-        const int64_t n = g.n_local;
-        Solver solver(ctx, L.op, nullptr, 1);  // only for its block layout choice
+        // multi-GPU: every rank passes the full X and receives the full Y; each
+        // computes its row block after a halo exchange (the bit-exactness check
+        // of the row-partitioned operator)
+        localize_operator(ctx->comm, g, L, s);
+        const int64_t nloc = g.n_local;
+        Solver solver(ctx, L.op, nullptr, m);
         DBuf<double> xd(solver.block_elems(m)), yd(solver.block_elems(m));
-        upload_block(X, n, 0, n, m, solver.block(xd.p, m), s);
-        EpiArgs ea;
-        ea.mode = EPI_STORE;
-        ea.Y = solver.block(yd.p, m);
-        spmm_launch(L.op, solver.block(xd.p, m), m, ea, s);
-        download_block(solver.block(yd.p, m), n, m, Y, s);
+        upload_block(X, hg->n, g.row0, nloc, m, solver.block(xd.p, m), s);
+        solver.spmm_store(solver.block(xd.p, m), m, solver.block(yd.p, m));
+        DBuf<double> keep;
+        const View Yg = gather_block(ctx, solver.block(yd.p, m), m, keep);
+        download_block(Yg, hg->n, m, Y, s);
     });
 }
 
@@ -675,6 +678,7 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
         DevLaplacian A;
         build_laplacian(operator_kind(problem), g, false, A, s);
         A.op.bound = ctx->comm.max_f64(A.op.bound, s);
+        localize_operator(ctx->comm, g, A, s);
         const double* bdiag = nullptr;
         if (problem == SP_PROBLEM_GENERALIZED) {
             if (!g.positive_degrees) throw_degenerate("generalized problem requires positive degrees");

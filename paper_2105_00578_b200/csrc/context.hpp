@@ -20,6 +20,19 @@ namespace spb {
                                         __FILE__ + ":" + std::to_string(__LINE__));      \
     } while (0)
 
+// Halo exchange plan of one row-partitioned operator (built by localize_operator).
+// Local numbering: own rows [0, nloc), then the halo rows [nloc, nloc+nhalo) in
+// ascending global id (hence grouped by owner rank). Every SpMM input block has
+// room for the halo rows after its own rows.
+struct HaloPlan {
+    bool on = false;
+    int64_t nhalo = 0;
+    int64_t total_send = 0;
+    std::vector<int64_t> send_cnt, send_off, recv_cnt, recv_off;  // rows, per peer
+    DBuf<int32_t> send_idx;  // local row ids sent, grouped by destination rank
+    DBuf<double> sendbuf, recvbuf;
+};
+
 // 1-D row partition over the ranks of one box: rank k owns global
 // rows [k*n_pad, min(n, (k+1)*n_pad)), so a row-gathered block indexed by global
 // id is exactly the NCCL all-gather of the equal-size (padded) rank slices.
@@ -33,6 +46,7 @@ struct Comm {
     DBuf<double> full;     // world*n_pad x m gathered block
     DBuf<double> small;    // world x count for deterministic small sums
     int64_t bytes_moved = 0;
+    HaloPlan halo;
 
     bool active() const { return world > 1; }
     void setup(int64_t n) {
@@ -48,6 +62,9 @@ struct Comm {
     // Gathers the local n_loc x m block `local` into a row-major (world*n_pad) x m
     // block indexed by global row id. One GPU: returns `local` untouched.
     View gather_rows(const View& local, int m, cudaStream_t s);
+    // Fills the halo rows [nloc, nloc+nhalo) of the m-column block X from their
+    // owners: pack -> grouped ncclSend/ncclRecv -> unpack (halo.cu).
+    void halo_exchange(const View& X, int m, cudaStream_t s);
     // In-place deterministic sum over ranks of `count` doubles on the device:
     // all-gather then a fixed rank-order sum (bit-identical on every rank).
     void sum_small(double* dev, int count, cudaStream_t s);
@@ -81,6 +98,13 @@ struct Timers {
     int64_t poly_launches = 0;
     double poly_bytes = 0.0;
 };
+
+struct DevGraph;
+struct DevLaplacian;
+// Rewrites L.op into the local halo numbering (cols -> local ids, row0 -> 0, isd
+// -> own+halo entries, dpos = diagonal storage slots) and builds comm.halo.
+// No-op on one GPU.
+void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_t s);
 
 } // namespace spb
 

@@ -46,6 +46,9 @@ struct DevLaplacian {
     DBuf<int32_t> cols_L;
     DBuf<double> vals_L;
     DBuf<int32_t> long_rows;
+    DBuf<int32_t> cols_halo;  // multi-GPU: op columns in local halo numbering
+    DBuf<double> isd_halo;    // multi-GPU normalized: isd of own + halo rows
+    DBuf<int32_t> dpos;       // multi-GPU: per-row diagonal storage slot
 };
 
 // Weighted degrees, unit-cost detection and max degree of the local block.

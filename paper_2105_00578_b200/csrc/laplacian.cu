@@ -226,6 +226,7 @@ void build_laplacian(int kind, const DevGraph& g, bool materialize, DevLaplacian
     L.op = DevOp{};
     L.op.n = n;
     L.op.row0 = g.row0;
+    L.op.x_rows = g.n_global;
     L.op.long_threshold = int64_t(1) << 40;
     L.diag.alloc(std::max<int64_t>(n, 1));
     DBuf<unsigned long long> bb(1);

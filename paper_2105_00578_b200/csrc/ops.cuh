@@ -35,6 +35,10 @@ struct DevOp {
     int64_t n_long = 0;
     int64_t long_threshold = 1 << 30;
     int max_row = 1 << 30;      // max stored entries in a row (selects the tiled kernel when <= 32)
+    // multi-GPU halo numbering: cols are local ids (own rows, then halo rows) and
+    // dpos[i] is the storage slot of the diagonal (count of global cols < global i)
+    const int32_t* dpos = nullptr;
+    int64_t x_rows = 0;         // rows of the SpMM input block the columns address
     double bound = 0.0;
     bool is_diagonal = false;
 };

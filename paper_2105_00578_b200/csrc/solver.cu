@@ -57,8 +57,13 @@ __global__ void unit_vec_kernel(int64_t n, int64_t row0, View v) {
 
 Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_cols)
     : ctx_(ctx), s_(ctx->stream), A_(A), bdiag_(bdiag), n_(A.n), max_cols_(max_cols) {
-    colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0 && !ctx->comm.active();
-    ld_ = colmajor_ ? ((std::max<int64_t>(n_, 1) + 63) / 64) * 64 : max_cols;
+    // multi-GPU: blocks carry the halo rows after the own rows (halo.cu); without
+    // a halo plan (operator not localized) the input is all-gathered instead
+    halo_ = ctx->comm.active() && ctx->comm.halo.on;
+    if (ctx->comm.active() && !halo_) throw SpError(1, "Solver: multi-GPU operator without a halo plan");
+    rows_cap_ = std::max<int64_t>(n_ + (halo_ ? ctx->comm.halo.nhalo : 0), 1);
+    colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0;
+    ld_ = colmajor_ ? ((rows_cap_ + 63) / 64) * 64 : max_cols;
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
@@ -102,7 +107,8 @@ std::vector<double> Solver::gram_to_host(const TsSpec& spec, int& P, int& Q) {
 }
 
 void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
-    const View Xg = ctx_->comm.gather_rows(Xlocal, m, s_);
+    if (halo_) ctx_->comm.halo_exchange(Xlocal, m, s_);
+    const View& Xg = Xlocal;
     const bool timed = ctx_->time_spmm;
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
     if (timed) {
@@ -409,8 +415,10 @@ void Solver::build_poly(uint64_t seed, int degree) {
     const int64_t row0 = cm.active() ? cm.row0() : 0;
 
     // v0: seeded uniform(-1,1) (preconditioners.cpp:82-87), minus its mean, normalized
-    DBuf<double> Vb(static_cast<size_t>(std::max<int64_t>(n_, 1)) * (k_req + 1));
-    auto vcol = [&](int j) { return colmajor(Vb.p + static_cast<size_t>(j) * std::max<int64_t>(n_, 1), std::max<int64_t>(n_, 1), 1); };
+    // basis columns carry halo rows (they are SpMM inputs)
+    const int64_t vld = rows_cap_;
+    DBuf<double> Vb(static_cast<size_t>(vld) * (k_req + 1));
+    auto vcol = [&](int j) { return colmajor(Vb.p + static_cast<size_t>(j) * vld, vld, 1); };
     mt_uniform_block(seed, n_glob, 1, row0, n_, vcol(0), s_);
     const int rows = colsum_partials(n_, vcol(0), scratch_.p, s_);
     reduce_partials(scratch_.p, rows, 1, norms_.p, s_);
@@ -442,7 +450,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
     const double tiny = 1e-13 * (A_.bound > 0.0 ? A_.bound : 1.0);
     DBuf<double> wbuf(static_cast<size_t>(std::max<int64_t>(n_, 1)));
     const View w = colmajor(wbuf.p, std::max<int64_t>(n_, 1), 1);
-    const View Vall = colmajor(Vb.p, std::max<int64_t>(n_, 1), k_req + 1);
+    const View Vall = colmajor(Vb.p, vld, k_req + 1);
     for (int j = 0; j < k_req; ++j) {
         spmm_store(vcol(j), 1, w);
         const View basis = Vall.sub(0, j + 1);

@@ -67,7 +67,7 @@ public:
     bool colmajor_blocks() const { return colmajor_; }
     int64_t ld() const { return ld_; }
     View block(double* p, int cols) const { return colmajor_ ? colmajor(p, ld_, cols) : rowmajor(p, cols, cols); }
-    size_t block_elems(int cols) const { return static_cast<size_t>(colmajor_ ? ld_ : std::max<int64_t>(n_, 1)) * cols; }
+    size_t block_elems(int cols) const { return static_cast<size_t>(colmajor_ ? ld_ : rows_cap_) * cols; }
 
 private:
     struct Orth {
@@ -91,6 +91,8 @@ private:
     int64_t n_;       // local rows
     int max_cols_;
     bool colmajor_ = false;
+    bool halo_ = false;     // multi-GPU: inputs get their halo rows before each SpMM
+    int64_t rows_cap_ = 1;  // own rows + halo rows
     int64_t ld_ = 1;
     PrecKind prec_ = PREC_NONE;
     const double* inv_diag_ = nullptr;

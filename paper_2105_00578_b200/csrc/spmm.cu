@@ -38,6 +38,7 @@ struct RowAcc {
         double dval = 0.0, isdi = 0.0;
         if (MODE == OP_LAPLACE_UNIT) dval = op.diag[row];
         if (MODE == OP_NORMAL_UNIT) isdi = op.isd[grow];
+        const int64_t kdiag = op.dpos ? k0 + op.dpos[row] : -1;
         for (int64_t kb = k0; kb < k1; kb += G) {
             const int cnt = static_cast<int>(min(static_cast<int64_t>(G), k1 - kb));
             int jl = 0;
@@ -53,14 +54,15 @@ struct RowAcc {
                 double v = 0.0;
                 if (MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) v = __shfl_sync(gmask, vl, t, G);
                 const double xj = act ? X.at(j, c) : 0.0;
+                const bool at_diag = op.dpos ? (kb + t == kdiag) : (j > grow);
                 if (MODE == OP_LAPLACE_UNIT) {
-                    if (!placed && j > grow) {
+                    if (!placed && at_diag) {
                         acc = __dadd_rn(acc, __dmul_rn(dval, xi));
                         placed = true;
                     }
                     acc = __dsub_rn(acc, xj);  // (-1.0) * x_j added: exact negation
                 } else if (MODE == OP_NORMAL_UNIT) {
-                    if (!placed && j > grow) {
+                    if (!placed && at_diag) {
                         acc = __dadd_rn(acc, xi);  // 1.0 * x_i
                         placed = true;
                     }
@@ -301,7 +303,9 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
             const int64_t grow = op.row0 + r0 + lane;
             int kd = 0;
             if (MODE == OP_LAPLACE_UNIT || MODE == OP_NORMAL_UNIT) {
-                while (kd < len && sc[st + kd] < grow) ++kd;
+                if (op.dpos) kd = op.dpos[r0 + lane];
+                else
+                    while (kd < len && sc[st + kd] < grow) ++kd;
                 if (MODE == OP_NORMAL_UNIT) {
                     const double nisdi = -op.isd[grow];
                     for (int k = 0; k < len; ++k) sv[st + k] = __dmul_rn(nisdi, sv[st + k]);
@@ -417,8 +421,12 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
             int kd = MAXR + 1;  // explicit CSR: the diagonal is a stored entry
             if (MODE != OP_EXPLICIT) {
                 kd = 0;
+                if (op.dpos) {
+                    kd = live ? op.dpos[row] : 0;
+                } else {
 #pragma unroll
-                for (int k = 0; k < MAXR; ++k) kd += (k < len && jv[k] < grow) ? 1 : 0;
+                    for (int k = 0; k < MAXR; ++k) kd += (k < len && jv[k] < grow) ? 1 : 0;
+                }
             }
 #pragma unroll
             for (int sidx = 0; sidx < NS; ++sidx) {
@@ -580,7 +588,7 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
     const bool colmajor = m > 1 ? (X.rs == 1 && ea.Y.rs == 1 && (ea.mode != EPI_POLY || ea.H.rs == 1))
                                 : (X.rs == 1 && ea.Y.rs == 1);
     if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && colmajor &&
-        (op.row0 + op.n) * 8 < (int64_t(1) << 32) && m <= kMaxCols) {
+        std::max(op.x_rows, op.row0 + op.n) * 8 < (int64_t(1) << 32) && m <= kMaxCols) {
         TileArgs ta;
         ta.X = X.ptr;
         ta.ldx = static_cast<int>(m > 1 ? X.cs : 0);

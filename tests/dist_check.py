@@ -28,6 +28,20 @@ def main():
          RunConfig(num_parts=16, precond="polynomial", problem="generalized", seed=42)),
         ("rmat12_norm_jacobi", rg, RunConfig(num_parts=8, precond="jacobi", problem="normalized", seed=42)),
     ]
+    # bit-exact row-partitioned SpMM (halo exchange) against the reference's spmv
+    rng = np.random.default_rng(9)
+    wg = gen.random_connected_graph(300, 900, seed=4)
+    wvals = np.repeat(rng.uniform(0.5, 2.0, 1), wg.col_indices.size)  # uniform non-unit cost: explicit operator
+    from paper_2105_00578_b200.api import Graph
+    wg = Graph(wg.row_offsets, wg.col_indices, wvals, None)
+    spmm_cases = [("grid64", gen.grid2d(64, 64)), ("st27_12", gen.stencil3d(12, 12, 12, 27)),
+                  ("rmat12", rg), ("wrand300", wg)]
+    spmm_out = {}
+    for name, g in spmm_cases:
+        X = np.random.default_rng(3).uniform(-1, 1, (g.n, 5))
+        for kind in ("combinatorial", "normalized"):
+            Y = ctx.spmm(kind, g, X)
+            spmm_out[f"{name}/{kind}"] = Y
     out = {}
     for name, g, cfg in cases:
         r = ctx.partition_graph(g, cfg)
@@ -46,6 +60,11 @@ def main():
                      theta_maxdiff=float(np.max(np.abs(np.array(o["theta"]) - np.array(b.report.theta)))))
             o["ok"] = bool(o["same_on_all_ranks"] and abs(o["cut"] - o["ref_cut"]) <= 0.02 * o["ref_cut"]
                            and o["imbalance"] <= o["ref_imbalance"] + 1e-12 and o["n_gpus"] == world)
+        for name, g in spmm_cases:
+            X = np.random.default_rng(3).uniform(-1, 1, (g.n, 5))
+            for kind in ("combinatorial", "normalized"):
+                Yr = np.asarray(ref.spmm(kind, g, X))
+                out[f"spmm/{name}/{kind}"] = dict(ok=bool(Yr.tobytes() == spmm_out[f"{name}/{kind}"].tobytes()))
         print("DIST_RESULT " + json.dumps(out), flush=True)
     ctx.close()
     dist.destroy_process_group()
