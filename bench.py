@@ -316,6 +316,7 @@ def main():
                      "kernel_share_of_step": round((kms / 1e3) / max(sum(t_res), 1e-12), 4),
                      "all_spmm": {"achieved": round(spmm_bytes / (spmm_ms / 1e3) / 1e9, 1) if spmm_ms > 0 else 0.0,
                                   "launches_per_step": spmm_launches // max(len(r_res), 1)}},
+        "step_s": [round(x, 5) for x in t_res], "e2e_step_s": [round(x, 5) for x in t_e2e],
         "clocks": clocks, "gpu_launches": int(launches),
         "result": {"cut": rep.cutsize, "imbalance": rep.imbalance, "iterations": rep.iterations,
                    "converged": all(rep.converged), "times": rep.times,

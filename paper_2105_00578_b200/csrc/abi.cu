@@ -212,6 +212,7 @@ template <class F> sp_status guarded(sp_context* ctx, F&& f) {
     if (!ctx) return SP_INVALID;
     try {
         SPB_CUDA(cudaSetDevice(ctx->device));
+        AllocStreamScope scope(ctx->stream);
         f();
         return SP_OK;
     } catch (...) {
@@ -428,6 +429,10 @@ sp_status sp_context_create(int device, sp_context** out) {
     try {
         SPB_CUDA(cudaSetDevice(device));
         SPB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        SPB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        SPB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         SPB_CUDA(cudaEventCreate(&c->ev0));
         SPB_CUDA(cudaEventCreate(&c->ev1));
     } catch (...) {
@@ -475,6 +480,7 @@ sp_status sp_context_create_dist(int device, int rank, int world, const void* nc
 void sp_context_destroy(sp_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm.nccl) nccl().CommDestroy(c->comm.nccl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
@@ -521,6 +527,7 @@ sp_status sp_graph_upload(sp_context* ctx, const sp_graph* hg, sp_device_graph**
 void sp_graph_free(sp_device_graph* h) {
     if (!h) return;
     cudaSetDevice(h->ctx->device);
+    cudaStreamSynchronize(h->ctx->stream);
     delete h;
 }
 

@@ -47,6 +47,21 @@ long long& launch_counter();
     } while (0)
 
 // ---- device buffers ----
+// Stream-ordered allocation from the device's default memory pool (release
+// threshold raised at context creation, so freed blocks stay cached): the many
+// per-call scratch buffers cost no cudaMalloc/cudaFree and no implicit device
+// synchronization. Allocations and frees are ordered on the stream of the
+// entry point running on this thread (set by guarded() in abi.cu).
+inline cudaStream_t& alloc_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+struct AllocStreamScope {
+    cudaStream_t prev;
+    explicit AllocStreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+    ~AllocStreamScope() { alloc_stream() = prev; }
+};
+
 template <class T> struct DBuf {
     T* p = nullptr;
     size_t n = 0;
@@ -63,11 +78,11 @@ template <class T> struct DBuf {
     void alloc(size_t count) {
         if (count <= n && p) return;
         release();
-        if (count) SPB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (count) SPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
         n = count;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, alloc_stream());
         p = nullptr;
         n = 0;
     }
