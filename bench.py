@@ -316,6 +316,13 @@ def main():
                      "kernel_share_of_step": round((kms / 1e3) / max(sum(t_res), 1e-12), 4),
                      "all_spmm": {"achieved": round(spmm_bytes / (spmm_ms / 1e3) / 1e9, 1) if spmm_ms > 0 else 0.0,
                                   "launches_per_step": spmm_launches // max(len(r_res), 1)}},
+        "halo": ({"exchanges_per_step": sum(r.report.device["halo_launches"] for r in r_res) // max(len(r_res), 1),
+                  "us_per_exchange": round(1e3 * sum(r.report.device["halo_ms"] for r in r_res)
+                                           / max(1, sum(r.report.device["halo_launches"] for r in r_res)), 2),
+                  "bytes_per_exchange": round(sum(r.report.device["halo_bytes"] for r in r_res)
+                                              / max(1, sum(r.report.device["halo_launches"] for r in r_res))),
+                  "path": "nccl" if os.environ.get("SPB_P2P", "1") == "0" else "p2p (NVLink peer writes)"}
+                 if world > 1 else None),
         "step_s": [round(x, 5) for x in t_res], "e2e_step_s": [round(x, 5) for x in t_e2e],
         "clocks": clocks, "gpu_launches": int(launches),
         "result": {"cut": rep.cutsize, "imbalance": rep.imbalance, "iterations": rep.iterations,

@@ -143,6 +143,10 @@ typedef struct sp_report {
     int64_t poly_launches;
     double poly_bytes;
     double poly_ms;
+    /* multi-GPU halo exchanges before SpMMs (count, bytes sent, device ms incl. peer waits) */
+    int64_t halo_launches;
+    double halo_bytes;
+    double halo_ms;
     /* caller-provided outputs (may be NULL) */
     double* part_weights;          /* num_parts */
     sp_trace_record* trace;        /* trace_capacity records */

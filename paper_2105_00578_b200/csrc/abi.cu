@@ -214,6 +214,7 @@ template <class F> sp_status guarded(sp_context* ctx, F&& f) {
         SPB_CUDA(cudaSetDevice(ctx->device));
         AllocStreamScope scope(ctx->stream);
         f();
+        ctx->comm.sym_check(ctx->stream);  // a timed-out peer wait fails the call
         return SP_OK;
     } catch (...) {
         return map_exception(ctx);
@@ -337,8 +338,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     }
     ctx->prof.mark(s, "precond_build");
     const int64_t nloc = g.n_local;
-    DBuf<double> Xb(solver.block_elems(d));
-    const View X = solver.block(Xb.p, d);
+    DBuf<double> Xb;
+    const View X = solver.block(solver.input_block(d, Xb), d);
     if (x0) upload_block(x0, n, g.row0, nloc, d, X, s);
     else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X, s);
     else initial_block_piecewise(n, d, g.row0, nloc, X, s);
@@ -387,6 +388,9 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     R.poly_launches = ctx->timers.poly_launches;
     R.poly_bytes = ctx->timers.poly_bytes;
     R.poly_ms = ctx->timers.poly_ms;
+    R.halo_launches = ctx->timers.halo_launches;
+    R.halo_bytes = ctx->timers.halo_bytes;
+    R.halo_ms = ctx->timers.halo_ms;
     R.kernel_launches = static_cast<int32_t>(launch_counter() - launches0 + ctx->timers.kernel_launches);
     R.n_gpus = ctx->comm.world;
     if (rep) {
@@ -481,6 +485,7 @@ void sp_context_destroy(sp_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    sym_release(c->comm);
     if (c->comm.nccl) nccl().CommDestroy(c->comm.nccl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
@@ -588,9 +593,10 @@ sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* hg, const doubl
         localize_operator(ctx->comm, g, L, s);
         const int64_t nloc = g.n_local;
         Solver solver(ctx, L.op, nullptr, m);
-        DBuf<double> xd(solver.block_elems(m)), yd(solver.block_elems(m));
-        upload_block(X, hg->n, g.row0, nloc, m, solver.block(xd.p, m), s);
-        solver.spmm_store(solver.block(xd.p, m), m, solver.block(yd.p, m));
+        DBuf<double> xd, yd(solver.block_elems(m));
+        const View Xv = solver.block(solver.input_block(m, xd), m);
+        upload_block(X, hg->n, g.row0, nloc, m, Xv, s);
+        solver.spmm_store(Xv, m, solver.block(yd.p, m));
         DBuf<double> keep;
         const View Yg = gather_block(ctx, solver.block(yd.p, m), m, keep);
         download_block(Yg, hg->n, m, Y, s);
@@ -700,8 +706,8 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
             solver.build_poly(poly_seed, poly_degree > 0 ? poly_degree : 25);
         }
         const int64_t nloc = g.n_local;
-        DBuf<double> Xb(solver.block_elems(nev));
-        const View X = solver.block(Xb.p, nev);
+        DBuf<double> Xb;
+        const View X = solver.block(solver.input_block(nev, Xb), nev);
         upload_block(X0, hg->n, g.row0, nloc, nev, X, s);
         SolveOpts so;
         so.nev = nev;

@@ -117,6 +117,7 @@ View Comm::gather_rows(const View& local, int m, cudaStream_t s) {
 
 void Comm::sum_small(double* dev, int count, cudaStream_t s) {
     if (!active() || count <= 0) return;
+    if (sum_p2p(*this, dev, count, s)) return;  // NVLink slots (symm.cu), same rank order
     small.alloc(static_cast<size_t>(count) * world);
     SPB_NCCL(::spb::nccl().AllGather(dev, small.p, count, ncclDouble, nccl, s));
     ordered_sum_kernel<<<ceil_div(count, 128), 128, 0, s>>>(small.p, world, count, dev);

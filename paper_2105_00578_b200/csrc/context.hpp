@@ -5,6 +5,7 @@
 #include "graph_dev.cuh"
 
 #include "nccl_dyn.hpp"
+#include "p2p.cuh"
 
 #include <string>
 #include <utility>
@@ -31,7 +32,39 @@ struct HaloPlan {
     std::vector<int64_t> send_cnt, send_off, recv_cnt, recv_off;  // rows, per peer
     DBuf<int32_t> send_idx;  // local row ids sent, grouped by destination rank
     DBuf<double> sendbuf, recvbuf;
+    // P2P push: per send entry, destination rank and row in that rank's block
+    DBuf<int32_t> dst_peer, dst_row;
+    uint32_t send_mask = 0, recv_mask = 0;
+    int64_t max_rows = 0;  // max over ranks of nloc_pad + nhalo (common block height)
+    int64_t halo_base = 0; // first halo row: nloc rounded up to 32 rows (own and halo rows never share a cache line)
+    int64_t rot_tiles = 0, n_int_tiles = 0;  // fused SpMM tile order (p2p.cuh HaloFuse)
 };
+
+// Symmetric peer memory (symm.cu): cudaMalloc'd segments mapped into every
+// rank of the box through CUDA IPC, carved by a bump allocator that runs the
+// same sequence on every rank, so an offset names the same block everywhere.
+// SpMM input blocks live here; the halo rows of a peer's copy are written
+// directly over NVLink, and small sums are gathered into per-rank slots.
+constexpr int kSumMax = 16384;  // doubles per rank slot of a P2P sum
+struct SymSeg {
+    char* base = nullptr;
+    size_t size = 0;
+    std::vector<char*> peer;  // mapped base of every rank's segment (own = base)
+};
+struct SymHeap {
+    bool tried = false;
+    bool on = false;
+    std::vector<SymSeg> segs;
+    size_t seg_i = 0, off = 0;  // bump position
+    SymSeg ctrl;                // flags + sum slots
+    uint64_t halo_epoch = 0, sum_epoch = 0, bar_epoch = 0;
+    DBuf<int> counter;          // last-CTA ticket of the push kernel
+    DBuf<int> err;              // device error word (peer wait timed out)
+    const void* last_halo_src = nullptr;
+};
+// control segment layout (bytes)
+constexpr size_t kFlHalo = 0, kFlSum = 256, kFlBar = 512, kSumSlots = 4096;
+constexpr size_t kCtrlBytes = kSumSlots + 2 * kMaxPeers * kSumMax * sizeof(double);
 
 // 1-D row partition over the ranks of one box: rank k owns global
 // rows [k*n_pad, min(n, (k+1)*n_pad)), so a row-gathered block indexed by global
@@ -47,6 +80,7 @@ struct Comm {
     DBuf<double> small;    // world x count for deterministic small sums
     int64_t bytes_moved = 0;
     HaloPlan halo;
+    SymHeap sym;
 
     bool active() const { return world > 1; }
     void setup(int64_t n) {
@@ -65,6 +99,14 @@ struct Comm {
     // Fills the halo rows [nloc, nloc+nhalo) of the m-column block X from their
     // owners: pack -> grouped ncclSend/ncclRecv -> unpack (halo.cu).
     void halo_exchange(const View& X, int m, cudaStream_t s);
+    // Symmetric heap (collective calls: every rank, same order, same sizes).
+    bool sym_init(cudaStream_t s);   // maps the control segment; false = NCCL paths
+    void sym_reset() { sym.seg_i = 0; sym.off = 0; sym.last_halo_src = nullptr; }
+    double* sym_alloc(size_t elems, cudaStream_t s);
+    // byte distance from a local symmetric address to the same object on `peer`
+    int64_t sym_delta(const void* p, int peer) const;
+    void sym_check(cudaStream_t s);  // throws if a peer wait timed out
+    void barrier_p2p(cudaStream_t s);
     // In-place deterministic sum over ranks of `count` doubles on the device:
     // all-gather then a fixed rank-order sum (bit-identical on every rank).
     void sum_small(double* dev, int count, cudaStream_t s);
@@ -95,9 +137,19 @@ struct Timers {
     double spmm_bytes = 0.0;
     int64_t kernel_launches = 0;
     double poly_ms = 0.0;
+    int64_t halo_launches = 0;
+    double halo_bytes = 0.0;
+    double halo_ms = 0.0;
     int64_t poly_launches = 0;
     double poly_bytes = 0.0;
 };
+
+// symm.cu: P2P fast paths; return false when not applicable (caller uses NCCL)
+bool halo_push(Comm& cm, const View& X, int m, cudaStream_t s);
+// Fills hf for an SpMM with the exchange fused in; false = not applicable.
+bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s);
+bool sum_p2p(Comm& cm, double* dev, int count, cudaStream_t s);
+void sym_release(Comm& cm);
 
 struct DevGraph;
 struct DevLaplacian;
@@ -119,18 +171,18 @@ struct sp_context {
     // event pairs recorded around SpMM launches; resolved without extra syncs
     // once the pipeline has synchronized (collect_spmm_times)
     std::vector<cudaEvent_t> evpool;
-    std::vector<char> ev_poly;  // per event pair: was it a polynomial-step launch
+    std::vector<char> ev_poly;  // per event pair: 0 SpMM, 1 polynomial-step SpMM, 2 halo exchange
     size_t ev_used = 0;
     spb::PhaseProf prof;
 
-    std::pair<cudaEvent_t, cudaEvent_t> next_event_pair(bool poly = false) {
+    std::pair<cudaEvent_t, cudaEvent_t> next_event_pair(int kind = 0) {
         while (evpool.size() < ev_used + 2) {
             cudaEvent_t e;
             SPB_CUDA(cudaEventCreate(&e));
             evpool.push_back(e);
         }
         if (ev_poly.size() < ev_used / 2 + 1) ev_poly.resize(ev_used / 2 + 1);
-        ev_poly[ev_used / 2] = poly;
+        ev_poly[ev_used / 2] = static_cast<char>(kind);
         auto p = std::make_pair(evpool[ev_used], evpool[ev_used + 1]);
         ev_used += 2;
         return p;
@@ -140,8 +192,12 @@ struct sp_context {
         for (size_t i = 0; i + 1 < ev_used; i += 2) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, evpool[i], evpool[i + 1]) == cudaSuccess) {
+                if (ev_poly[i / 2] == 2) {
+                    timers.halo_ms += ms;
+                    continue;
+                }
                 timers.spmm_ms += ms;
-                if (ev_poly[i / 2]) timers.poly_ms += ms;
+                if (ev_poly[i / 2] == 1) timers.poly_ms += ms;
             }
         }
         ev_used = 0;

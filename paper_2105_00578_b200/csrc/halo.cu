@@ -64,11 +64,27 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t n, 
 }
 
 __global__ void remap_cols_kernel(int64_t nnz, const int32_t* cols, int64_t lo, int64_t hi, const int32_t* halo,
-                                  int64_t nhalo, int64_t nloc, int32_t* out) {
+                                  int64_t nhalo, int64_t base, int32_t* out) {
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t j = cols[k];
-        out[k] = static_cast<int32_t>((j >= lo && j < hi) ? j - lo : nloc + lower_bound_i32(halo, nhalo, j));
+        out[k] = static_cast<int32_t>((j >= lo && j < hi) ? j - lo : base + lower_bound_i32(halo, nhalo, j));
+    }
+}
+
+// interior rows: [P, Q) with P = 1 + last row referencing a lower rank, Q = first
+// row referencing a higher rank (a slab partition of a banded mesh)
+__global__ void interior_kernel(int64_t n, const int64_t* offs, const int32_t* cols, int64_t lo, int64_t hi,
+                                unsigned long long* pq) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        bool below = false, above = false;
+        for (int64_t k = offs[i]; k < offs[i + 1]; ++k) {
+            below |= cols[k] < lo;
+            above |= cols[k] >= hi;
+        }
+        if (below) atomicMax(&pq[0], static_cast<unsigned long long>(i + 1));
+        if (above) atomicMin(&pq[1], static_cast<unsigned long long>(i));
     }
 }
 
@@ -81,11 +97,11 @@ __global__ void dpos_kernel(int64_t n, int64_t row0, const int64_t* offs, const 
     }
 }
 
-__global__ void isd_halo_kernel(int64_t nloc, int64_t row0, const int32_t* halo, int64_t nhalo, const double* isd,
-                                double* out) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nloc + nhalo;
+__global__ void isd_halo_kernel(int64_t nloc, int64_t base, int64_t row0, const int32_t* halo, int64_t nhalo,
+                                const double* isd, double* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < base + nhalo;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = i < nloc ? isd[row0 + i] : isd[halo[i - nloc]];
+        out[i] = i < nloc ? isd[row0 + i] : (i < base ? 0.0 : isd[halo[i - base]]);
 }
 
 __global__ void owner_bounds_kernel(const int32_t* halo, int64_t nhalo, int64_t n_pad, int world, int64_t* b) {
@@ -154,10 +170,30 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
     emit_halo_kernel<<<grid_for(words, 256, 8), 256, 0, s>>>(words, bm.p, woff.p, halo.p);
     SPB_LAUNCH_CHECK();
 
-    // 2./3. local column ids, diagonal slots, isd over own + halo rows
+    // 2./3. local column ids, diagonal slots, isd over own + halo rows; halo
+    // rows start at a 32-row boundary so no cache line holds own and halo rows
+    const int64_t base = (nloc + 31) / 32 * 32;
+    hp.halo_base = base;
+    {
+        DBuf<unsigned long long> pq(2);
+        const unsigned long long init[2] = {0ull, static_cast<unsigned long long>(nloc)};
+        SPB_CUDA(cudaMemcpyAsync(pq.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        if (nnz > 0 && nloc > 0) {
+            interior_kernel<<<grid_for(nloc, 256, 8), 256, 0, s>>>(nloc, op.offs, op.cols, lo, hi, pq.p);
+            SPB_LAUNCH_CHECK();
+        }
+        unsigned long long h[2];
+        SPB_CUDA(cudaMemcpyAsync(h, pq.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        const int64_t ntiles = (nloc + 31) / 32;
+        const int64_t P = static_cast<int64_t>(h[0]), Q = static_cast<int64_t>(h[1]);
+        hp.rot_tiles = ntiles > 0 ? std::min<int64_t>((P + 31) / 32, ntiles) % ntiles : 0;
+        const int64_t q_t = Q >= nloc ? ntiles : Q / 32;
+        hp.n_int_tiles = (P <= Q && ntiles > 0) ? std::max<int64_t>(0, q_t - (P + 31) / 32) : 0;
+    }
     if (nnz > 0) {
         L.cols_halo.alloc(nnz);
-        remap_cols_kernel<<<grid_for(nnz, 256, 8), 256, 0, s>>>(nnz, op.cols, lo, hi, halo.p, nh, nloc,
+        remap_cols_kernel<<<grid_for(nnz, 256, 8), 256, 0, s>>>(nnz, op.cols, lo, hi, halo.p, nh, base,
                                                                L.cols_halo.p);
         SPB_LAUNCH_CHECK();
         if (op.mode == OP_LAPLACE_UNIT || op.mode == OP_NORMAL_UNIT) {
@@ -170,14 +206,14 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
         op.cols = L.cols_halo.p;
     }
     if (op.isd) {
-        L.isd_halo.alloc(std::max<int64_t>(nloc + nh, 1));
-        isd_halo_kernel<<<grid_for(std::max<int64_t>(nloc + nh, 1), 256, 8), 256, 0, s>>>(nloc, lo, halo.p, nh,
-                                                                                        op.isd, L.isd_halo.p);
+        L.isd_halo.alloc(std::max<int64_t>(base + nh, 1));
+        isd_halo_kernel<<<grid_for(std::max<int64_t>(base + nh, 1), 256, 8), 256, 0, s>>>(nloc, base, lo, halo.p,
+                                                                                        nh, op.isd, L.isd_halo.p);
         SPB_LAUNCH_CHECK();
         op.isd = L.isd_halo.p;
     }
     op.row0 = 0;
-    op.x_rows = nloc + nh;
+    op.x_rows = base + nh;
 
     // 4. per-owner counts, all-gathered; halo id lists to their owners
     DBuf<int64_t> bounds(world + 1), cnt(world), allcnt(static_cast<size_t>(world) * world);
@@ -220,14 +256,42 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
         to_local_kernel<<<grid_for(off, 256, 8), 256, 0, s>>>(off, hp.send_idx.p, lo);
         SPB_LAUNCH_CHECK();
     }
+    // P2P push targets: destination rank and row of every send entry; the
+    // common block height (max over ranks of own + halo rows)
+    {
+        std::vector<int32_t> dpeer(std::max<int64_t>(off, 1)), drow(std::max<int64_t>(off, 1));
+        int64_t maxrows = 0;
+        for (int p = 0; p < world; ++p) {
+            const int64_t r0p = static_cast<int64_t>(p) * cm.n_pad;
+            const int64_t nlp = (((r0p >= n ? 0 : std::min<int64_t>(cm.n_pad, n - r0p))) + 31) / 32 * 32;
+            int64_t nhp = 0, before_me = 0;
+            for (int q = 0; q < world; ++q) {
+                nhp += M[static_cast<size_t>(p) * world + q];
+                if (q < cm.rank) before_me += M[static_cast<size_t>(p) * world + q];
+            }
+            maxrows = std::max(maxrows, nlp + nhp);
+            for (int64_t t = 0; t < hp.send_cnt[p]; ++t) {
+                dpeer[hp.send_off[p] + t] = p;
+                drow[hp.send_off[p] + t] = static_cast<int32_t>(nlp + before_me + t);
+            }
+            if (hp.send_cnt[p] > 0) hp.send_mask |= 1u << p;
+            if (hp.recv_cnt[p] > 0) hp.recv_mask |= 1u << p;
+        }
+        hp.max_rows = maxrows;
+        hp.dst_peer.alloc(dpeer.size());
+        hp.dst_row.alloc(drow.size());
+        SPB_CUDA(cudaMemcpyAsync(hp.dst_peer.p, dpeer.data(), sizeof(int32_t) * dpeer.size(), cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemcpyAsync(hp.dst_row.p, drow.data(), sizeof(int32_t) * drow.size(), cudaMemcpyHostToDevice, s));
+    }
     SPB_CUDA(cudaStreamSynchronize(s));  // halo/bm/tmp are freed on return
+    cm.sym_init(s);
     hp.on = true;
 }
 
 void Comm::halo_exchange(const View& X, int m, cudaStream_t s) {
     if (!active() || !halo.on) return;
+    if (halo_push(*this, X, m, s)) return;  // NVLink peer writes (symm.cu)
     HaloPlan& hp = halo;
-    const int64_t nl = nloc();
     hp.sendbuf.alloc(std::max<int64_t>(hp.total_send * m, 1));
     hp.recvbuf.alloc(std::max<int64_t>(hp.nhalo * m, 1));
     if (hp.total_send > 0) {
@@ -248,7 +312,7 @@ void Comm::halo_exchange(const View& X, int m, cudaStream_t s) {
     SPB_NCCL(::spb::nccl().GroupEnd());
     bytes_moved += hp.nhalo * m * 8;
     if (hp.nhalo > 0) {
-        halo_unpack_kernel<<<grid_for(hp.nhalo * m, 256, 8), 256, 0, s>>>(hp.nhalo, nl, hp.recvbuf.p, m, X);
+        halo_unpack_kernel<<<grid_for(hp.nhalo * m, 256, 8), 256, 0, s>>>(hp.nhalo, hp.halo_base, hp.recvbuf.p, m, X);
         SPB_LAUNCH_CHECK();
     }
 }

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "p2p.cuh"
 
 namespace spb {
 
@@ -66,7 +67,11 @@ struct EpiArgs {
 // Y-block SpMM with epilogue. X is the gathered block (rows = global columns of
 // A; on one GPU the same n), m columns. Returns the number of partial rows
 // written to ea.partial (for RESIDUAL), so the caller can reduce them.
-int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
+// hf: multi-GPU halo exchange fused into the kernel (column-major short-row path only)
+int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s,
+                const HaloFuse* hf = nullptr);
+// true when spmm_launch uses the column-major row-per-lane kernel for these arguments
+bool spmm_col_path(const DevOp& op, const View& X, int m, const EpiArgs& ea);
 // Reduce partial[rows x m] over rows in fixed order into out[m] (device).
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s);
 

@@ -1,0 +1,107 @@
+// p2p.cuh — peer-memory (NVLink) signalling primitives shared by the halo push
+// kernel (symm.cu) and the SpMM kernel with the fused halo exchange (spmm.cu).
+#pragma once
+
+#include <cstdint>
+
+namespace spb {
+
+constexpr int kMaxPeers = 8;
+
+struct PeerAddr {
+    char* p[kMaxPeers];
+};
+struct PeerDelta {
+    long long d[kMaxPeers];
+};
+
+// Arguments of an SpMM with its halo exchange fused in (spmm_col_kernel): the
+// CTAs first write the boundary rows every peer needs into the peers' copies of
+// X (byte delta xd[p] from the local address), raise one flag per destination
+// (last CTA), compute the interior row tiles, wait for the peers' flags and
+// finish with the tiles that read halo rows. Tiles are visited in rotated
+// order: logical tile t is physical tile (t + rot) mod ntiles, and logical
+// tiles < n_int read no halo row.
+struct HaloFuse {
+    int on = 0;
+    int world = 1;
+    int64_t rot = 0;
+    int64_t n_int = 0;
+    int64_t total = 0;  // send entries
+    const int32_t* src_row = nullptr;
+    const int32_t* dst_peer = nullptr;
+    const int32_t* dst_row = nullptr;
+    PeerDelta xd{};
+    int* counter = nullptr;
+    unsigned long long epoch = 0;
+    PeerAddr remote_flag{};
+    uint32_t send_mask = 0, recv_mask = 0;
+    const uint64_t* my_flags = nullptr;
+    int* err = nullptr;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// spins until *f >= epoch; after 30 s sets *err and gives up (no GPU hang)
+__device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t epoch, int* err) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(f) < epoch) {
+        if (global_ns() - t0 > 30ull * 1000000000ull) {
+            atomicExch(err, 1);
+            return;
+        }
+    }
+}
+// The push half of a halo exchange, run by every thread of the grid; the last
+// CTA to finish raises the destination flags. Column-major element order so a
+// warp's reads and remote writes are contiguous for slab halos.
+template <class XAt>
+__device__ __forceinline__ void halo_push_part(const HaloFuse& hf, int m, XAt xat) {
+    const int64_t elems = hf.total * m;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < elems;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(e / hf.total);
+        const int64_t t = e - static_cast<int64_t>(c) * hf.total;
+        const double v = *xat(hf.src_row[t], c);
+        char* dst = reinterpret_cast<char*>(xat(hf.dst_row[t], c)) + hf.xd.d[hf.dst_peer[t]];
+        *reinterpret_cast<double*>(dst) = v;
+    }
+    // one system-scope fence per CTA: the barrier makes the CTA's stores
+    // observed by thread 0, whose fence is cumulative over them
+    __syncthreads();
+    __shared__ int last_cta;
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        last_cta = (atomicAdd(hf.counter, 1) == static_cast<int>(gridDim.x) - 1);
+    }
+    __syncthreads();
+    if (last_cta) {
+        const int p = threadIdx.x;
+        if (p < hf.world && ((hf.send_mask >> p) & 1u)) {
+            __threadfence_system();
+            st_release_sys(reinterpret_cast<uint64_t*>(hf.remote_flag.p[p]), hf.epoch);
+        }
+        if (p == 0) *hf.counter = 0;
+    }
+}
+// wait for every source peer's data (one lane per peer), then the warp proceeds
+__device__ __forceinline__ void halo_wait_warp(const HaloFuse& hf) {
+    const int lane = threadIdx.x & 31;
+    if (lane < hf.world && ((hf.recv_mask >> lane) & 1u)) wait_flag(hf.my_flags + lane, hf.epoch, hf.err);
+    __syncwarp();
+}
+#endif
+
+} // namespace spb

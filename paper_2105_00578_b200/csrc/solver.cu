@@ -61,7 +61,14 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     // a halo plan (operator not localized) the input is all-gathered instead
     halo_ = ctx->comm.active() && ctx->comm.halo.on;
     if (ctx->comm.active() && !halo_) throw SpError(1, "Solver: multi-GPU operator without a halo plan");
-    rows_cap_ = std::max<int64_t>(n_ + (halo_ ? ctx->comm.halo.nhalo : 0), 1);
+    rows_cap_ = std::max<int64_t>(halo_ ? ctx->comm.halo.halo_base + ctx->comm.halo.nhalo : n_, 1);
+    // SpMM inputs in the symmetric heap (peers write their halo rows directly):
+    // identical block shapes on every rank, so the height is the max over ranks
+    sym_ = halo_ && ctx->comm.sym.on;
+    if (sym_) {
+        rows_cap_ = std::max<int64_t>(ctx->comm.halo.max_rows, 1);
+        ctx->comm.sym_reset();
+    }
     colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0;
     ld_ = colmajor_ ? ((rows_cap_ + 63) / 64) * 64 : max_cols;
     const int m3 = 3 * max_cols;
@@ -71,11 +78,20 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
     partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 + A.n_long + 64) * 64);
     norms_.alloc(64);
-    R_.alloc(block_elems(max_cols));
     H_.alloc(block_elems(max_cols));
     P_.alloc(block_elems(max_cols));
-    S_.alloc(block_elems(m3));
     AS_.alloc(block_elems(m3));
+    pR_ = input_block(max_cols, R_);
+    pS_ = input_block(m3, S_);
+    pW_ = input_block(max_cols, work_);
+    pPA_ = input_block(max_cols, prodA_);
+    pPB_ = input_block(max_cols, prodB_);
+}
+
+double* Solver::input_block(int cols, DBuf<double>& fallback) {
+    if (sym_) return ctx_->comm.sym_alloc(block_elems(cols), s_);
+    fallback.alloc(block_elems(cols));
+    return fallback.p;
 }
 
 void Solver::upload(const std::vector<double>& h, DBuf<double>& d) {
@@ -107,15 +123,35 @@ std::vector<double> Solver::gram_to_host(const TsSpec& spec, int& P, int& Q) {
 }
 
 void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
-    if (halo_) ctx_->comm.halo_exchange(Xlocal, m, s_);
-    const View& Xg = Xlocal;
     const bool timed = ctx_->time_spmm;
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    HaloFuse hf;
+    bool fused = false;
+    if (halo_) {
+        // mesh operators: the exchange runs inside the SpMM (interior tiles overlap it)
+        fused = spmm_col_path(A_, Xlocal, m, ea) && halo_fuse_prepare(ctx_->comm, Xlocal, m, hf, s_);
+        if (fused) {
+            ctx_->timers.halo_launches += 1;
+            ctx_->timers.halo_bytes += static_cast<double>(ctx_->comm.halo.total_send) * m * 8;
+        }
+    }
+    if (halo_ && !fused) {
+        if (timed) {
+            ev = ctx_->next_event_pair(2);
+            SPB_CUDA(cudaEventRecord(ev.first, s_));
+        }
+        const int64_t b0 = ctx_->comm.bytes_moved;
+        ctx_->comm.halo_exchange(Xlocal, m, s_);
+        if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
+        ctx_->timers.halo_launches += 1;
+        ctx_->timers.halo_bytes += static_cast<double>(ctx_->comm.bytes_moved - b0);
+    }
+    const View& Xg = Xlocal;
     if (timed) {
-        ev = ctx_->next_event_pair(ea.mode == EPI_POLY);
+        ev = ctx_->next_event_pair(ea.mode == EPI_POLY ? 1 : 0);
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
-    const int rows = spmm_launch(A_, Xg, m, ea, s_);
+    const int rows = spmm_launch(A_, Xg, m, ea, s_, fused ? &hf : nullptr);
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;
     // algorithmic bytes of this launch: index stream,
@@ -150,7 +186,7 @@ void Solver::residuals(const View& X, const std::vector<double>& theta, SolveRes
     const int nev = static_cast<int>(theta.size());
     EpiArgs ea;
     ea.mode = EPI_RESIDUAL;
-    ea.Y = block(R_.p, nev);
+    ea.Y = block(pR_, nev);
     ea.bdiag = bdiag_;
     for (int j = 0; j < nev; ++j) ea.theta[j] = theta[j];
     ea.partial = partial_.p;
@@ -387,11 +423,9 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         poly_first_only(n_, 1.0 / roots_[0], R.sub(0, k), H.sub(0, k), s_);
         return;
     }
-    prodA_.alloc(block_elems(max_cols_));
-    prodB_.alloc(block_elems(max_cols_));
     View cur = R.sub(0, k);
     for (int i = 0; i + 1 < deg; ++i) {
-        const View nxt = block((i % 2 == 0) ? prodA_.p : prodB_.p, k);
+        const View nxt = block((i % 2 == 0) ? pPA_ : pPB_, k);
         EpiArgs ea;
         ea.mode = EPI_POLY;
         ea.Y = nxt;
@@ -417,8 +451,10 @@ void Solver::build_poly(uint64_t seed, int degree) {
     // v0: seeded uniform(-1,1) (preconditioners.cpp:82-87), minus its mean, normalized
     // basis columns carry halo rows (they are SpMM inputs)
     const int64_t vld = rows_cap_;
-    DBuf<double> Vb(static_cast<size_t>(vld) * (k_req + 1));
-    auto vcol = [&](int j) { return colmajor(Vb.p + static_cast<size_t>(j) * vld, vld, 1); };
+    DBuf<double> Vbuf;
+    double* Vb = sym_ ? ctx_->comm.sym_alloc(static_cast<size_t>(vld) * (k_req + 1), s_)
+                      : (Vbuf.alloc(static_cast<size_t>(vld) * (k_req + 1)), Vbuf.p);
+    auto vcol = [&](int j) { return colmajor(Vb + static_cast<size_t>(j) * vld, vld, 1); };
     mt_uniform_block(seed, n_glob, 1, row0, n_, vcol(0), s_);
     const int rows = colsum_partials(n_, vcol(0), scratch_.p, s_);
     reduce_partials(scratch_.p, rows, 1, norms_.p, s_);
@@ -450,7 +486,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
     const double tiny = 1e-13 * (A_.bound > 0.0 ? A_.bound : 1.0);
     DBuf<double> wbuf(static_cast<size_t>(std::max<int64_t>(n_, 1)));
     const View w = colmajor(wbuf.p, std::max<int64_t>(n_, 1), 1);
-    const View Vall = colmajor(Vb.p, vld, k_req + 1);
+    const View Vall = colmajor(Vb, vld, k_req + 1);
     for (int j = 0; j < k_req; ++j) {
         spmm_store(vcol(j), 1, w);
         const View basis = Vall.sub(0, j + 1);
@@ -524,10 +560,10 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     res.residual_norms.assign(nev, 0.0);
 
     const int m3 = 3 * nev;
-    const View S = colmajor_ ? colmajor(S_.p, ld_, m3) : rowmajor(S_.p, m3, m3);
+    const View S = colmajor_ ? colmajor(pS_, ld_, m3) : rowmajor(pS_, m3, m3);
     const View AS = colmajor_ ? colmajor(AS_.p, ld_, m3) : rowmajor(AS_.p, m3, m3);
     const View Xv = X.sub(0, nev);
-    const View Rv = block(R_.p, nev);
+    const View Rv = block(pR_, nev);
     const View Hv = block(H_.p, nev);
     const View Pv = block(P_.p, nev);
     int p_cols = 0;
@@ -612,9 +648,8 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         View RI = Rv;
         if (na != nev) {
             // compact R_I into work_, then precondition into H
-            work_.alloc(block_elems(nev));
-            gather_cols(n_, Rv, active.data(), na, block(work_.p, na), s_);
-            RI = block(work_.p, na);
+            gather_cols(n_, Rv, active.data(), na, block(pW_, na), s_);
+            RI = block(pW_, na);
         }
         const View HI = block(H_.p, na);
         ctx_->prof.mark(s_, "lobpcg_misc");

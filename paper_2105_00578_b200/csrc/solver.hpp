@@ -67,6 +67,9 @@ public:
     bool colmajor_blocks() const { return colmajor_; }
     int64_t ld() const { return ld_; }
     View block(double* p, int cols) const { return colmajor_ ? colmajor(p, ld_, cols) : rowmajor(p, cols, cols); }
+    // A block that can be an SpMM input (symmetric heap on multi-GPU P2P runs;
+    // otherwise allocated into `fallback`). Collective in the multi-GPU case.
+    double* input_block(int cols, DBuf<double>& fallback);
     size_t block_elems(int cols) const { return static_cast<size_t>(colmajor_ ? ld_ : rows_cap_) * cols; }
 
 private:
@@ -92,6 +95,8 @@ private:
     int max_cols_;
     bool colmajor_ = false;
     bool halo_ = false;     // multi-GPU: inputs get their halo rows before each SpMM
+    bool sym_ = false;      // SpMM inputs live in the symmetric heap (P2P halo push)
+    double *pR_ = nullptr, *pS_ = nullptr, *pW_ = nullptr, *pPA_ = nullptr, *pPB_ = nullptr;
     int64_t rows_cap_ = 1;  // own rows + halo rows
     int64_t ld_ = 1;
     PrecKind prec_ = PREC_NONE;

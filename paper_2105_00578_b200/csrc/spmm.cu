@@ -14,6 +14,7 @@
 // CTA-per-row kernel with a fixed-order tree reduction (deterministic, not
 // bit-identical to the sequential sum).
 #include "ops.cuh"
+#include "p2p.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -361,8 +362,9 @@ __global__ void __launch_bounds__(kThreads) spmm_tile_kernel(const DevOp op, con
 // bit-identical; padded slots add +-0, which cannot change an accumulator that
 // starts at +0 (round-to-nearest never produces -0 from +0 by addition).
 // For mesh orderings the 32 lanes gather 32 consecutive addresses per slot.
-template <int MAXR, int MODE, int EPI, int CBT = 2, int MINB = 1>
-__global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea) {
+template <int MAXR, int MODE, int EPI, int CBT = 2, int MINB = 1, bool HF = false>
+__global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea,
+                                                                   const HaloFuse hf) {
     constexpr bool kRegs = MAXR <= 8;       // slots in registers, several columns per pass
     constexpr int NS = MAXR + 1;            // + the diagonal slot
     constexpr int NSR = kRegs ? NS : 1;
@@ -372,6 +374,11 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
+    // multi-GPU: push this rank's boundary rows into the peers' X first (p2p.cuh)
+    if (HF)
+        halo_push_part(hf, m, [&](int64_t r, int c) {
+            return const_cast<double*>(ta.X) + static_cast<int64_t>(c) * ta.ldx + r;
+        });
     if (EPI == EPI_RESIDUAL) {
         for (int c = threadIdx.x; c < m; c += kThreads) s_theta[c] = ea.theta[c];
         for (int c = lane; c < m; c += 32) s_sq[warp][c] = 0.0;
@@ -384,7 +391,17 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
     const uint64_t ldx8 = 8ull * static_cast<uint32_t>(ta.ldx);
     const char* xbase = reinterpret_cast<const char*>(ta.X);
-    for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
+    bool waited = false;
+    for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
+        int64_t tile = lt;
+        if (HF) {
+            // interior tiles first; the first halo-reading tile waits for the peers
+            if (lt >= hf.n_int && !waited) {
+                halo_wait_warp(hf);
+                waited = true;
+            }
+            tile = (lt + hf.rot) % ntiles;
+        }
         const int64_t row = tile * 32 + lane;
         const bool live = row < op.n;
         const int64_t grow = op.row0 + row;
@@ -581,14 +598,11 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
 }
 
 template <int MODE, int EPI>
-int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
+int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     int G = 1;
     while (G < m && G < 32) G <<= 1;
     // column-major blocks (regular graphs): row per lane
-    const bool colmajor = m > 1 ? (X.rs == 1 && ea.Y.rs == 1 && (ea.mode != EPI_POLY || ea.H.rs == 1))
-                                : (X.rs == 1 && ea.Y.rs == 1);
-    if (MODE != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && colmajor &&
-        std::max(op.x_rows, op.row0 + op.n) * 8 < (int64_t(1) << 32) && m <= kMaxCols) {
+    if (MODE != OP_DIAGONAL && spmm_col_path(op, X, m, ea)) {
         TileArgs ta;
         ta.X = X.ptr;
         ta.ldx = static_cast<int>(m > 1 ? X.cs : 0);
@@ -616,24 +630,29 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
                 occ.emplace_back(key, per_sm);
             }
             grid = grid_for(ntiles, kThreads / 32, per_sm);
-            kern<<<grid, kThreads, smem, s>>>(op, ta, ea);
+            kern<<<grid, kThreads, smem, s>>>(op, ta, ea, hf ? *hf : HaloFuse{});
         };
         static const int variant = [] {
             const char* e = std::getenv("SPB_SPMM_VARIANT");
             return e ? std::atoi(e) : 0;
         }();
+        // HF instantiations (halo exchange fused in) only for the default variants
         if (mr <= 8) {
-            switch (variant) {
-            case 1: go(spmm_col_kernel<8, MODE, EPI, 1, 1>, 8); break;
-            case 2: go(spmm_col_kernel<8, MODE, EPI, 1, 8>, 8); break;
-            case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
-            case 4: go(spmm_col_kernel<8, MODE, EPI, 4, 3>, 8); break;
-            case 5: go(spmm_col_kernel<8, MODE, EPI, 4, 1>, 8); break;
-            default: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
+            if (hf) {
+                go(spmm_col_kernel<8, MODE, EPI, 2, 5, true>, 8);
+            } else {
+                switch (variant) {
+                case 1: go(spmm_col_kernel<8, MODE, EPI, 1, 1>, 8); break;
+                case 2: go(spmm_col_kernel<8, MODE, EPI, 1, 8>, 8); break;
+                case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
+                case 4: go(spmm_col_kernel<8, MODE, EPI, 4, 3>, 8); break;
+                case 5: go(spmm_col_kernel<8, MODE, EPI, 4, 1>, 8); break;
+                default: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
+                }
             }
         }
-        else if (mr <= 16) go(spmm_col_kernel<16, MODE, EPI>, 16);
-        else go(spmm_col_kernel<32, MODE, EPI>, 32);
+        else if (mr <= 16) go(hf ? spmm_col_kernel<16, MODE, EPI, 2, 1, true> : spmm_col_kernel<16, MODE, EPI>, 16);
+        else go(hf ? spmm_col_kernel<32, MODE, EPI, 2, 1, true> : spmm_col_kernel<32, MODE, EPI>, 32);
         SPB_LAUNCH_CHECK();
         return grid;
     }
@@ -706,12 +725,12 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
 }
 
 template <int EPI>
-int launch_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
+int launch_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     switch (op.mode) {
-    case OP_EXPLICIT: return launch_mode_epi<OP_EXPLICIT, EPI>(op, X, m, ea, s);
-    case OP_LAPLACE_UNIT: return launch_mode_epi<OP_LAPLACE_UNIT, EPI>(op, X, m, ea, s);
-    case OP_NORMAL_UNIT: return launch_mode_epi<OP_NORMAL_UNIT, EPI>(op, X, m, ea, s);
-    default: return launch_mode_epi<OP_DIAGONAL, EPI>(op, X, m, ea, s);
+    case OP_EXPLICIT: return launch_mode_epi<OP_EXPLICIT, EPI>(op, X, m, ea, s, hf);
+    case OP_LAPLACE_UNIT: return launch_mode_epi<OP_LAPLACE_UNIT, EPI>(op, X, m, ea, s, hf);
+    case OP_NORMAL_UNIT: return launch_mode_epi<OP_NORMAL_UNIT, EPI>(op, X, m, ea, s, hf);
+    default: return launch_mode_epi<OP_DIAGONAL, EPI>(op, X, m, ea, s, hf);
     }
 }
 
@@ -728,15 +747,23 @@ __global__ void reduce_partials_kernel(const double* partial, int rows, int m, d
 
 } // namespace
 
-int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
+int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     if (m <= 0) return 0;
     if (ea.mode != EPI_STORE && m > 32)
         throw_dimension("spmm: fused epilogues support at most 32 columns");
+    if (hf && !spmm_col_path(op, X, m, ea)) throw SpError(1, "spmm: fused halo exchange needs the column kernel");
     switch (ea.mode) {
-    case EPI_STORE: return launch_epi<EPI_STORE>(op, X, m, ea, s);
-    case EPI_RESIDUAL: return launch_epi<EPI_RESIDUAL>(op, X, m, ea, s);
-    default: return launch_epi<EPI_POLY>(op, X, m, ea, s);
+    case EPI_STORE: return launch_epi<EPI_STORE>(op, X, m, ea, s, hf);
+    case EPI_RESIDUAL: return launch_epi<EPI_RESIDUAL>(op, X, m, ea, s, hf);
+    default: return launch_epi<EPI_POLY>(op, X, m, ea, s, hf);
     }
+}
+
+bool spmm_col_path(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
+    const bool colmajor = m > 1 ? (X.rs == 1 && ea.Y.rs == 1 && (ea.mode != EPI_POLY || ea.H.rs == 1))
+                                : (X.rs == 1 && ea.Y.rs == 1);
+    return op.mode != OP_DIAGONAL && op.max_row <= 32 && op.n_long == 0 && colmajor &&
+           std::max(op.x_rows, op.row0 + op.n) * 8 < (int64_t(1) << 32) && m <= kMaxCols;
 }
 
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s) {

@@ -18,7 +18,10 @@ def _ngpus():
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-def test_row_partitioned_matches_reference():
+@pytest.mark.parametrize("p2p", ["1", "0"])  # NVLink peer-memory halo/sums, or the NCCL fallback
+def test_row_partitioned_matches_reference(p2p):
+    import os
+    env = dict(os.environ, SPB_P2P=p2p)
     n = min(_ngpus(), 4)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -26,7 +29,7 @@ def test_row_partitioned_matches_reference():
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "dist_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
     line = [l for l in r.stdout.splitlines() if l.startswith("DIST_RESULT ")]
     assert r.returncode == 0 and line, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(line[0][len("DIST_RESULT "):])
