@@ -743,9 +743,10 @@ sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* hg, uint6
         Solver solver(ctx, A.op, nullptr, m);
         solver.build_poly(seed, degree > 0 ? degree : 25);
         const int64_t n = g.n_local;
-        DBuf<double> rd(solver.block_elems(m)), hd(solver.block_elems(m));
-        upload_block(Rh, n, 0, n, m, solver.block(rd.p, m), s);
-        solver.apply_precond(solver.block(rd.p, m), m, solver.block(hd.p, m));
+        DBuf<double> rd, hd(solver.block_elems(m));
+        const View Rv = solver.block(solver.input_block(m, rd), m);
+        upload_block(Rh, n, 0, n, m, Rv, s);
+        solver.apply_precond(Rv, m, solver.block(hd.p, m));
         download_block(solver.block(hd.p, m), n, m, H_out, s);
         const std::vector<double>& rt = solver.roots();
         if (roots_out) std::memcpy(roots_out, rt.data(), sizeof(double) * rt.size());

@@ -172,7 +172,7 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
 
     // 2./3. local column ids, diagonal slots, isd over own + halo rows; halo
     // rows start at a 32-row boundary so no cache line holds own and halo rows
-    const int64_t base = (nloc + 31) / 32 * 32;
+    const int64_t base = (nloc + 1 + 31) / 32 * 32;  // row nloc stays zero (ELL padding)
     hp.halo_base = base;
     {
         DBuf<unsigned long long> pq(2);
@@ -263,7 +263,7 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
         int64_t maxrows = 0;
         for (int p = 0; p < world; ++p) {
             const int64_t r0p = static_cast<int64_t>(p) * cm.n_pad;
-            const int64_t nlp = (((r0p >= n ? 0 : std::min<int64_t>(cm.n_pad, n - r0p))) + 31) / 32 * 32;
+            const int64_t nlp = (((r0p >= n ? 0 : std::min<int64_t>(cm.n_pad, n - r0p))) + 1 + 31) / 32 * 32;
             int64_t nhp = 0, before_me = 0;
             for (int q = 0; q < world; ++q) {
                 nhp += M[static_cast<size_t>(p) * world + q];

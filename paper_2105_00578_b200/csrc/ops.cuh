@@ -40,6 +40,12 @@ struct DevOp {
     // dpos[i] is the storage slot of the diagonal (count of global cols < global i)
     const int32_t* dpos = nullptr;
     int64_t x_rows = 0;         // rows of the SpMM input block the columns address
+    // fixed-slot ELL of a mesh Laplacian (spmm_ell_kernel), built by the solver;
+    // slot s of row i at ell[s*ell_ld + i]; padding slots hold ell_zero_row
+    const int32_t* ell = nullptr;
+    int ell_kl = 0, ell_ku = 0;
+    int64_t ell_ld = 0;
+    int64_t ell_zero_row = 0;
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -72,6 +78,9 @@ int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t
                 const HaloFuse* hf = nullptr);
 // true when spmm_launch uses the column-major row-per-lane kernel for these arguments
 bool spmm_col_path(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+// Builds the fixed-slot ELL of a LAPLACE_UNIT operator (spmm.cu); returns false
+// (op unchanged) when the rows are too wide. Padding slots point at zero_row.
+bool build_ell(DevOp& op, int64_t zero_row, DBuf<int32_t>& store, cudaStream_t s);
 // Reduce partial[rows x m] over rows in fixed order into out[m] (device).
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s);
 

@@ -14,6 +14,8 @@
 // orthogonality to rounding level when the coefficient recurrence lost it.
 #include "solver.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -61,7 +63,8 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     // a halo plan (operator not localized) the input is all-gathered instead
     halo_ = ctx->comm.active() && ctx->comm.halo.on;
     if (ctx->comm.active() && !halo_) throw SpError(1, "Solver: multi-GPU operator without a halo plan");
-    rows_cap_ = std::max<int64_t>(halo_ ? ctx->comm.halo.halo_base + ctx->comm.halo.nhalo : n_, 1);
+    // row n_ of every SpMM input block is kept zero (ELL padding target)
+    rows_cap_ = std::max<int64_t>(halo_ ? ctx->comm.halo.halo_base + ctx->comm.halo.nhalo : n_ + 1, 1);
     // SpMM inputs in the symmetric heap (peers write their halo rows directly):
     // identical block shapes on every rank, so the height is the max over ranks
     sym_ = halo_ && ctx->comm.sym.on;
@@ -71,6 +74,11 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     }
     colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0;
     ld_ = colmajor_ ? ((rows_cap_ + 63) / 64) * 64 : max_cols;
+    static const bool no_ell = [] {
+        const char* e = std::getenv("SPB_NO_ELL");
+        return e && e[0] == '1';
+    }();
+    if (colmajor_ && !no_ell) build_ell(A_, n_, ell_, s_);
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
@@ -89,9 +97,17 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
 }
 
 double* Solver::input_block(int cols, DBuf<double>& fallback) {
-    if (sym_) return ctx_->comm.sym_alloc(block_elems(cols), s_);
-    fallback.alloc(block_elems(cols));
-    return fallback.p;
+    double* p;
+    if (sym_) {
+        p = ctx_->comm.sym_alloc(block_elems(cols), s_);
+    } else {
+        fallback.alloc(block_elems(cols));
+        p = fallback.p;
+    }
+    // the zero row (ELL padding slots gather it)
+    if (colmajor_ && cols > 0)
+        SPB_CUDA(cudaMemset2DAsync(p + n_, sizeof(double) * ld_, 0, sizeof(double), cols, s_));
+    return p;
 }
 
 void Solver::upload(const std::vector<double>& h, DBuf<double>& d) {
@@ -455,6 +471,8 @@ void Solver::build_poly(uint64_t seed, int degree) {
     double* Vb = sym_ ? ctx_->comm.sym_alloc(static_cast<size_t>(vld) * (k_req + 1), s_)
                       : (Vbuf.alloc(static_cast<size_t>(vld) * (k_req + 1)), Vbuf.p);
     auto vcol = [&](int j) { return colmajor(Vb + static_cast<size_t>(j) * vld, vld, 1); };
+    if (n_ < vld)  // zero row of the basis columns (ELL padding target)
+        SPB_CUDA(cudaMemset2DAsync(Vb + n_, sizeof(double) * vld, 0, sizeof(double), k_req + 1, s_));
     mt_uniform_block(seed, n_glob, 1, row0, n_, vcol(0), s_);
     const int rows = colsum_partials(n_, vcol(0), scratch_.p, s_);
     reduce_partials(scratch_.p, rows, 1, norms_.p, s_);

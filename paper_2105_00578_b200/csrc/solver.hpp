@@ -103,6 +103,7 @@ private:
     const double* inv_diag_ = nullptr;
     std::vector<double> roots_;
 
+    DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
     DBuf<double> gram_, scratch_, cmat_, cmat2_, partial_, norms_;
     DBuf<double> R_, H_, P_, S_, AS_, prodA_, prodB_, work_;
 };

@@ -597,6 +597,118 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
     }
 }
 
+// Laplacian of a mesh in fixed-slot ELL form (spmm_ell_kernel). Built once per
+// operator by the solver: row i keeps its columns < i right-aligned in slots
+// [0, KL), its columns > i left-aligned in [KL, KL+KU), padding slots point at
+// a zero row of the input block. The reference's row sum (laplacian.cpp:53-79:
+// off-diagonals in column order with the diagonal spliced before the first
+// column > i) is then the same straight-line chain for every row:
+//   acc = 0; acc -= x_s (s < KL); acc += deg_i * x_i; acc -= x_s (s >= KL)
+// Subtracting a padding zero leaves the accumulator unchanged (acc - 0 == acc,
+// also for -0), and (-1) * x_j == -x_j exactly, so the result is bit-identical
+// to the CSR kernels. No per-row slot construction, no offsets, 32-bit gathers.
+template <int KL, int KU, int EPI, int CB, int MINB, bool HF>
+__global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea,
+                                                                   const HaloFuse hf) {
+    constexpr int W = KL + KU;
+    __shared__ double s_sq[kThreads / 32][kMaxCols];
+    __shared__ double s_theta[kMaxCols];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int m = ta.m;
+    if (HF)
+        halo_push_part(hf, m, [&](int64_t r, int c) {
+            return const_cast<double*>(ta.X) + static_cast<int64_t>(c) * ta.ldx + r;
+        });
+    if (EPI == EPI_RESIDUAL) {
+        for (int c = threadIdx.x; c < m; c += kThreads) s_theta[c] = ea.theta[c];
+        for (int c = lane; c < m; c += 32) s_sq[warp][c] = 0.0;
+        __syncthreads();
+    }
+    const int64_t ntiles = (op.n + 31) / 32;
+    const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+    const uint32_t zrow = static_cast<uint32_t>(op.ell_zero_row);
+    bool waited = false;
+    for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
+        int64_t tile = lt;
+        if (HF) {
+            if (lt >= hf.n_int && !waited) {
+                halo_wait_warp(hf);
+                waited = true;
+            }
+            tile = (lt + hf.rot) % ntiles;
+        }
+        const int64_t row = tile * 32 + lane;
+        const bool live = row < op.n;
+        uint32_t j[W];
+#pragma unroll
+        for (int sidx = 0; sidx < W; ++sidx)
+            j[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
+        const double dw = live ? __ldg(op.diag + row) : 0.0;
+        const uint32_t own = live ? static_cast<uint32_t>(row) : zrow;
+        for (int c0 = 0; c0 < m; c0 += CB) {
+            const double* xc[CB];
+            bool on[CB];
+            double xi[CB], hv[CB], acc[CB];
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                on[q] = c0 + q < m;
+                xc[q] = ta.X + static_cast<int64_t>(on[q] ? c0 + q : c0) * ta.ldx;
+                xi[q] = __ldg(xc[q] + own);
+                hv[q] = 0.0;
+                if (EPI == EPI_POLY && !ea.first && ea.h_terms && live && on[q])
+                    hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
+                acc[q] = 0.0;
+            }
+#pragma unroll
+            for (int sidx = 0; sidx < KL; ++sidx)
+#pragma unroll
+                for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], __ldg(xc[q] + j[sidx]));
+#pragma unroll
+            for (int q = 0; q < CB; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(dw, xi[q]));
+#pragma unroll
+            for (int sidx = KL; sidx < W; ++sidx)
+#pragma unroll
+                for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], __ldg(xc[q] + j[sidx]));
+#pragma unroll
+            for (int q = 0; q < CB; ++q) {
+                double sq = 0.0;
+                if (live && on[q]) {
+                    const int c = c0 + q;
+                    const int64_t yo = static_cast<int64_t>(c) * ta.ldy + row;
+                    if (EPI == EPI_STORE) {
+                        ta.Y[yo] = acc[q];
+                    } else if (EPI == EPI_RESIDUAL) {
+                        const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[row], xi[q]) : xi[q];
+                        const double r = __dsub_rn(acc[q], __dmul_rn(s_theta[c], bx));
+                        ta.Y[yo] = r;
+                        sq = r * r;
+                    } else {
+                        const double pn = __dsub_rn(xi[q], __dmul_rn(ea.inv_cur, acc[q]));
+                        ta.Y[yo] = pn;
+                        if (ea.h_terms)
+                            ta.H[static_cast<int64_t>(c) * ta.ldh + row] = poly_h(ea, hv[q], xi[q], pn);
+                    }
+                }
+                if (EPI == EPI_RESIDUAL) {
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+                    if (lane == 0 && on[q]) s_sq[warp][c0 + q] += sq;
+                }
+            }
+        }
+    }
+    if (EPI == EPI_RESIDUAL) {
+        __syncthreads();
+        for (int c = threadIdx.x; c < m; c += kThreads) {
+            double s = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) s += s_sq[w][c];
+            ea.partial[static_cast<int64_t>(blockIdx.x) * m + c] = s;
+        }
+    }
+}
+
 template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     int G = 1;
@@ -636,6 +748,34 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             const char* e = std::getenv("SPB_SPMM_VARIANT");
             return e ? std::atoi(e) : 0;
         }();
+        if (MODE == OP_LAPLACE_UNIT && op.ell) {
+            // fixed-slot ELL (meshes): the slot pair is chosen by the solver
+            static const int evariant = [] {
+                const char* e = std::getenv("SPB_ELL_VARIANT");
+                return e ? std::atoi(e) : 0;
+            }();
+#define SPB_ELL(KL_, KU_)                                                                                   \
+    do {                                                                                                    \
+        if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                          \
+        else if (evariant == 1) go(spmm_ell_kernel<KL_, KU_, EPI, 1, 6, false>, 0);                         \
+        else if (evariant == 2) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 5, false>, 0);                         \
+        else if (evariant == 3) go(spmm_ell_kernel<KL_, KU_, EPI, 4, 3, false>, 0);                         \
+        else go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, false>, 0);                                            \
+    } while (0)
+            switch (op.ell_kl * 100 + op.ell_ku) {
+            case 202: SPB_ELL(2, 2); break;
+            case 303: SPB_ELL(3, 3); break;
+            case 404: SPB_ELL(4, 4); break;
+            case 1313: SPB_ELL(13, 13); break;
+            default:
+                if (op.ell_kl == 8 && op.ell_ku == 8) SPB_ELL(8, 8);
+                else SPB_ELL(16, 16);
+                break;
+            }
+#undef SPB_ELL
+            SPB_LAUNCH_CHECK();
+            return grid;
+        }
         // HF instantiations (halo exchange fused in) only for the default variants
         if (mr <= 8) {
             if (hf) {
@@ -757,6 +897,73 @@ int spmm_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t
     case EPI_RESIDUAL: return launch_epi<EPI_RESIDUAL>(op, X, m, ea, s, hf);
     default: return launch_epi<EPI_POLY>(op, X, m, ea, s, hf);
     }
+}
+
+namespace {
+__device__ __forceinline__ int ell_lower(const DevOp& op, int64_t i, int64_t k0, int len) {
+    if (op.dpos) return op.dpos[i];
+    int c = 0;
+    for (int t = 0; t < len; ++t) c += op.cols[k0 + t] < op.row0 + i ? 1 : 0;
+    return c;
+}
+__global__ void ell_count_kernel(const DevOp op, unsigned* klku) {
+    unsigned kl = 0, ku = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k0 = op.offs[i];
+        const int len = static_cast<int>(op.offs[i + 1] - k0);
+        const int lo = ell_lower(op, i, k0, len);
+        kl = max(kl, static_cast<unsigned>(lo));
+        ku = max(ku, static_cast<unsigned>(len - lo));
+    }
+    atomicMax(&klku[0], kl);
+    atomicMax(&klku[1], ku);
+}
+__global__ void ell_fill_kernel(const DevOp op, int KL, int KU, int64_t ld, int32_t zrow, int32_t* ell) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t k0 = op.offs[i];
+        const int len = static_cast<int>(op.offs[i + 1] - k0);
+        const int lo = ell_lower(op, i, k0, len);
+        const int up = len - lo;
+        for (int s = 0; s < KL - lo; ++s) ell[s * ld + i] = zrow;
+        for (int t = 0; t < lo; ++t) ell[(KL - lo + t) * ld + i] = op.cols[k0 + t];
+        for (int t = 0; t < up; ++t) ell[(KL + t) * ld + i] = op.cols[k0 + lo + t];
+        for (int s = KL + up; s < KL + KU; ++s) ell[s * ld + i] = zrow;
+    }
+}
+} // namespace
+
+bool build_ell(DevOp& op, int64_t zero_row, DBuf<int32_t>& store, cudaStream_t s) {
+    if (op.mode != OP_LAPLACE_UNIT || op.n <= 0 || op.n_long > 0 || op.max_row > 32) return false;
+    DBuf<unsigned> klku(2);
+    SPB_CUDA(cudaMemsetAsync(klku.p, 0, 2 * sizeof(unsigned), s));
+    ell_count_kernel<<<grid_for(op.n, 256, 4), 256, 0, s>>>(op, klku.p);
+    SPB_LAUNCH_CHECK();
+    unsigned h[2];
+    SPB_CUDA(cudaMemcpyAsync(h, klku.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    int KL, KU;
+    const unsigned kl = h[0], ku = h[1];
+    if ((kl == 2 && ku == 2) || (kl == 3 && ku == 3) || (kl == 4 && ku == 4) || (kl == 13 && ku == 13)) {
+        KL = static_cast<int>(kl);
+        KU = static_cast<int>(ku);
+    } else if (kl <= 8 && ku <= 8) {
+        KL = KU = 8;
+    } else if (kl <= 16 && ku <= 16) {
+        KL = KU = 16;
+    } else {
+        return false;
+    }
+    store.alloc(static_cast<size_t>(KL + KU) * op.n);
+    ell_fill_kernel<<<grid_for(op.n, 256, 4), 256, 0, s>>>(op, KL, KU, op.n, static_cast<int32_t>(zero_row), store.p);
+    SPB_LAUNCH_CHECK();
+    op.ell = store.p;
+    op.ell_kl = KL;
+    op.ell_ku = KU;
+    op.ell_ld = op.n;
+    op.ell_zero_row = zero_row;
+    return true;
 }
 
 bool spmm_col_path(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
