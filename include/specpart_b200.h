@@ -211,6 +211,14 @@ sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64
 
 /* G = U^T diag(b) V (kernels::gram, kernels.cpp:79-110; b == NULL means identity).
  * U: n x mu, V: n x mv column-major; G: mu x mv column-major. Deterministic. */
+/* Diagnostics: times the tall-skinny block kernel (Gram / block update /
+ * block combine, blockops.cu) on device-resident column-major blocks of n rows
+ * filled with uniform(-1,1) data: mu columns of U, mv of V; transform 0 none,
+ * 1 W = V - U C, 2 W = V C (C: mv x mw); gram 0 none, 1 [U V]^T V-or-W, 2
+ * U^T V-or-W, 3 (V-or-W)^T (V-or-W). Writes the mean device ms per call over
+ * iters calls (after one warm-up) to ms_out. */
+sp_status sp_bench_blockop(sp_context* ctx, int64_t n, int32_t mu, int32_t mv, int32_t mw, int32_t transform,
+                           int32_t gram, int32_t iters, double* ms_out);
 sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const double* V,
                   int32_t mv, const double* b, double* G);
 

@@ -125,6 +125,7 @@ SIGNATURES = {
     "sp_spmm": (I32, [P, I32, C.POINTER(SpGraph), P, I32, P]),
     "sp_spmm_csr": (I32, [P, I64, I64, P, P, P, P, I32, P]),
     "sp_gram": (I32, [P, I64, P, I32, P, I32, P, P]),
+    "sp_bench_blockop": (I32, [P, I64, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),
     "sp_initial_guess": (I32, [P, I32, I64, I32, U64, P]),
     "sp_lobpcg": (I32, [P, C.POINTER(SpGraph), I32, I32, U64, I32, P, I32, F64, I32, I32, P, P, P, P,
                         C.POINTER(I32), C.POINTER(I32)]),

@@ -665,6 +665,49 @@ sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const
     });
 }
 
+sp_status sp_bench_blockop(sp_context* ctx, int64_t n, int32_t mu, int32_t mv, int32_t mw, int32_t transform,
+                           int32_t gram, int32_t iters, double* ms_out) {
+    return guarded(ctx, [&] {
+        if (n < 1 || mv < 1 || mu < 0 || iters < 1) throw_invalid("sp_bench_blockop: bad sizes");
+        if (transform == TS_UPDATE && mu < 1) throw_invalid("sp_bench_blockop: update needs mu >= 1");
+        cudaStream_t s = ctx->stream;
+        const int64_t ld = (n + 63) / 64 * 64;
+        const int kw = transform == TS_UPDATE ? mv : (transform == TS_COMBINE ? mw : 0);
+        DBuf<double> ub(static_cast<size_t>(ld) * std::max(mu, 1)), vb(static_cast<size_t>(ld) * mv),
+            wb(static_cast<size_t>(ld) * std::max(kw, 1)), cb(static_cast<size_t>(std::max(mu, mv)) * std::max(kw, 1) + 1),
+            gb(static_cast<size_t>(mu + mv + kw) * (mv + kw) + 64),
+            scratch(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(mu + mv + kw) * (mv + kw) + 64));
+        mt_uniform_block(7, ld, std::max(mu, 1), 0, ld, colmajor(ub.p, ld, std::max(mu, 1)), s);
+        mt_uniform_block(8, ld, mv, 0, ld, colmajor(vb.p, ld, mv), s);
+        mt_uniform_block(9, static_cast<int64_t>(cb.n), 1, 0, static_cast<int64_t>(cb.n), colmajor(cb.p, static_cast<int64_t>(cb.n), 1), s);
+        TsSpec sp;
+        sp.n = n;
+        sp.U0 = mu > 0 ? colmajor(ub.p, ld, mu) : View{};
+        sp.V = colmajor(vb.p, ld, mv);
+        sp.transform = transform;
+        if (transform != TS_NONE) {
+            sp.W = colmajor(wb.p, ld, kw);
+            sp.C = cb.p;
+        }
+        sp.gram = gram != 0;
+        sp.gram_left_u = gram == 1 || gram == 2;
+        sp.gram_left_self = gram == 1 || gram == 3;
+        ts_run(sp, gb.p, scratch.p, scratch.n, s);
+        cudaEvent_t e0, e1;
+        SPB_CUDA(cudaEventCreate(&e0));
+        SPB_CUDA(cudaEventCreate(&e1));
+        SPB_CUDA(cudaEventRecord(e0, s));
+        for (int it = 0; it < iters; ++it) ts_run(sp, gb.p, scratch.p, scratch.n, s);
+        SPB_CUDA(cudaEventRecord(e1, s));
+        SPB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms / iters;
+    });
+}
+
 sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed, double* X_out) {
     return guarded(ctx, [&] {
         cudaStream_t s = ctx->stream;

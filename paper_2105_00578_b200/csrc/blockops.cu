@@ -14,6 +14,7 @@
 #include "ops.cuh"
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 
 namespace spb {
@@ -412,6 +413,275 @@ __global__ void __launch_bounds__(kTsThreads) ts_mma_kernel(const TsDev a) {
 }
 
 // ---------------------------------------------------------------------------
+// Column-major blocks fed by the bulk-copy engine (ts_bulk_kernel). Every
+// operand column's tile segment (TR rows, contiguous) is one cp.async.bulk
+// issued by a single thread into a ring of smem stages tracked by mbarriers,
+// so staging costs a handful of instructions per tile instead of one per
+// element. Smem columns have stride SC = TR + 4 doubles: both DMMA fragment
+// shapes used here (8 rows x 4 columns for the transform's A, 4 rows x 8
+// columns for the Gram) then hit every bank pair exactly twice (two
+// wavefronts, conflict-free). The transform (W = V - U C or V C) runs on
+// DMMA.8x8x4 per 8-row strip; the Gram splits the tile's k-steps over the
+// warps; per-warp fragments are summed in a fixed order (deterministic).
+constexpr int kBulkMaxBlk = 9;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Stage layout (columns of SC doubles): U [0, u) | V [cV, cV+kv) | 3 zero | b.
+// The zero columns pad the transform's k-steps past V (COMBINE) and stand in
+// for Gram fragment rows/columns past P/Q; past U (UPDATE) the k-steps read V
+// columns against zero rows of the padded C. Warp w owns the 8-row strips
+// w, w+8, ... of every tile for both the transform and the Gram, so W (one
+// per-CTA smem buffer) needs only warp-level synchronization and each tile
+// costs one block barrier.
+struct BulkCfg {
+    int TR, SC, nst;
+    int nload;        // bulk-loaded columns per stage
+    int has_b;
+    int ncol;         // columns per stage
+    int cV, cb, zc;
+};
+
+template <int NBLK>  // Gram 8x8 blocks (MB*NB), compile-time so the k-step loop is straight-line
+__global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, const BulkCfg g) {
+    constexpr int NCH = NBLK <= 2 ? 4 : 2;  // independent accumulator chains per block
+    extern __shared__ __align__(128) double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int TR = g.TR, SC = g.SC;
+    const int u = a.u0 + a.u1;
+    const int inner = a.transform == TS_UPDATE ? u : a.kv;
+    const int KBp = (inner + 3) / 4 * 4, NWp = (a.kw + 7) / 8 * 8;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    const double** src = reinterpret_cast<const double**>(smem + 8);
+    int* scol = reinterpret_cast<int*>(smem + 8 + 64);
+    double* st0 = smem + 8 + 64 + 64;
+    const size_t stage_elems = static_cast<size_t>(g.ncol) * SC;
+    double* Wb = st0 + g.nst * stage_elems;              // kw columns
+    double* Cs = Wb + static_cast<size_t>(a.kw) * SC;     // KBp x NWp column-major, zero padded
+    if (threadIdx.x == 0) {
+        for (int s2 = 0; s2 < g.nst; ++s2) mbar_init(bar + s2, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        int c = 0;
+        if ((a.transform == TS_UPDATE) || (a.gram && a.left_u)) {
+            for (int j = 0; j < a.u0; ++j, ++c) { src[c] = a.U0.ptr + static_cast<int64_t>(j) * a.U0.cs; scol[c] = j; }
+            for (int j = 0; j < a.u1; ++j, ++c) { src[c] = a.U1.ptr + static_cast<int64_t>(j) * a.U1.cs; scol[c] = a.u0 + j; }
+        }
+        for (int j = 0; j < a.kv; ++j, ++c) { src[c] = a.V.ptr + static_cast<int64_t>(j) * a.V.cs; scol[c] = g.cV + j; }
+        if (g.has_b) { src[c] = a.b; scol[c] = g.cb; }
+    }
+    if (a.transform != TS_NONE)
+        for (int i = threadIdx.x; i < KBp * NWp; i += blockDim.x) {
+            const int c = i / KBp, q = i - c * KBp;
+            Cs[i] = (q < inner && c < a.kw) ? a.C[q + static_cast<int64_t>(c) * a.ldc] : 0.0;
+        }
+    for (int s2 = 0; s2 < g.nst; ++s2)
+        for (int e = threadIdx.x; e < 3 * TR; e += blockDim.x) {
+            const int zz = e / TR, r = e - zz * TR;
+            st0[s2 * stage_elems + static_cast<size_t>(g.zc + zz) * SC + r] = 0.0;
+        }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    const int ntiles = static_cast<int>((a.n + TR - 1) / TR);
+    const int nt = ntiles > static_cast<int>(blockIdx.x) ? (ntiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1 : 0;
+    auto issue = [&](int tile, int s2) {
+        const int64_t r0 = static_cast<int64_t>(tile) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        const int brows = rows & ~1;  // bulk sizes are multiples of 16 B
+        double* T = st0 + s2 * stage_elems;
+        mbar_expect_tx(bar + s2, static_cast<unsigned>(brows) * 8u * g.nload);
+        if (brows > 0)
+            for (int c = 0; c < g.nload; ++c) bulk_g2s(T + scol[c] * SC, src[c] + r0, brows * 8u, bar + s2);
+    };
+    if (threadIdx.x == 0)
+        for (int s2 = 0; s2 < g.nst && s2 < nt; ++s2) issue(blockIdx.x + s2 * gridDim.x, s2);
+
+    const bool right_w = a.transform != TS_NONE;
+    const int uL = a.left_u ? u : 0;
+    const int MB = a.gram ? (a.P + 7) / 8 : 0, NB = a.gram ? (a.Q + 7) / 8 : 0;
+    const int nblk = MB * NB;
+    // per block: this lane's fragment column, in the stage (>= 0) or in W (-1 - col).
+    // Two accumulator chains per block (DMMA latency ~137 cycles: independent
+    // chains keep the tensor pipe busy); summed in a fixed order at the end.
+    constexpr int NB1 = NBLK > 0 ? NBLK : 1;
+    int lcol[NB1], rcol[NB1];
+    double acc0[NB1][NCH], acc1[NB1][NCH];
+    {
+        int mb = 0, nb = 0;
+#pragma unroll
+        for (int t = 0; t < NB1; ++t) {
+            const int mrow = mb * 8 + gid, ncol = nb * 8 + gid;
+            int l = g.zc, r = g.zc;
+            if (t < nblk && mrow < a.P) l = mrow < uL ? mrow : (right_w ? -1 - (mrow - uL) : g.cV + mrow - uL);
+            if (t < nblk && ncol < a.Q) r = right_w ? -1 - ncol : g.cV + ncol;
+            lcol[t] = l;
+            rcol[t] = r;
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) acc0[t][c] = acc1[t][c] = 0.0;
+            if (++mb == MB) {
+                mb = 0;
+                ++nb;
+            }
+        }
+    }
+    const int a_col = a.transform == TS_UPDATE ? 0 : g.cV;
+    const int w1 = a.W.cols;
+    const int spw = TR / 64;  // strips per warp per tile (warp w: strips w, w+8, ...)
+
+    int tile = blockIdx.x, s2 = 0;
+    unsigned ph = 0;
+    for (int i = 0; i < nt; ++i, tile += gridDim.x) {
+        const int64_t r0 = static_cast<int64_t>(tile) * TR;
+        const int rows = static_cast<int>(min(static_cast<int64_t>(TR), a.n - r0));
+        double* T = st0 + s2 * stage_elems;
+        mbar_wait(bar + s2, ph);
+        if (rows < TR) {
+            // tail tile (the CTA's last): odd last row by hand, zero rows [rows, TR)
+            if (rows & 1)
+                for (int c = threadIdx.x; c < g.nload; c += blockDim.x) T[scol[c] * SC + rows - 1] = src[c][r0 + rows - 1];
+            for (int e = threadIdx.x; e < g.nload * (TR - rows); e += blockDim.x) {
+                const int c = e / (TR - rows), r = rows + e - c * (TR - rows);
+                T[scol[c] * SC + r] = 0.0;
+            }
+            __syncthreads();
+        }
+        const double* lp[NB1];
+        const double* rp[NB1];
+#pragma unroll
+        for (int t = 0; t < NB1; ++t) {
+            lp[t] = (lcol[t] >= 0 ? T + lcol[t] * SC : Wb + (-1 - lcol[t]) * SC) + tig;
+            rp[t] = (rcol[t] >= 0 ? T + rcol[t] * SC : Wb + (-1 - rcol[t]) * SC) + tig;
+        }
+        const double* bcol = T + g.cb * SC + tig;
+        // groups of 4 strips: 4 independent DMMA chains in the transform
+        for (int j0 = 0; j0 < spw; j0 += 4) {
+            if (right_w) {
+                for (int nb = 0; nb * 8 < a.kw; ++nb) {
+                    double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+                    const double* ap = T + (a_col + tig) * SC + (warp + 8 * j0) * 8 + gid;
+                    const double* cp = Cs + (nb * 8 + gid) * KBp + tig;
+                    for (int k0 = 0; k0 < KBp; k0 += 4) {
+                        const double cv = *cp;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (j0 + j < spw) dmma(d0[j], d1[j], ap[j * 64], cv);
+                        ap += 4 * SC;
+                        cp += 4;
+                    }
+                    const int c0 = nb * 8 + 2 * tig;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j0 + j >= spw) break;
+                        const int rr = (warp + 8 * (j0 + j)) * 8 + gid;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int cc = c0 + h;
+                            if (cc < a.kw) {
+                                double w = h ? d1[j] : d0[j];
+                                if (a.transform == TS_UPDATE) w = T[(g.cV + cc) * SC + rr] - w;
+                                Wb[cc * SC + rr] = w;
+                                if (rr < rows) {
+                                    double* dst = cc < w1 ? a.W.ptr + static_cast<int64_t>(cc) * a.W.cs
+                                                          : a.W2.ptr + static_cast<int64_t>(cc - w1) * a.W2.cs;
+                                    dst[r0 + rr] = w;
+                                }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (NBLK > 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j0 + j >= spw) break;
+                    const int sr = (warp + 8 * (j0 + j)) * 8;
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int k0 = sr + 4 * kk;
+                        const int ch = (j * 2 + kk) % NCH;
+                        const double bb = g.has_b ? bcol[k0] : 1.0;
+#pragma unroll
+                        for (int t = 0; t < NBLK; ++t) {
+                            double bv = rp[t][k0];
+                            if (g.has_b) bv *= bb;
+                            dmma(acc0[t][ch], acc1[t][ch], lp[t][k0], bv);
+                        }
+                    }
+                }
+            }
+            if (right_w) __syncwarp();  // W rows of these strips are rewritten next tile
+        }
+        __syncthreads();  // stage s2 free
+        if (threadIdx.x == 0 && i + g.nst < nt) issue(tile + g.nst * gridDim.x, s2);
+        if (++s2 == g.nst) {
+            s2 = 0;
+            ph ^= 1u;
+        }
+    }
+
+    if (!a.gram) return;
+    double* red = st0;
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NB1; ++t) {
+        if (t < nblk) {
+            double s0 = acc0[t][0], s1 = acc1[t][0];
+#pragma unroll
+            for (int c = 1; c < NCH; ++c) {
+                s0 += acc0[t][c];
+                s1 += acc1[t][c];
+            }
+            red[(warp * nblk + t) * 64 + gid * 8 + 2 * tig] = s0;
+            red[(warp * nblk + t) * 64 + gid * 8 + 2 * tig + 1] = s1;
+        }
+    }
+    __syncthreads();
+    double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
+    for (int e = threadIdx.x; e < a.P * a.Q; e += blockDim.x) {
+        const int i2 = e % a.P, j = e / a.P;
+        const int blk = (i2 / 8) + (j / 8) * MB;
+        const int off = (i2 % 8) * 8 + (j % 8);
+        double sum = 0.0;
+        for (int w = 0; w < kTsThreads / 32; ++w) sum += red[(w * nblk + blk) * 64 + off];
+        part[i2 + j * a.P] = sum;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Column-major blocks (rs == 1): no staging. A warp walks 8-row blocks; MMA
 // fragments are read straight from global memory (a fragment load touches 8
 // columns x 4 consecutive rows = 8 full 32-byte sectors). The transform's C
@@ -714,6 +984,87 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     auto cm = [](const View& v, int cols) { return cols == 0 || v.rs == 1; };
     const bool colmajor_all = cm(s.U0, a.u0) && cm(s.U1, a.u1) && cm(s.V, a.kv) &&
                               (s.transform == TS_NONE || (cm(s.W, s.W.cols) && (!s.W2.ptr || cm(s.W2, s.W2.cols))));
+    // bulk-copy kernel for aligned column-major operands (meshes' default)
+    static const bool no_bulk = [] {
+        const char* e = std::getenv("SPB_TS_BULK");
+        return e && e[0] == '0';
+    }();
+    auto aligned = [](const View& v, int cols) {
+        return cols == 0 || (reinterpret_cast<uintptr_t>(v.ptr) % 16 == 0 && (cols == 1 || v.cs % 2 == 0));
+    };
+    const int nblk_b = a.gram ? ((a.P + 7) / 8) * ((a.Q + 7) / 8) : 0;
+    const int nw1 = s.transform == TS_NONE ? 0 : s.W.cols, nw2 = s.transform == TS_NONE ? 0 : a.kw - nw1;
+    if (!no_bulk && colmajor_all && !ts_force_cuda_cores() && aligned(s.U0, a.u0) && aligned(s.U1, a.u1) &&
+        aligned(s.V, a.kv) && aligned(s.W, nw1) && aligned(s.W2, nw2) &&
+        (!s.b || reinterpret_cast<uintptr_t>(s.b) % 16 == 0) && nblk_b <= kBulkMaxBlk &&
+        a.u0 + a.u1 + a.kv + 1 <= 64 && a.kw <= 64) {
+        BulkCfg g{};
+        g.has_b = (a.gram && s.b) ? 1 : 0;
+        const int cu_b = need_u ? u : 0;
+        g.nload = cu_b + a.kv + g.has_b;
+        g.cV = cu_b;
+        g.zc = g.cV + a.kv;
+        g.cb = g.zc + 3;
+        g.ncol = g.cb + g.has_b;
+        size_t smb = 0;
+        bool found = false;
+        static const int tr_env = [] {
+            const char* e = std::getenv("SPB_TS_TR");
+            return e ? std::atoi(e) : 0;
+        }();
+        static const int kb_env = [] {
+            const char* e = std::getenv("SPB_TS_STAGE_KB");
+            return e ? std::atoi(e) : 48;
+        }();
+        const int KBp = (inner + 3) / 4 * 4, NWp = (a.kw + 7) / 8 * 8;
+        // tile rows: ~kb_env KB of loaded columns per stage, 64..2048 rows
+        int TR = 64;
+        while (TR < 2048 && static_cast<size_t>(g.nload) * (2 * TR) * 8 <= static_cast<size_t>(kb_env) * 1024) TR *= 2;
+        if (tr_env) TR = tr_env;
+        for (; TR >= 64 && !found; TR /= 2) {
+            for (int nst : {4, 3, 2}) {
+                const int SC = TR + 4;
+                const size_t stage = static_cast<size_t>(g.ncol) * SC;
+                size_t bytes = sizeof(double) * (8 + 64 + 64 + nst * stage + static_cast<size_t>(a.kw) * SC +
+                                                 static_cast<size_t>(KBp) * NWp);
+                const size_t red = sizeof(double) * (200 + 64 * static_cast<size_t>(kTsThreads / 32) * std::max(nblk_b, 1));
+                bytes = std::max(bytes, red);
+                if (bytes <= 112 * 1024) {
+                    g.TR = TR;
+                    g.SC = SC;
+                    g.nst = nst;
+                    smb = bytes;
+                    found = true;
+                    break;
+                }
+            }
+        }
+        if (found) {
+            const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(2, (227 * 1024) / smb)));
+            const int64_t nt2 = (s.n + g.TR - 1) / g.TR;
+            int gridb = grid_for(nt2, 1, per_sm);
+            if (a.gram) {
+                while (static_cast<size_t>(gridb) * PQ > scratch_elems && gridb > 1) gridb = (gridb + 1) / 2;
+            }
+            static void (*const kerns[kBulkMaxBlk + 1])(const TsDev, const BulkCfg) = {
+                ts_bulk_kernel<0>, ts_bulk_kernel<1>, ts_bulk_kernel<2>, ts_bulk_kernel<3>, ts_bulk_kernel<4>,
+                ts_bulk_kernel<5>, ts_bulk_kernel<6>, ts_bulk_kernel<7>, ts_bulk_kernel<8>, ts_bulk_kernel<9>};
+            static bool attr_set = false;  // once, at the maximum (no attribute changes between launches)
+            if (!attr_set) {
+                for (auto k : kerns)
+                    SPB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+                attr_set = true;
+            }
+            kerns[nblk_b]<<<gridb, kTsThreads, smb, st>>>(a, g);
+            SPB_LAUNCH_CHECK();
+            if (a.gram) {
+                reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 4), 128, 0, st>>>(scratch, gridb,
+                                                                                      static_cast<int>(PQ), gram_out);
+                SPB_LAUNCH_CHECK();
+            }
+            return a.P;
+        }
+    }
     static const bool direct = std::getenv("SPB_TS_DIRECT") != nullptr;  // experimental, off by default
     if (direct && colmajor_all && !ts_force_cuda_cores() && (s.transform == TS_NONE || (inner <= 32 && a.kw <= 32)) &&
         (!a.gram || (a.P <= 40 && a.Q <= 32))) {

@@ -466,7 +466,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
 
     // v0: seeded uniform(-1,1) (preconditioners.cpp:82-87), minus its mean, normalized
     // basis columns carry halo rows (they are SpMM inputs)
-    const int64_t vld = rows_cap_;
+    const int64_t vld = (rows_cap_ + 63) / 64 * 64;  // aligned columns (bulk-copy tall-skinny kernels)
     DBuf<double> Vbuf;
     double* Vb = sym_ ? ctx_->comm.sym_alloc(static_cast<size_t>(vld) * (k_req + 1), s_)
                       : (Vbuf.alloc(static_cast<size_t>(vld) * (k_req + 1)), Vbuf.p);
