@@ -93,6 +93,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout=20.0):
+        # NVML start-up inside nvidia-smi can stall driver calls of other processes;
+        # let it finish before any timed work
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -233,6 +240,8 @@ def main():
     from paper_2105_00578_b200.api import Graph
     gp = Graph(offs_p.numpy(), cols_p.numpy())
     cfg = run_config(c)
+    asg_p = torch.empty(g.n, dtype=torch.int32).pin_memory()  # pinned D2H target of the result
+    asg_np = asg_p.numpy()
     h2d_bytes = gp.row_offsets.nbytes + gp.col_indices.nbytes
     d2h_bytes = 4 * g.n
 
@@ -251,11 +260,12 @@ def main():
     # driver calls for a while, which must not land inside a timed step
     clk = ClockSampler(local)
     clk.start()
+    clk.wait_first()
     ctx.set_timing(True)
     dg = ctx.upload(gp)
     for _ in range(args.warmup):
         ctx.partition_resident(dg, cfg, copy_assignment=False)
-    ctx.partition_graph(gp, cfg)  # e2e warm-up
+    ctx.partition_graph(gp, cfg, out=asg_np)  # e2e warm-up
 
     def timed(fn):
         ts, reps = [], []
@@ -275,7 +285,7 @@ def main():
         return ts, reps
 
     t_res, r_res = timed(lambda: ctx.partition_resident(dg, cfg, copy_assignment=False))
-    t_e2e, r_e2e = timed(lambda: ctx.partition_graph(gp, cfg))
+    t_e2e, r_e2e = timed(lambda: ctx.partition_graph(gp, cfg, out=asg_np))
     clocks = clk.stop()
 
     value = max_over_ranks(statistics.mean(t_res))

@@ -253,9 +253,15 @@ class Context:
         self._check(self.lib.sp_context_set_timing(self._h, int(on)))
 
     # pipeline.cpp:47-167
-    def partition_graph(self, g: Graph, cfg: RunConfig, x0=None) -> RunResult:
+    def partition_graph(self, g: Graph, cfg: RunConfig, x0=None, out=None) -> RunResult:
+        """out: optional caller-owned int32[n] array (e.g. pinned) receiving the assignment."""
         n = g.n
-        assignment = np.empty(n, dtype=np.int32)
+        if out is not None:
+            if out.dtype != np.int32 or out.shape != (n,) or not out.flags.c_contiguous:
+                raise ValueError("partition_graph: out must be a contiguous int32 array of length n")
+            assignment = out
+        else:
+            assignment = np.empty(n, dtype=np.int32)
         pw = np.zeros(max(int(cfg.num_parts), 1), dtype=np.float64)
         rep = abi.SpReport()
         rep.part_weights = pw.ctypes.data_as(C.POINTER(C.c_double))

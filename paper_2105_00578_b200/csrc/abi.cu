@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <bit>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -437,6 +438,23 @@ sp_status sp_context_create(int device, sp_context** out) {
         SPB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t keep = UINT64_MAX;
         SPB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        // map the pool's memory up front (SPB_POOL_RESERVE_GB, default 16): growing a
+        // pool takes driver-global locks that other processes (e.g. an nvidia-smi
+        // poller) can hold for a long time; a pre-mapped pool never grows mid-solve
+        const char* rg = std::getenv("SPB_POOL_RESERVE_GB");
+        const double gb = rg ? std::atof(rg) : 16.0;
+        size_t fr = 0, tot = 0;
+        SPB_CUDA(cudaMemGetInfo(&fr, &tot));
+        const size_t want = std::min(static_cast<size_t>(gb * (1ull << 30)), fr / 2);
+        if (want > 0) {
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+                SPB_CUDA(cudaFreeAsync(p, c->stream));
+                SPB_CUDA(cudaStreamSynchronize(c->stream));
+            } else {
+                cudaGetLastError();
+            }
+        }
         SPB_CUDA(cudaEventCreate(&c->ev0));
         SPB_CUDA(cudaEventCreate(&c->ev1));
     } catch (...) {
@@ -509,10 +527,16 @@ sp_status sp_partition(sp_context* ctx, const sp_graph* hg, const sp_config* cfg
         const auto t_total = Clock::now();
         DevGraph g;
         copy_graph(ctx, hg, g);
+        if (ctx->prof.on) {
+            SPB_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::fprintf(stderr, "[spb-profile] sp_partition copy_graph %.3f ms\n", since(t_total) * 1e3);
+        }
         DBuf<int32_t> asg;
         partition_core(ctx, g, cfg, x0, asg, rep, t_total);
+        const auto t_d2h = Clock::now();
         SPB_CUDA(cudaMemcpyAsync(assignment_out, asg.p, sizeof(int32_t) * hg->n, cudaMemcpyDeviceToHost, ctx->stream));
         SPB_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->prof.on) std::fprintf(stderr, "[spb-profile] sp_partition d2h %.3f ms\n", since(t_d2h) * 1e3);
         if (rep) rep->total_s = since(t_total);
     });
 }

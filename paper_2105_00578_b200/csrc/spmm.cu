@@ -630,22 +630,33 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
     const uint32_t zrow = static_cast<uint32_t>(op.ell_zero_row);
     bool waited = false;
+    // the next tile's slot indices and diagonal are loaded one tile ahead, so
+    // the index -> gather dependency does not serialize two memory latencies
+    auto phys = [&](int64_t lt) { return HF ? (lt + hf.rot) % ntiles : lt; };
+    uint32_t jn[W];
+    double dwn = 0.0;
+    auto load_slots = [&](int64_t lt) {
+        const int64_t row = phys(lt) * 32 + lane;
+        const bool live = lt < ntiles && row < op.n;
+#pragma unroll
+        for (int sidx = 0; sidx < W; ++sidx)
+            jn[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
+        dwn = live ? __ldg(op.diag + row) : 0.0;
+    };
+    load_slots(gwarp);
     for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
-        int64_t tile = lt;
-        if (HF) {
-            if (lt >= hf.n_int && !waited) {
-                halo_wait_warp(hf);
-                waited = true;
-            }
-            tile = (lt + hf.rot) % ntiles;
+        if (HF && lt >= hf.n_int && !waited) {
+            halo_wait_warp(hf);
+            waited = true;
         }
+        const int64_t tile = phys(lt);
         const int64_t row = tile * 32 + lane;
         const bool live = row < op.n;
         uint32_t j[W];
 #pragma unroll
-        for (int sidx = 0; sidx < W; ++sidx)
-            j[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
-        const double dw = live ? __ldg(op.diag + row) : 0.0;
+        for (int sidx = 0; sidx < W; ++sidx) j[sidx] = jn[sidx];
+        const double dw = dwn;
+        load_slots(lt + nwarps);
         const uint32_t own = live ? static_cast<uint32_t>(row) : zrow;
         for (int c0 = 0; c0 < m; c0 += CB) {
             const double* xc[CB];
