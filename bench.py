@@ -301,7 +301,7 @@ def main():
     if poly_launches:
         kb = sum(r.report.device["poly_bytes"] for r in r_res)
         kms = sum(r.report.device["poly_ms"] for r in r_res)
-        kl, kname = poly_launches, "spmm_col_kernel (CSR SpMM fused with the GMRES-polynomial step)"
+        kl, kname = poly_launches, "SpMM fused with the GMRES-polynomial step (spmm_ell_kernel on meshes)"
     else:
         kb, kms, kl, kname = spmm_bytes, spmm_ms, spmm_launches, "spmm (CSR SpMM + fused epilogues)"
     achieved = kb / (kms / 1e3) / 1e9 if kms > 0 else 0.0
