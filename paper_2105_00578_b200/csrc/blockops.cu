@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kTsThreads) ts_mma_kernel(const TsDev a) {
 // DMMA.8x8x4 per 8-row strip; the Gram splits the tile's k-steps over the
 // warps; per-warp fragments are summed in a fixed order (deterministic).
 constexpr int kBulkMaxBlk = 9;
+constexpr int kBulkThreads = kTsThreads + 32;  // 8 consumer warps + 1 producer warp
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -475,8 +476,8 @@ struct BulkCfg {
 };
 
 template <int NBLK>  // Gram 8x8 blocks (MB*NB), compile-time so the k-step loop is straight-line
-__global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, const BulkCfg g) {
-    constexpr int NCH = NBLK <= 2 ? 4 : 2;  // independent accumulator chains per block
+__global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a, const BulkCfg g) {
+    constexpr int NCH = NBLK <= 2 ? 4 : (NBLK <= 4 ? 2 : 1);  // independent accumulator chains per block
     extern __shared__ __align__(128) double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
     const int u = a.u0 + a.u1;
     const int inner = a.transform == TS_UPDATE ? u : a.kv;
     const int KBp = (inner + 3) / 4 * 4, NWp = (a.kw + 7) / 8 * 8;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // full[nst] then empty[nst]
+    uint64_t* ebar = bar + g.nst;
     const double** src = reinterpret_cast<const double**>(smem + 8);
     int* scol = reinterpret_cast<int*>(smem + 8 + 64);
     double* st0 = smem + 8 + 64 + 64;
@@ -492,7 +494,10 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
     double* Wb = st0 + g.nst * stage_elems;              // kw columns
     double* Cs = Wb + static_cast<size_t>(a.kw) * SC;     // KBp x NWp column-major, zero padded
     if (threadIdx.x == 0) {
-        for (int s2 = 0; s2 < g.nst; ++s2) mbar_init(bar + s2, 1);
+        for (int s2 = 0; s2 < g.nst; ++s2) {
+            mbar_init(bar + s2, 1);
+            mbar_init(ebar + s2, kTsThreads / 32);  // one arrival per consumer warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         int c = 0;
         if ((a.transform == TS_UPDATE) || (a.gram && a.left_u)) {
@@ -526,9 +531,6 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
         if (brows > 0)
             for (int c = 0; c < g.nload; ++c) bulk_g2s(T + scol[c] * SC, src[c] + r0, brows * 8u, bar + s2);
     };
-    if (threadIdx.x == 0)
-        for (int s2 = 0; s2 < g.nst && s2 < nt; ++s2) issue(blockIdx.x + s2 * gridDim.x, s2);
-
     const bool right_w = a.transform != TS_NONE;
     const int uL = a.left_u ? u : 0;
     const int MB = a.gram ? (a.P + 7) / 8 : 0, NB = a.gram ? (a.Q + 7) / 8 : 0;
@@ -561,6 +563,23 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
     const int w1 = a.W.cols;
     const int spw = TR / 64;  // strips per warp per tile (warp w: strips w, w+8, ...)
 
+    if (warp == kTsThreads / 32) {
+        // producer warp: refill stage s once all consumer warps released it
+        if (lane == 0) {
+            int s2 = 0;
+            unsigned eph = 0;
+            for (int i = 0; i < nt; ++i) {
+                if (i >= g.nst) mbar_wait(ebar + s2, eph);
+                issue(blockIdx.x + i * gridDim.x, s2);
+                if (++s2 == g.nst) {
+                    s2 = 0;
+                    if (i >= g.nst) eph ^= 1u;
+                    else if (i + 1 == g.nst) eph = 0;
+                }
+            }
+        }
+    }
+    else {
     int tile = blockIdx.x, s2 = 0;
     unsigned ph = 0;
     for (int i = 0; i < nt; ++i, tile += gridDim.x) {
@@ -571,12 +590,12 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
         if (rows < TR) {
             // tail tile (the CTA's last): odd last row by hand, zero rows [rows, TR)
             if (rows & 1)
-                for (int c = threadIdx.x; c < g.nload; c += blockDim.x) T[scol[c] * SC + rows - 1] = src[c][r0 + rows - 1];
-            for (int e = threadIdx.x; e < g.nload * (TR - rows); e += blockDim.x) {
+                for (int c = threadIdx.x; c < g.nload; c += kTsThreads) T[scol[c] * SC + rows - 1] = src[c][r0 + rows - 1];
+            for (int e = threadIdx.x; e < g.nload * (TR - rows); e += kTsThreads) {
                 const int c = e / (TR - rows), r = rows + e - c * (TR - rows);
                 T[scol[c] * SC + r] = 0.0;
             }
-            __syncthreads();
+            asm volatile("bar.sync 1, %0;" ::"n"(kTsThreads) : "memory");  // consumers only
         }
         const double* lp[NB1];
         const double* rp[NB1];
@@ -645,20 +664,21 @@ __global__ void __launch_bounds__(kTsThreads, 2) ts_bulk_kernel(const TsDev a, c
             }
             if (right_w) __syncwarp();  // W rows of these strips are rewritten next tile
         }
-        __syncthreads();  // stage s2 free
-        if (threadIdx.x == 0 && i + g.nst < nt) issue(tile + g.nst * gridDim.x, s2);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ebar + s2)) : "memory");
         if (++s2 == g.nst) {
             s2 = 0;
             ph ^= 1u;
         }
     }
 
+    }
     if (!a.gram) return;
     double* red = st0;
-    __syncthreads();
+    __syncthreads();  // all stages consumed (every full barrier waited)
 #pragma unroll
     for (int t = 0; t < NB1; ++t) {
-        if (t < nblk) {
+        if (warp < kTsThreads / 32 && t < nblk) {
             double s0 = acc0[t][0], s1 = acc1[t][0];
 #pragma unroll
             for (int c = 1; c < NCH; ++c) {
@@ -1055,7 +1075,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
                     SPB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
                 attr_set = true;
             }
-            kerns[nblk_b]<<<gridb, kTsThreads, smb, st>>>(a, g);
+            kerns[nblk_b]<<<gridb, kBulkThreads, smb, st>>>(a, g);
             SPB_LAUNCH_CHECK();
             if (a.gram) {
                 reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 4), 128, 0, st>>>(scratch, gridb,
