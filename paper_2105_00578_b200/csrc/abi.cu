@@ -34,6 +34,10 @@ int device_sm_count() {
 
 namespace {
 
+// rows with at least this many entries get a CTA each (spmm_long_kernel) in the
+// solver; shorter rows stay in the order-exact group kernel
+constexpr int64_t kLongRow = 512;
+
 using Clock = std::chrono::steady_clock;
 double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
 
@@ -312,7 +316,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     DevLaplacian A;
     build_laplacian(operator_kind(R.problem), g, false, A, s);
     A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
-    if (!kind.regular) collect_long_rows(g, A, 4096, s);
+    if (!kind.regular) collect_long_rows(g, A, kLongRow, s);
     localize_operator(ctx->comm, g, A, s);  // multi-GPU: halo numbering + exchange plan
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {
@@ -438,14 +442,16 @@ sp_status sp_context_create(int device, sp_context** out) {
         SPB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t keep = UINT64_MAX;
         SPB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-        // map the pool's memory up front (SPB_POOL_RESERVE_GB, default 16): growing a
+        // map the pool's memory up front (SPB_POOL_RESERVE_GB, default 96, at most
+        // 60% of the free memory; the pool is per device and shared by every
+        // context of the process): growing a
         // pool takes driver-global locks that other processes (e.g. an nvidia-smi
         // poller) can hold for a long time; a pre-mapped pool never grows mid-solve
         const char* rg = std::getenv("SPB_POOL_RESERVE_GB");
-        const double gb = rg ? std::atof(rg) : 16.0;
+        const double gb = rg ? std::atof(rg) : 96.0;
         size_t fr = 0, tot = 0;
         SPB_CUDA(cudaMemGetInfo(&fr, &tot));
-        const size_t want = std::min(static_cast<size_t>(gb * (1ull << 30)), fr / 2);
+        const size_t want = std::min(static_cast<size_t>(gb * (1ull << 30)), fr / 10 * 6);
         if (want > 0) {
             void* p = nullptr;
             if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {

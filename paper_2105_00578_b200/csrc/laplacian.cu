@@ -125,21 +125,31 @@ __global__ void bound_diag_kernel(int64_t n, int64_t row0, const int64_t* offs,
 // Gershgorin bound of the unit-cost L_N from the pattern (no materialization):
 // row i = 1 + sum_k |(-1*isd_i)*isd_j| in storage order; the diagonal term is
 // added first because gershgorin_bound keeps separate diag/off accumulators.
+// Warp per row: the 32 lanes compute 32 consecutive terms in parallel (coalesced
+// column loads, independent isd gathers), then every lane folds them into the
+// row sum in storage order via shuffles, so power-law hub rows cost one
+// shuffle+add per entry instead of one dependent memory latency.
 __global__ void normal_bound_kernel(int64_t n, int64_t row0, const int64_t* offs,
                                     const int32_t* cols, const double* isd,
                                     unsigned long long* bound_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     double best = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double isdi = isd[row0 + i];
+    for (int64_t i = warp0; i < n; i += nwarps) {
+        const double nisdi = -isd[row0 + i];
+        const int64_t k0 = offs[i], k1 = offs[i + 1];
         double off = 0.0;
-        for (int64_t k = offs[i]; k < offs[i + 1]; ++k)
-            off = __dadd_rn(off, fabs(__dmul_rn(-isdi, isd[cols[k]])));
+        for (int64_t kb = k0; kb < k1; kb += 32) {
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(32), k1 - kb));
+            const double term = lane < cnt ? fabs(__dmul_rn(nisdi, isd[cols[kb + lane]])) : 0.0;
+            for (int t = 0; t < cnt; ++t) off = __dadd_rn(off, __shfl_sync(0xffffffffu, term, t));
+        }
         best = fmax(best, __dadd_rn(1.0, off));
     }
     unsigned long long b = __double_as_longlong(best);
-    for (int off = 16; off > 0; off >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, off));
-    if ((threadIdx.x & 31) == 0) atomicMax(bound_bits, b);
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if (lane == 0) atomicMax(bound_bits, b);
 }
 
 __global__ void max_value_kernel(int64_t n, const double* v, unsigned long long* bits) {

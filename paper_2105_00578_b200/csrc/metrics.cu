@@ -70,12 +70,16 @@ __global__ void part_sum_kernel(int64_t n, const int32_t* sorted_parts, const in
 
 __global__ void cut_kernel(int64_t n, int64_t row0, const int64_t* offs, const int32_t* cols,
                            const double* vals, const int32_t* a_global, double* partial) {
+    // warp per row, lanes over the row's entries (balanced on power-law rows;
+    // unit costs make the sum an exact integer in any order)
     double s = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = warp0; i < n; i += nwarps) {
         const int64_t gi = row0 + i;
         const int32_t pi = a_global[gi];
-        for (int64_t k = offs[i]; k < offs[i + 1]; ++k) {
+        for (int64_t k = offs[i] + lane; k < offs[i + 1]; k += 32) {
             const int32_t j = cols[k];
             if (j > gi && a_global[j] != pi) s += vals ? vals[k] : 1.0;
         }

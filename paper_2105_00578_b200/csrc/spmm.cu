@@ -49,12 +49,26 @@ struct RowAcc {
                 if (MODE == OP_EXPLICIT) vl = __ldg(op.vals + kb + gl);
                 if (MODE == OP_NORMAL_UNIT) vl = __dmul_rn(-isdi, __ldg(op.isd + jl));
             }
-#pragma unroll 4
-            for (int t = 0; t < cnt; ++t) {
-                const int j = __shfl_sync(gmask, jl, t, G);
+            // gathers issued U at a time ahead of the ordered accumulation
+            constexpr int U = G < 8 ? G : 8;
+#pragma unroll
+            for (int t0 = 0; t0 < G; t0 += U) {
+            if (t0 >= cnt) break;
+            int jt[U];
+            double xt[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                jt[u] = __shfl_sync(gmask, jl, t0 + u, G);
+                xt[u] = (act && t0 + u < cnt) ? X.at(jt[u], c) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u;
+                if (t >= cnt) break;
+                const int j = jt[u];
                 double v = 0.0;
                 if (MODE == OP_EXPLICIT || MODE == OP_NORMAL_UNIT) v = __shfl_sync(gmask, vl, t, G);
-                const double xj = act ? X.at(j, c) : 0.0;
+                const double xj = xt[u];
                 const bool at_diag = op.dpos ? (kb + t == kdiag) : (j > grow);
                 if (MODE == OP_LAPLACE_UNIT) {
                     if (!placed && at_diag) {
@@ -71,6 +85,7 @@ struct RowAcc {
                 } else {
                     acc = __dadd_rn(acc, __dmul_rn(v, xj));
                 }
+            }
             }
         }
         if (MODE == OP_LAPLACE_UNIT && !placed) acc = __dadd_rn(acc, __dmul_rn(dval, xi));
@@ -537,8 +552,10 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
     }
 }
 
-// One CTA per long row (power-law hubs). Thread t accumulates entries
-// k0+t, k0+t+256, ... for every column; fixed-order warp butterfly + smem tree.
+// One CTA per long row (power-law hubs). Warp w takes entries k0+w, k0+w+8, ...
+// (unrolled by 4 for memory-level parallelism); lane c accumulates column c0+c,
+// so every entry is one coalesced read of the X row. The 8 warp partials are
+// summed in a fixed order.
 template <int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, const View X,
                                                              const EpiArgs ea, const int m,
@@ -546,48 +563,56 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
     const int64_t row = op.long_rows[blockIdx.x];
     const int64_t grow = op.row0 + row;
     const int64_t k0 = op.offs[row], k1 = op.offs[row + 1];
-    __shared__ double red[kThreads / 32][32];
+    constexpr int NW = kThreads / 32;
+    __shared__ double red[NW][32];
     __shared__ double sqs[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double isdi = 0.0;
     if (MODE == OP_NORMAL_UNIT) isdi = op.isd[grow];
     for (int c0 = 0; c0 < m; c0 += 32) {
         const int mc = min(32, m - c0);
-        double acc[32];
+        const bool act = lane < mc;
+        const int c = c0 + (act ? lane : 0);
+        double acc = 0.0;
+        int64_t k = k0 + warp;
+        for (; k + 3 * NW < k1; k += 4 * NW) {
+            int j[4];
+            double v[4], x[4];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) {
+            for (int u = 0; u < 4; ++u) {
+                j[u] = op.cols[k + u * NW];
+                if (MODE == OP_EXPLICIT) v[u] = op.vals[k + u * NW];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (MODE == OP_NORMAL_UNIT) v[u] = __dmul_rn(-isdi, op.isd[j[u]]);
+                else if (MODE == OP_LAPLACE_UNIT) v[u] = -1.0;
+                x[u] = act ? X.at(j[u], c) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], x[u]));
+        }
+        for (; k < k1; k += NW) {
             const int j = op.cols[k];
             double v;
             if (MODE == OP_EXPLICIT) v = op.vals[k];
             else if (MODE == OP_NORMAL_UNIT) v = __dmul_rn(-isdi, op.isd[j]);
             else v = -1.0;
-            const double* xr = &X.at(j, c0);
-#pragma unroll
-            for (int c = 0; c < 32; ++c)
-                if (c < mc) acc[c] = __dadd_rn(acc[c], __dmul_rn(v, xr[c * X.cs]));
+            const double x = act ? X.at(j, c) : 0.0;
+            acc = __dadd_rn(acc, __dmul_rn(v, x));
         }
-        // fixed-order reductions
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-            double a = acc[c];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-            acc[c] = a;
-        }
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (lane == 0)
-            for (int c = 0; c < 32; ++c) red[warp][c] = acc[c];
+        red[warp][lane] = acc;
         __syncthreads();
         if (threadIdx.x < mc) {
-            const int c = threadIdx.x;
+            const int cc = threadIdx.x;
             double s = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) s += red[w][c];
-            const double xi = X.at(grow, c0 + c);
+            for (int w = 0; w < NW; ++w) s += red[w][cc];
+            const double xi = X.at(grow, c0 + cc);
             if (MODE == OP_LAPLACE_UNIT) s = __dadd_rn(s, __dmul_rn(op.diag[row], xi));
             if (MODE == OP_NORMAL_UNIT) s = __dadd_rn(s, xi);
             double sq = 0.0;
-            epilogue<EPI>(ea, row, c0 + c, s, xi, sq);
-            sqs[c] = sq;
+            epilogue<EPI>(ea, row, c0 + cc, s, xi, sq);
+            sqs[cc] = sq;
         }
         __syncthreads();
         if (EPI == EPI_RESIDUAL && threadIdx.x < mc)
@@ -597,16 +622,6 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
     }
 }
 
-// Laplacian of a mesh in fixed-slot ELL form (spmm_ell_kernel). Built once per
-// operator by the solver: row i keeps its columns < i right-aligned in slots
-// [0, KL), its columns > i left-aligned in [KL, KL+KU), padding slots point at
-// a zero row of the input block. The reference's row sum (laplacian.cpp:53-79:
-// off-diagonals in column order with the diagonal spliced before the first
-// column > i) is then the same straight-line chain for every row:
-//   acc = 0; acc -= x_s (s < KL); acc += deg_i * x_i; acc -= x_s (s >= KL)
-// Subtracting a padding zero leaves the accumulator unchanged (acc - 0 == acc,
-// also for -0), and (-1) * x_j == -x_j exactly, so the result is bit-identical
-// to the CSR kernels. No per-row slot construction, no offsets, 32-bit gathers.
 template <int KL, int KU, int EPI, int CB, int MINB, bool HF>
 __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea,
                                                                    const HaloFuse hf) {
@@ -632,6 +647,8 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     bool waited = false;
     // the next tile's slot indices and diagonal are loaded one tile ahead, so
     // the index -> gather dependency does not serialize two memory latencies
+    // (wide stencils skip the look-ahead: their W indices already fill the registers)
+    constexpr bool kAhead = W <= 8;
     auto phys = [&](int64_t lt) { return HF ? (lt + hf.rot) % ntiles : lt; };
     uint32_t jn[W];
     double dwn = 0.0;
@@ -643,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
             jn[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
         dwn = live ? __ldg(op.diag + row) : 0.0;
     };
-    load_slots(gwarp);
+    if (kAhead) load_slots(gwarp);
     for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
         if (HF && lt >= hf.n_int && !waited) {
             halo_wait_warp(hf);
@@ -652,11 +669,12 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
         const int64_t tile = phys(lt);
         const int64_t row = tile * 32 + lane;
         const bool live = row < op.n;
+        if (!kAhead) load_slots(lt);
         uint32_t j[W];
 #pragma unroll
         for (int sidx = 0; sidx < W; ++sidx) j[sidx] = jn[sidx];
         const double dw = dwn;
-        load_slots(lt + nwarps);
+        if (kAhead) load_slots(lt + nwarps);
         const uint32_t own = live ? static_cast<uint32_t>(row) : zrow;
         for (int c0 = 0; c0 < m; c0 += CB) {
             const double* xc[CB];
@@ -672,16 +690,38 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                     hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
                 acc[q] = 0.0;
             }
+            // gathers in chunks of CH slots, each chunk issued before its ordered adds
+            constexpr int CH = 8;
 #pragma unroll
-            for (int sidx = 0; sidx < KL; ++sidx)
+            for (int s0 = 0; s0 < KL; s0 += CH) {
+                double gv[CB][CH];
 #pragma unroll
-                for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], __ldg(xc[q] + j[sidx]));
+                for (int u = 0; u < CH; ++u)
+                    if (s0 + u < KL)
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) gv[q][u] = __ldg(xc[q] + j[s0 + u]);
+#pragma unroll
+                for (int u = 0; u < CH; ++u)
+                    if (s0 + u < KL)
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], gv[q][u]);
+            }
 #pragma unroll
             for (int q = 0; q < CB; ++q) acc[q] = __dadd_rn(acc[q], __dmul_rn(dw, xi[q]));
 #pragma unroll
-            for (int sidx = KL; sidx < W; ++sidx)
+            for (int s0 = KL; s0 < W; s0 += CH) {
+                double gv[CB][CH];
 #pragma unroll
-                for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], __ldg(xc[q] + j[sidx]));
+                for (int u = 0; u < CH; ++u)
+                    if (s0 + u < W)
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) gv[q][u] = __ldg(xc[q] + j[s0 + u]);
+#pragma unroll
+                for (int u = 0; u < CH; ++u)
+                    if (s0 + u < W)
+#pragma unroll
+                        for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], gv[q][u]);
+            }
 #pragma unroll
             for (int q = 0; q < CB; ++q) {
                 double sq = 0.0;
@@ -777,7 +817,12 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             case 202: SPB_ELL(2, 2); break;
             case 303: SPB_ELL(3, 3); break;
             case 404: SPB_ELL(4, 4); break;
-            case 1313: SPB_ELL(13, 13); break;
+            case 1313:
+                if (hf) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true>, 0);
+                else if (evariant == 1) go(spmm_ell_kernel<13, 13, EPI, 2, 2, false>, 0);
+                else if (evariant == 2) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false>, 0);
+                else go(spmm_ell_kernel<13, 13, EPI, 1, 4, false>, 0);
+                break;
             default:
                 if (op.ell_kl == 8 && op.ell_ku == 8) SPB_ELL(8, 8);
                 else SPB_ELL(16, 16);

@@ -10,6 +10,7 @@ c = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
 g = bench.make_graph(c["gen"])
 ctx = Context(0)
 dg = ctx.upload(g)
-for _ in range(2):
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+for _ in range(reps):
     r = ctx.partition_resident(dg, bench.run_config(c), copy_assignment=False)
 print("launches per partition", r.report.device["kernel_launches"], "total", r.report.times["total_s"])
