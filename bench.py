@@ -45,6 +45,13 @@ CONFIGS = {
     "cfg4": dict(desc="3D 27-point Brick mesh 256^3, K=256, generalized, GMRES polynomial",
                  gen=("stencil3d", 256, 256, 256, 27), K=256, problem="generalized", precond="polynomial",
                  ref_iters=12),
+    # diagnostics: the per-GPU row block of cfg2 at 4 and 8 GPUs, on one GPU
+    "cfg2q": dict(desc="3D 7-point mesh 128x128x32 (cfg2 / 4), K=64, combinatorial, GMRES polynomial",
+                  gen=("stencil3d", 128, 128, 32, 7), K=64, problem="combinatorial", precond="polynomial",
+                  ref_iters=18),
+    "cfg2e": dict(desc="3D 7-point mesh 128x128x16 (cfg2 / 8), K=64, combinatorial, GMRES polynomial",
+                  gen=("stencil3d", 128, 128, 16, 7), K=64, problem="combinatorial", precond="polynomial",
+                  ref_iters=18),
     "cfg5": dict(desc="R-MAT scale 24 ef16 (LCC), K=256, normalized, Jacobi", gen=("rmat", 24, 16, 1),
                  K=256, problem="normalized", precond="jacobi", ref_iters=20),
 }

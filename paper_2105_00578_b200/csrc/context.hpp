@@ -35,6 +35,7 @@ struct HaloPlan {
     // P2P push: per send entry, destination rank and row in that rank's block
     DBuf<int32_t> dst_peer, dst_row;
     uint32_t send_mask = 0, recv_mask = 0;
+    bool vec2 = false;     // send entries pair up for 16-byte pushes (slab halos)
     int64_t max_rows = 0;  // max over ranks of nloc_pad + nhalo (common block height)
     int64_t halo_base = 0; // first halo row: nloc rounded up to 32 rows (own and halo rows never share a cache line)
     int64_t rot_tiles = 0, n_int_tiles = 0;  // fused SpMM tile order (p2p.cuh HaloFuse)

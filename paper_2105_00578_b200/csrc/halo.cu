@@ -278,6 +278,18 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
             if (hp.recv_cnt[p] > 0) hp.recv_mask |= 1u << p;
         }
         hp.max_rows = maxrows;
+        // 16-byte pushes need every even entry paired with the next one
+        {
+            std::vector<int32_t> srow(std::max<int64_t>(off, 1));
+            if (off > 0)
+                SPB_CUDA(cudaMemcpyAsync(srow.data(), hp.send_idx.p, sizeof(int32_t) * off, cudaMemcpyDeviceToHost, s));
+            SPB_CUDA(cudaStreamSynchronize(s));
+            bool ok = off > 0 && off % 2 == 0;
+            for (int64_t t = 0; ok && t < off; t += 2)
+                ok = dpeer[t] == dpeer[t + 1] && srow[t] % 2 == 0 && drow[t] % 2 == 0 && srow[t + 1] == srow[t] + 1 &&
+                     drow[t + 1] == drow[t] + 1;
+            hp.vec2 = ok;
+        }
         hp.dst_peer.alloc(dpeer.size());
         hp.dst_row.alloc(drow.size());
         SPB_CUDA(cudaMemcpyAsync(hp.dst_peer.p, dpeer.data(), sizeof(int32_t) * dpeer.size(), cudaMemcpyHostToDevice, s));

@@ -28,6 +28,7 @@ struct HaloFuse {
     int64_t rot = 0;
     int64_t n_int = 0;
     int64_t total = 0;  // send entries
+    int vec2 = 0;       // entries pair up (consecutive even src/dst rows, same peer): 16-byte pushes
     const int32_t* src_row = nullptr;
     const int32_t* dst_peer = nullptr;
     const int32_t* dst_row = nullptr;
@@ -38,6 +39,9 @@ struct HaloFuse {
     uint32_t send_mask = 0, recv_mask = 0;
     const uint64_t* my_flags = nullptr;
     int* err = nullptr;
+    // SPB_HALO_PROBE diagnostics: [0] kernel start (min), [1] push fenced (max over
+    // CTAs), [2] sum of warp wait ns, [3] waits, [4] kernel end (max)
+    unsigned long long* probe = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -69,38 +73,55 @@ __device__ __forceinline__ void wait_flag(const uint64_t* f, uint64_t epoch, int
 // warp's reads and remote writes are contiguous for slab halos.
 template <class XAt>
 __device__ __forceinline__ void halo_push_part(const HaloFuse& hf, int m, XAt xat) {
-    const int64_t elems = hf.total * m;
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < elems;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(e / hf.total);
-        const int64_t t = e - static_cast<int64_t>(c) * hf.total;
-        const double v = *xat(hf.src_row[t], c);
-        char* dst = reinterpret_cast<char*>(xat(hf.dst_row[t], c)) + hf.xd.d[hf.dst_peer[t]];
-        *reinterpret_cast<double*>(dst) = v;
+    if (hf.vec2) {
+        // column-major pairs of rows: one 16-byte load and one 16-byte remote store
+        const int64_t pairs = hf.total / 2;
+        const int64_t elems = pairs * m;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < elems;
+             e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int c = static_cast<int>(e / pairs);
+            const int64_t t = 2 * (e - static_cast<int64_t>(c) * pairs);
+            const double2 v = *reinterpret_cast<const double2*>(xat(hf.src_row[t], c));
+            char* dst = reinterpret_cast<char*>(xat(hf.dst_row[t], c)) + hf.xd.d[hf.dst_peer[t]];
+            *reinterpret_cast<double2*>(dst) = v;
+        }
+    } else {
+        const int64_t elems = hf.total * m;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < elems;
+             e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int c = static_cast<int>(e / hf.total);
+            const int64_t t = e - static_cast<int64_t>(c) * hf.total;
+            const double v = *xat(hf.src_row[t], c);
+            char* dst = reinterpret_cast<char*>(xat(hf.dst_row[t], c)) + hf.xd.d[hf.dst_peer[t]];
+            *reinterpret_cast<double*>(dst) = v;
+        }
     }
-    // one system-scope fence per CTA: the barrier makes the CTA's stores
-    // observed by thread 0, whose fence is cumulative over them
+    // one system-scope fence per CTA, by thread 0 only: the barrier makes the
+    // CTA's stores observed by thread 0, whose fence is cumulative over them.
+    // The other warps go straight on to their interior rows; the last CTA's
+    // thread 0 raises the destination flags.
     __syncthreads();
-    __shared__ int last_cta;
     if (threadIdx.x == 0) {
         __threadfence_system();
-        last_cta = (atomicAdd(hf.counter, 1) == static_cast<int>(gridDim.x) - 1);
-    }
-    __syncthreads();
-    if (last_cta) {
-        const int p = threadIdx.x;
-        if (p < hf.world && ((hf.send_mask >> p) & 1u)) {
+        if (hf.probe) atomicMax(&hf.probe[1], global_ns());
+        if (atomicAdd(hf.counter, 1) == static_cast<int>(gridDim.x) - 1) {
             __threadfence_system();
-            st_release_sys(reinterpret_cast<uint64_t*>(hf.remote_flag.p[p]), hf.epoch);
+            for (int p = 0; p < hf.world; ++p)
+                if ((hf.send_mask >> p) & 1u) st_release_sys(reinterpret_cast<uint64_t*>(hf.remote_flag.p[p]), hf.epoch);
+            *hf.counter = 0;
         }
-        if (p == 0) *hf.counter = 0;
     }
 }
 // wait for every source peer's data (one lane per peer), then the warp proceeds
 __device__ __forceinline__ void halo_wait_warp(const HaloFuse& hf) {
     const int lane = threadIdx.x & 31;
+    const uint64_t t0 = hf.probe ? global_ns() : 0;
     if (lane < hf.world && ((hf.recv_mask >> lane) & 1u)) wait_flag(hf.my_flags + lane, hf.epoch, hf.err);
     __syncwarp();
+    if (hf.probe && lane == 0) {
+        atomicAdd(&hf.probe[2], global_ns() - t0);
+        atomicAdd(&hf.probe[3], 1ull);
+    }
 }
 #endif
 

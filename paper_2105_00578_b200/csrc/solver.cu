@@ -149,6 +149,16 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
         if (fused) {
             ctx_->timers.halo_launches += 1;
             ctx_->timers.halo_bytes += static_cast<double>(ctx_->comm.halo.total_send) * m * 8;
+            static const bool probe = [] {
+                const char* e = std::getenv("SPB_HALO_PROBE");
+                return e && e[0] == '1';
+            }();
+            if (probe) {
+                probe_.alloc(8);
+                const unsigned long long init[5] = {~0ull, 0ull, 0ull, 0ull, 0ull};
+                SPB_CUDA(cudaMemcpyAsync(probe_.p, init, sizeof(init), cudaMemcpyHostToDevice, s_));
+                hf.probe = probe_.p;
+            }
         }
     }
     if (halo_ && !fused) {
@@ -168,6 +178,19 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
     const int rows = spmm_launch(A_, Xg, m, ea, s_, fused ? &hf : nullptr);
+    if (fused && hf.probe) {
+        unsigned long long h[5];
+        SPB_CUDA(cudaMemcpyAsync(h, hf.probe, sizeof(h), cudaMemcpyDeviceToHost, s_));
+        SPB_CUDA(cudaStreamSynchronize(s_));
+        probe_n_ += 1;
+        probe_push_ += static_cast<double>(h[1] - h[0]);
+        probe_wait_ += h[3] ? static_cast<double>(h[2]) / static_cast<double>(h[3]) : 0.0;
+        probe_total_ += static_cast<double>(h[4] - h[0]);
+        if (probe_n_ % 400 == 0)
+            std::fprintf(stderr, "[spb-halo] rank %d: %lld fused SpMMs, push+fence %.2f us, mean warp wait %.2f us, kernel %.2f us\n",
+                         ctx_->comm.rank, probe_n_, probe_push_ / probe_n_ / 1e3, probe_wait_ / probe_n_ / 1e3,
+                         probe_total_ / probe_n_ / 1e3);
+    }
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;
     // algorithmic bytes of this launch: index stream,

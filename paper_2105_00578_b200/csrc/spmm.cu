@@ -631,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
+    if (HF && hf.probe && threadIdx.x == 0) atomicMin(&hf.probe[0], global_ns());
     if (HF)
         halo_push_part(hf, m, [&](int64_t r, int c) {
             return const_cast<double*>(ta.X) + static_cast<int64_t>(c) * ta.ldx + r;
@@ -649,7 +650,11 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     // the index -> gather dependency does not serialize two memory latencies
     // (wide stencils skip the look-ahead: their W indices already fill the registers)
     constexpr bool kAhead = W <= 8;
-    auto phys = [&](int64_t lt) { return HF ? (lt + hf.rot) % ntiles : lt; };
+    auto phys = [&](int64_t lt) {
+        if (!HF) return lt;
+        const int64_t p = lt + hf.rot;
+        return p >= ntiles ? p - ntiles : p;
+    };
     uint32_t jn[W];
     double dwn = 0.0;
     auto load_slots = [&](int64_t lt) {
@@ -750,6 +755,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
             }
         }
     }
+    if (HF && hf.probe && lane == 0) atomicMax(&hf.probe[4], global_ns());
     if (EPI == EPI_RESIDUAL) {
         __syncthreads();
         for (int c = threadIdx.x; c < m; c += kThreads) {
@@ -805,9 +811,22 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
                 const char* e = std::getenv("SPB_ELL_VARIANT");
                 return e ? std::atoi(e) : 0;
             }();
+            // few tiles per warp (small row blocks, e.g. a mesh split over many GPUs):
+            // all columns in one pass (one gather latency per tile instead of m/2)
+            static const int wide_env = [] {
+                const char* e = std::getenv("SPB_ELL_WIDE");
+                return e ? std::atoi(e) : -1;
+            }();
+            const int64_t warps_total = static_cast<int64_t>(device_sm_count()) * 32;
+            // (measured slower than the 2-column passes at every size on cfg2: off unless asked for)
+            const bool wide = m > 2 && wide_env == 1 && ntiles < 4 * warps_total;
 #define SPB_ELL(KL_, KU_)                                                                                   \
     do {                                                                                                    \
-        if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                          \
+        if (wide && m <= 4) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 4, 2, true>                               \
+                                  : spmm_ell_kernel<KL_, KU_, EPI, 4, 2, false>, 0);                         \
+        else if (wide) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 8, 1, true>                                   \
+                             : spmm_ell_kernel<KL_, KU_, EPI, 8, 1, false>, 0);                             \
+        else if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                     \
         else if (evariant == 1) go(spmm_ell_kernel<KL_, KU_, EPI, 1, 6, false>, 0);                         \
         else if (evariant == 2) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 5, false>, 0);                         \
         else if (evariant == 3) go(spmm_ell_kernel<KL_, KU_, EPI, 4, 3, false>, 0);                         \

@@ -183,6 +183,9 @@ static void fill_fuse(Comm& cm, const View& X, HaloFuse& hf) {
     hf.rot = hp.rot_tiles;
     hf.n_int = hp.n_int_tiles;
     hf.total = hp.total_send;
+    // pairs are 16-byte aligned only in column-major blocks with even leading dimension
+    hf.vec2 = (hp.vec2 && X.rs == 1 && (X.cols == 1 || X.cs % 2 == 0) &&
+               reinterpret_cast<uintptr_t>(X.ptr) % 16 == 0) ? 1 : 0;
     hf.src_row = hp.send_idx.p;
     hf.dst_peer = hp.dst_peer.p;
     hf.dst_row = hp.dst_row.p;

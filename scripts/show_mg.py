@@ -1,8 +1,10 @@
-import json, sys, glob
-for f in sorted(glob.glob("gpurun_out/mg_n*.json")):
+import json, glob
+for f in sorted(glob.glob("gpurun_out/sc_*.json")):
     try:
         d = json.loads(open(f).read().strip().splitlines()[-1])
     except Exception as e:
         print(f, "unparsable", e); continue
-    print(f, d["n_gpus"], d["value"], d["e2e"]["value"], d["result"]["cut"], d["result"]["iterations"],
-          d["roofline"]["ms_per_launch"], d.get("halo"), d["result"]["times"])
+    h = d.get("halo") or {}
+    print(f.split("/")[-1], d["n_gpus"], "value", d["value"], "e2e", d["e2e"]["value"], "it", d["result"]["iterations"],
+          "cut", d["result"]["cut"], "spmm_us", round(d["roofline"]["ms_per_launch"] * 1e3, 1),
+          "halo_us", h.get("us_per_exchange"), "steps", d["step_s"])
