@@ -15,6 +15,8 @@
 #pragma once
 
 #include "common.cuh"
+
+#include <climits>
 #include "p2p.cuh"
 
 namespace spb {
@@ -46,6 +48,13 @@ struct DevOp {
     int ell_kl = 0, ell_ku = 0;
     int64_t ell_ld = 0;
     int64_t ell_zero_row = 0;
+    // pattern-compressed form (structured meshes): row i's slots are
+    // i + ell_pat_tab[pid*W + s] (kEllPad = zero row), its diagonal ell_pat_deg[pid],
+    // pid = ell_pat[i]; at most 256 distinct row patterns
+    const uint8_t* ell_pat = nullptr;
+    const int32_t* ell_pat_tab = nullptr;
+    const double* ell_pat_deg = nullptr;
+    int ell_npat = 0;
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -81,6 +90,16 @@ bool spmm_col_path(const DevOp& op, const View& X, int m, const EpiArgs& ea);
 // Builds the fixed-slot ELL of a LAPLACE_UNIT operator (spmm.cu); returns false
 // (op unchanged) when the rows are too wide. Padding slots point at zero_row.
 bool build_ell(DevOp& op, int64_t zero_row, DBuf<int32_t>& store, cudaStream_t s);
+constexpr int32_t kEllPad = INT32_MIN;
+// Pattern-compresses the ELL of a unit-cost Laplacian (ellpat.cu): succeeds when the
+// rows have at most 256 distinct (column - row) slot vectors and every diagonal
+// equals its row's neighbour count; the ELL stays as built otherwise.
+struct EllPatStore {
+    DBuf<uint8_t> pid;
+    DBuf<int32_t> tab;
+    DBuf<double> deg;
+};
+bool build_ell_patterns(DevOp& op, EllPatStore& st, cudaStream_t s);
 // Reduce partial[rows x m] over rows in fixed order into out[m] (device).
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s);
 

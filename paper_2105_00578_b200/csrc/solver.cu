@@ -78,7 +78,14 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
         const char* e = std::getenv("SPB_NO_ELL");
         return e && e[0] == '1';
     }();
-    if (colmajor_ && !no_ell) build_ell(A_, n_, ell_, s_);
+    static const bool no_pat = [] {
+        const char* e = std::getenv("SPB_NO_ELL_PAT");
+        return e && e[0] == '1';
+    }();
+    if (colmajor_ && !no_ell && build_ell(A_, n_, ell_, s_) && !no_pat) {
+        const int kk = A_.ell_kl * 100 + A_.ell_ku;
+        if (kk == 202 || kk == 303 || kk == 1313) build_ell_patterns(A_, ellpat_, s_);
+    }
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));

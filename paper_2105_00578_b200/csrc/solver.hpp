@@ -104,6 +104,7 @@ private:
     std::vector<double> roots_;
 
     DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
+    EllPatStore ellpat_; // its pattern-compressed form (ellpat.cu)
     DBuf<unsigned long long> probe_;  // SPB_HALO_PROBE timestamps
     long long probe_n_ = 0;
     double probe_push_ = 0.0, probe_wait_ = 0.0, probe_total_ = 0.0;

@@ -622,12 +622,20 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
     }
 }
 
-template <int KL, int KU, int EPI, int CB, int MINB, bool HF>
+template <int KL, int KU, int EPI, int CB, int MINB, bool HF, bool PAT = false>
 __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea,
                                                                    const HaloFuse hf) {
     constexpr int W = KL + KU;
     __shared__ double s_sq[kThreads / 32][kMaxCols];
     __shared__ double s_theta[kMaxCols];
+    // pattern-compressed slots (ellpat.cu): table of per-pattern column offsets and degrees
+    __shared__ int32_t s_tab[PAT ? 256 * W : 1];
+    __shared__ double s_deg[PAT ? 256 : 1];
+    if (PAT) {
+        for (int e = threadIdx.x; e < op.ell_npat * W; e += kThreads) s_tab[e] = op.ell_pat_tab[e];
+        for (int e = threadIdx.x; e < op.ell_npat; e += kThreads) s_deg[e] = op.ell_pat_deg[e];
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
@@ -660,10 +668,21 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     auto load_slots = [&](int64_t lt) {
         const int64_t row = phys(lt) * 32 + lane;
         const bool live = lt < ntiles && row < op.n;
+        if (PAT) {
+            const int p = live ? static_cast<int>(__ldg(op.ell_pat + row)) : 0;
+            const int32_t* tp = s_tab + p * W;
 #pragma unroll
-        for (int sidx = 0; sidx < W; ++sidx)
-            jn[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
-        dwn = live ? __ldg(op.diag + row) : 0.0;
+            for (int sidx = 0; sidx < W; ++sidx) {
+                const int32_t d = tp[sidx];
+                jn[sidx] = (live && d != kEllPad) ? static_cast<uint32_t>(row + d) : zrow;
+            }
+            dwn = live ? s_deg[p] : 0.0;
+        } else {
+#pragma unroll
+            for (int sidx = 0; sidx < W; ++sidx)
+                jn[sidx] = live ? static_cast<uint32_t>(__ldg(op.ell + static_cast<int64_t>(sidx) * op.ell_ld + row)) : zrow;
+            dwn = live ? __ldg(op.diag + row) : 0.0;
+        }
     };
     if (kAhead) load_slots(gwarp);
     for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
@@ -766,6 +785,15 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     }
 }
 
+// PAT instantiations exist only for the pattern-compressed stencil classes
+template <int KL, int KU, int EPI>
+auto pat_ell_kernel(bool hf) -> decltype(&spmm_ell_kernel<KL, KU, EPI, 2, 4, false>) {
+    if constexpr (KL == KU && (KL == 2 || KL == 3))
+        return hf ? &spmm_ell_kernel<KL, KU, EPI, 2, 4, true, true> : &spmm_ell_kernel<KL, KU, EPI, 2, 4, false, true>;
+    else
+        return nullptr;
+}
+
 template <int MODE, int EPI>
 int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     int G = 1;
@@ -820,12 +848,15 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             const int64_t warps_total = static_cast<int64_t>(device_sm_count()) * 32;
             // (measured slower than the 2-column passes at every size on cfg2: off unless asked for)
             const bool wide = m > 2 && wide_env == 1 && ntiles < 4 * warps_total;
+            const bool pat = op.ell_pat != nullptr;
 #define SPB_ELL(KL_, KU_)                                                                                   \
     do {                                                                                                    \
         if (wide && m <= 4) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 4, 2, true>                               \
                                   : spmm_ell_kernel<KL_, KU_, EPI, 4, 2, false>, 0);                         \
         else if (wide) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 8, 1, true>                                   \
                              : spmm_ell_kernel<KL_, KU_, EPI, 8, 1, false>, 0);                             \
+        else if (pat && pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr) != nullptr)                            \
+            go(pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr), 0);                                           \
         else if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                     \
         else if (evariant == 1) go(spmm_ell_kernel<KL_, KU_, EPI, 1, 6, false>, 0);                         \
         else if (evariant == 2) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 5, false>, 0);                         \
@@ -837,7 +868,9 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             case 303: SPB_ELL(3, 3); break;
             case 404: SPB_ELL(4, 4); break;
             case 1313:
-                if (hf) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true>, 0);
+                if (pat) go(hf ? spmm_ell_kernel<13, 13, EPI, 1, 4, true, true>
+                               : spmm_ell_kernel<13, 13, EPI, 1, 4, false, true>, 0);
+                else if (hf) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true>, 0);
                 else if (evariant == 1) go(spmm_ell_kernel<13, 13, EPI, 2, 2, false>, 0);
                 else if (evariant == 2) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false>, 0);
                 else go(spmm_ell_kernel<13, 13, EPI, 1, 4, false>, 0);
