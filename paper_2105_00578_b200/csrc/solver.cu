@@ -55,6 +55,28 @@ __global__ void unit_vec_kernel(int64_t n, int64_t row0, View v) {
         v.at(i, 0) = (row0 + i == 0) ? 1.0 : 0.0;
 }
 
+// Arnoldi bookkeeping on the device (no host round trip per step):
+// Hess(i, j) = h1[i] + h2[i], Hess(j+1, j) = ||w||; the first step whose norm is
+// <= tiny is recorded (the reference stops there; later steps are discarded).
+__global__ void arnoldi_col_kernel(const double* h1, const double* h2, const double* ww, int j, double* hess,
+                                   int ldh, double tiny, int* breakdown, double* nrm_out) {
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hess[i + static_cast<int64_t>(j) * ldh] = h1[i] + h2[i];
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(fmax(0.0, ww[0]));
+        nrm_out[j] = nrm;
+        if (nrm <= tiny) atomicMin(breakdown, j);
+        else hess[j + 1 + static_cast<int64_t>(j) * ldh] = nrm;
+    }
+}
+
+__global__ void arnoldi_next_kernel(int64_t n, View in, View out, const double* nrm, int j, const int* breakdown) {
+    const bool dead = *breakdown <= j;
+    const double d = nrm[j];
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out.at(i, 0) = dead ? 0.0 : in.at(i, 0) / d;
+}
+
 } // namespace
 
 Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_cols)
@@ -535,6 +557,11 @@ void Solver::build_poly(uint64_t seed, int degree) {
     DBuf<double> wbuf(static_cast<size_t>(std::max<int64_t>(n_, 1)));
     const View w = colmajor(wbuf.p, std::max<int64_t>(n_, 1), 1);
     const View Vall = colmajor(Vb, vld, k_req + 1);
+    const int ldh = k_req + 1;
+    DBuf<double> hess_d(static_cast<size_t>(ldh) * k_req), nrm_d(k_req);
+    DBuf<int> bd(1);
+    SPB_CUDA(cudaMemsetAsync(hess_d.p, 0, sizeof(double) * ldh * k_req, s_));
+    SPB_CUDA(cudaMemcpyAsync(bd.p, &k_req, sizeof(int), cudaMemcpyHostToDevice, s_));
     for (int j = 0; j < k_req; ++j) {
         spmm_store(vcol(j), 1, w);
         const View basis = Vall.sub(0, j + 1);
@@ -546,8 +573,6 @@ void Solver::build_poly(uint64_t seed, int degree) {
         g1.gram_left_self = false;
         gram_dev(g1, P, Q);
         SPB_CUDA(cudaMemcpyAsync(cmat_.p, gram_.p, sizeof(double) * (j + 1), cudaMemcpyDeviceToDevice, s_));
-        std::vector<double> h1(j + 1), h2(j + 1);
-        SPB_CUDA(cudaMemcpyAsync(h1.data(), gram_.p, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s_));
         // w -= V h1 ; h2 = V^T w
         TsSpec u1;
         u1.U0 = basis;
@@ -559,7 +584,6 @@ void Solver::build_poly(uint64_t seed, int degree) {
         u1.gram_left_self = false;
         gram_dev(u1, P, Q);
         SPB_CUDA(cudaMemcpyAsync(cmat2_.p, gram_.p, sizeof(double) * (j + 1), cudaMemcpyDeviceToDevice, s_));
-        SPB_CUDA(cudaMemcpyAsync(h2.data(), gram_.p, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, s_));
         // w -= V h2 ; |w|^2
         TsSpec u2;
         u2.U0 = basis;
@@ -569,18 +593,23 @@ void Solver::build_poly(uint64_t seed, int degree) {
         u2.transform = TS_UPDATE;
         u2.gram_left_u = false;
         u2.gram_left_self = true;
-        std::vector<double> ww = gram_to_host(u2, P, Q);
-        for (int i = 0; i <= j; ++i) Hess(i, j) = h1[i] + h2[i];
-        const double nrm = std::sqrt(std::max(0.0, ww[0]));
-        k_got = j + 1;
-        if (nrm <= tiny) {
-            beta = 0.0;
-            break;
-        }
-        Hess(j + 1, j) = nrm;
-        beta = nrm;
-        div_scalar_kernel<<<grid_for(std::max<int64_t>(n_, 1), 256, 4), 256, 0, s_>>>(n_, w, vcol(j + 1), nrm);
+        gram_dev(u2, P, Q);
+        arnoldi_col_kernel<<<1, 64, 0, s_>>>(cmat_.p, cmat2_.p, gram_.p, j, hess_d.p, ldh, tiny, bd.p, nrm_d.p);
         SPB_LAUNCH_CHECK();
+        arnoldi_next_kernel<<<grid_for(std::max<int64_t>(n_, 1), 256, 4), 256, 0, s_>>>(n_, w, vcol(j + 1), nrm_d.p,
+                                                                                        j, bd.p);
+        SPB_LAUNCH_CHECK();
+    }
+    int first_bd = k_req;
+    SPB_CUDA(cudaMemcpyAsync(Hess.a.data(), hess_d.p, sizeof(double) * ldh * k_req, cudaMemcpyDeviceToHost, s_));
+    SPB_CUDA(cudaMemcpyAsync(&first_bd, bd.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
+    SPB_CUDA(cudaStreamSynchronize(s_));
+    if (first_bd < k_req) {
+        k_got = first_bd + 1;  // the reference stops at the breakdown step (beta = 0)
+        beta = 0.0;
+    } else {
+        k_got = k_req;
+        beta = Hess(k_req, k_req - 1);
     }
     Mat Hk(k_got, k_got);
     for (int i = 0; i < k_got; ++i)
