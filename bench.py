@@ -49,6 +49,9 @@ CONFIGS = {
     "cfg2q": dict(desc="3D 7-point mesh 128x128x32 (cfg2 / 4), K=64, combinatorial, GMRES polynomial",
                   gen=("stencil3d", 128, 128, 32, 7), K=64, problem="combinatorial", precond="polynomial",
                   ref_iters=18),
+    "cfg2h": dict(desc="3D 7-point mesh 128x128x64 (cfg2 / 2), K=64, combinatorial, GMRES polynomial",
+                  gen=("stencil3d", 128, 128, 64, 7), K=64, problem="combinatorial", precond="polynomial",
+                  ref_iters=18),
     "cfg2e": dict(desc="3D 7-point mesh 128x128x16 (cfg2 / 8), K=64, combinatorial, GMRES polynomial",
                   gen=("stencil3d", 128, 128, 16, 7), K=64, problem="combinatorial", precond="polynomial",
                   ref_iters=18),

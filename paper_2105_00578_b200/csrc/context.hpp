@@ -36,6 +36,14 @@ struct HaloPlan {
     DBuf<int32_t> dst_peer, dst_row;
     uint32_t send_mask = 0, recv_mask = 0;
     bool vec2 = false;     // send entries pair up for 16-byte pushes (slab halos)
+    // copy-engine halo (slab partitions): per destination, one contiguous run of
+    // own rows -> one contiguous run of the peer's halo rows
+    struct CeSeg {
+        int peer;
+        int64_t src_row, dst_row, rows;
+    };
+    std::vector<CeSeg> ce;
+    bool ce_ok = false;
     int64_t max_rows = 0;  // max over ranks of nloc_pad + nhalo (common block height)
     int64_t halo_base = 0; // first halo row: nloc rounded up to 32 rows (own and halo rows never share a cache line)
     int64_t rot_tiles = 0, n_int_tiles = 0;  // fused SpMM tile order (p2p.cuh HaloFuse)
@@ -58,6 +66,9 @@ struct SymHeap {
     std::vector<SymSeg> segs;
     size_t seg_i = 0, off = 0;  // bump position
     SymSeg ctrl;                // flags + sum slots
+    cudaStream_t side = nullptr;            // copy-engine halo stream
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+    void* write_value64 = nullptr;          // cuStreamWriteValue64 (driver entry point)
     uint64_t halo_epoch = 0, sum_epoch = 0, bar_epoch = 0;
     DBuf<int> counter;          // last-CTA ticket of the push kernel
     DBuf<int> err;              // device error word (peer wait timed out)
@@ -149,6 +160,13 @@ struct Timers {
 bool halo_push(Comm& cm, const View& X, int m, cudaStream_t s);
 // Fills hf for an SpMM with the exchange fused in; false = not applicable.
 bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s);
+// Copy-engine variant: the boundary rows go out as 2-D peer copies on a side
+// stream, each followed by a stream-ordered flag write; hf is set to wait only.
+// After launching the SpMM the caller must call halo_ce_finish (the main stream
+// may not overwrite X before the copies have read it).
+bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s);
+void halo_ce_finish(Comm& cm, cudaStream_t s);
+void halo_wait_flags(const HaloFuse& hf, cudaStream_t s);  // one warp waits for the peers' flags
 bool sum_p2p(Comm& cm, double* dev, int count, cudaStream_t s);
 void sym_release(Comm& cm);
 

@@ -289,6 +289,18 @@ void localize_operator(Comm& cm, const DevGraph& g, DevLaplacian& L, cudaStream_
                 ok = dpeer[t] == dpeer[t + 1] && srow[t] % 2 == 0 && drow[t] % 2 == 0 && srow[t + 1] == srow[t] + 1 &&
                      drow[t + 1] == drow[t] + 1;
             hp.vec2 = ok;
+            // copy-engine plan: every destination's entries form one contiguous source
+            // run and one contiguous destination run
+            hp.ce.clear();
+            bool ce = off > 0;
+            for (int p = 0; p < world && ce; ++p) {
+                const int64_t t0 = hp.send_off[p], c = hp.send_cnt[p];
+                if (c == 0) continue;
+                for (int64_t t = t0 + 1; t < t0 + c && ce; ++t)
+                    ce = srow[t] == srow[t0] + (t - t0) && drow[t] == drow[t0] + (t - t0);
+                hp.ce.push_back({p, srow[t0], drow[t0], c});
+            }
+            hp.ce_ok = ce;
         }
         hp.dst_peer.alloc(dpeer.size());
         hp.dst_row.alloc(drow.size());

@@ -15,20 +15,24 @@ struct PeerDelta {
     long long d[kMaxPeers];
 };
 
-// Arguments of an SpMM with its halo exchange fused in (spmm_col_kernel): the
+// Arguments of an SpMM with its halo exchange fused in (spmm_col/ell_kernel): the
 // CTAs first write the boundary rows every peer needs into the peers' copies of
 // X (byte delta xd[p] from the local address), raise one flag per destination
-// (last CTA), compute the interior row tiles, wait for the peers' flags and
-// finish with the tiles that read halo rows. Tiles are visited in rotated
-// order: logical tile t is physical tile (t + rot) mod ntiles, and logical
-// tiles < n_int read no halo row.
+// (last CTA), and process the row tiles in an order that starts with interior
+// tiles (no halo row read); a warp waits for the peers' flags before its first
+// halo tile. Physical tiles (rot + k) mod ntiles, k < n_int, are interior.
 struct HaloFuse {
     int on = 0;
     int world = 1;
     int64_t rot = 0;
     int64_t n_int = 0;
+    // logical order: interior tiles [0, bnd), halo tiles [bnd, bnd + ntiles - n_int),
+    // then the remaining interior tiles — the halo tiles run early enough for the
+    // peers' rows to have arrived, and the kernel's tail is interior work
+    int64_t bnd = 0;
     int64_t total = 0;  // send entries
     int vec2 = 0;       // entries pair up (consecutive even src/dst rows, same peer): 16-byte pushes
+    int nopush = 0;     // the rows were sent by the copy engine (symm.cu halo_ce_start): wait only
     const int32_t* src_row = nullptr;
     const int32_t* dst_peer = nullptr;
     const int32_t* dst_row = nullptr;
@@ -119,8 +123,11 @@ __device__ __forceinline__ void halo_wait_warp(const HaloFuse& hf) {
     if (lane < hf.world && ((hf.recv_mask >> lane) & 1u)) wait_flag(hf.my_flags + lane, hf.epoch, hf.err);
     __syncwarp();
     if (hf.probe && lane == 0) {
-        atomicAdd(&hf.probe[2], global_ns() - t0);
+        const uint64_t t1 = global_ns();
+        atomicAdd(&hf.probe[2], t1 - t0);
         atomicAdd(&hf.probe[3], 1ull);
+        atomicMin(&hf.probe[5], t0);  // first warp to reach a halo tile
+        atomicMax(&hf.probe[6], t1);  // last warp released
     }
 }
 #endif

@@ -171,10 +171,16 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     const bool timed = ctx_->time_spmm;
     std::pair<cudaEvent_t, cudaEvent_t> ev{};
     HaloFuse hf;
-    bool fused = false;
+    bool fused = false, ce = false;
     if (halo_) {
         // mesh operators: the exchange runs inside the SpMM (interior tiles overlap it)
-        fused = spmm_col_path(A_, Xlocal, m, ea) && halo_fuse_prepare(ctx_->comm, Xlocal, m, hf, s_);
+        if (spmm_col_path(A_, Xlocal, m, ea)) {
+            ce = halo_ce_start(ctx_->comm, Xlocal, m, hf, s_);  // copy engine + flag writes
+            // SM-issued pushes fused into the kernel: the CSR column kernel only (the
+            // ELL kernel carries no push code; without the copy engine its halo comes
+            // from the separate push kernel below)
+            fused = ce || (!A_.ell && halo_fuse_prepare(ctx_->comm, Xlocal, m, hf, s_));
+        }
         if (fused) {
             ctx_->timers.halo_launches += 1;
             ctx_->timers.halo_bytes += static_cast<double>(ctx_->comm.halo.total_send) * m * 8;
@@ -184,7 +190,7 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
             }();
             if (probe) {
                 probe_.alloc(8);
-                const unsigned long long init[5] = {~0ull, 0ull, 0ull, 0ull, 0ull};
+                const unsigned long long init[7] = {~0ull, 0ull, 0ull, 0ull, 0ull, ~0ull, 0ull};
                 SPB_CUDA(cudaMemcpyAsync(probe_.p, init, sizeof(init), cudaMemcpyHostToDevice, s_));
                 hf.probe = probe_.p;
             }
@@ -206,19 +212,47 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
         ev = ctx_->next_event_pair(ea.mode == EPI_POLY ? 1 : 0);
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
+    static const bool fake_hf = [] {
+        const char* e = std::getenv("SPB_FAKE_HF");
+        return e && e[0] == '1';
+    }();
+    if (fake_hf && !halo_ && spmm_col_path(A_, Xlocal, m, ea)) {
+        // diagnostic: the fused-exchange kernel variant on one GPU (no peers)
+        hf = HaloFuse{};
+        hf.on = 1;
+        hf.nopush = 1;
+        hf.n_int = (A_.n + 31) / 32;
+        hf.bnd = hf.n_int;
+        fused = true;
+    }
+    static const bool ce_split = [] {
+        const char* e = std::getenv("SPB_HALO_CE_SPLIT");
+        return e && e[0] == '1';
+    }();
+    if (ce && ce_split) {
+        // diagnostic: wait for the halo first, then the plain kernel
+        halo_wait_flags(hf, s_);
+        fused = false;
+    }
     const int rows = spmm_launch(A_, Xg, m, ea, s_, fused ? &hf : nullptr);
+    if (ce) halo_ce_finish(ctx_->comm, s_);
     if (fused && hf.probe) {
-        unsigned long long h[5];
+        unsigned long long h[7];
         SPB_CUDA(cudaMemcpyAsync(h, hf.probe, sizeof(h), cudaMemcpyDeviceToHost, s_));
         SPB_CUDA(cudaStreamSynchronize(s_));
         probe_n_ += 1;
+        if (h[5] != ~0ull) {
+            probe_first_ += static_cast<double>(h[5] - h[0]);
+            probe_last_ += static_cast<double>(h[6] - h[0]);
+        }
         probe_push_ += static_cast<double>(h[1] - h[0]);
         probe_wait_ += h[3] ? static_cast<double>(h[2]) / static_cast<double>(h[3]) : 0.0;
         probe_total_ += static_cast<double>(h[4] - h[0]);
         if (probe_n_ % 400 == 0)
-            std::fprintf(stderr, "[spb-halo] rank %d: %lld fused SpMMs, push+fence %.2f us, mean warp wait %.2f us, kernel %.2f us\n",
+            std::fprintf(stderr, "[spb-halo] rank %d: %lld fused SpMMs, push+fence %.2f us, mean warp wait %.2f us, "
+                                 "first halo tile at %.2f us, last wait released at %.2f us, kernel %.2f us\n",
                          ctx_->comm.rank, probe_n_, probe_push_ / probe_n_ / 1e3, probe_wait_ / probe_n_ / 1e3,
-                         probe_total_ / probe_n_ / 1e3);
+                         probe_first_ / probe_n_ / 1e3, probe_last_ / probe_n_ / 1e3, probe_total_ / probe_n_ / 1e3);
     }
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;

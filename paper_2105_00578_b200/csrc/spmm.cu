@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
     // multi-GPU: push this rank's boundary rows into the peers' X first (p2p.cuh)
-    if (HF)
+    if (HF && !hf.nopush)
         halo_push_part(hf, m, [&](int64_t r, int c) {
             return const_cast<double*>(ta.X) + static_cast<int64_t>(c) * ta.ldx + r;
         });
@@ -639,11 +639,9 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int m = ta.m;
+    // HF: the halo rows were sent by the copy engine (halo_ce_start); warps wait
+    // for the peers' flags before their first halo tile
     if (HF && hf.probe && threadIdx.x == 0) atomicMin(&hf.probe[0], global_ns());
-    if (HF)
-        halo_push_part(hf, m, [&](int64_t r, int c) {
-            return const_cast<double*>(ta.X) + static_cast<int64_t>(c) * ta.ldx + r;
-        });
     if (EPI == EPI_RESIDUAL) {
         for (int c = threadIdx.x; c < m; c += kThreads) s_theta[c] = ea.theta[c];
         for (int c = lane; c < m; c += 32) s_sq[warp][c] = 0.0;
@@ -653,14 +651,17 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + warp;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
     const uint32_t zrow = static_cast<uint32_t>(op.ell_zero_row);
-    bool waited = false;
     // the next tile's slot indices and diagonal are loaded one tile ahead, so
     // the index -> gather dependency does not serialize two memory latencies
     // (wide stencils skip the look-ahead: their W indices already fill the registers)
     constexpr bool kAhead = W <= 8;
+    // logical -> physical tile (see HaloFuse::bnd)
+    const int64_t nb = ntiles - hf.n_int;
+    // each loop segment maps logical lt to physical (lt + koff + rot) mod ntiles
+    int64_t koff = 0;
     auto phys = [&](int64_t lt) {
         if (!HF) return lt;
-        const int64_t p = lt + hf.rot;
+        const int64_t p = lt + koff + hf.rot;
         return p >= ntiles ? p - ntiles : p;
     };
     uint32_t jn[W];
@@ -685,11 +686,11 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
         }
     };
     if (kAhead) load_slots(gwarp);
-    for (int64_t lt = gwarp; lt < ntiles; lt += nwarps) {
-        if (HF && lt >= hf.n_int && !waited) {
-            halo_wait_warp(hf);
-            waited = true;
-        }
+    // two loops: logical tiles before the halo segment, then (after this warp's
+    // one wait, if it has halo tiles) the rest — no flag logic inside the loops
+    const int64_t lt_split = HF ? hf.bnd : ntiles;
+    auto tile_loop = [&](int64_t lt_begin, int64_t lt_end) {
+    for (int64_t lt = lt_begin; lt < lt_end; lt += nwarps) {
         const int64_t tile = phys(lt);
         const int64_t row = tile * 32 + lane;
         const bool live = row < op.n;
@@ -772,6 +773,32 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                     if (lane == 0 && on[q]) s_sq[warp][c0 + q] += sq;
                 }
             }
+        }
+    }
+    };
+    tile_loop(gwarp, lt_split);
+    if (HF) {
+        // first logical tile of this warp at or after lt0
+        auto first_from = [&](int64_t lt0) {
+            int64_t lt = gwarp;
+            if (lt < lt0) lt += ((lt0 - lt + nwarps - 1) / nwarps) * nwarps;
+            return lt;
+        };
+        // halo segment [bnd, bnd + nb): physical k = n_int + (lt - bnd)
+        int64_t lt = first_from(hf.bnd);
+        const int64_t hend = hf.bnd + nb;
+        if (lt < hend) {
+            halo_wait_warp(hf);
+            koff = hf.n_int - hf.bnd;
+            if (kAhead) load_slots(lt);
+            tile_loop(lt, hend);
+        }
+        // remaining interior [bnd + nb, ntiles): physical k = lt - nb
+        lt = first_from(hend);
+        if (lt < ntiles) {
+            koff = -nb;
+            if (kAhead) load_slots(lt);
+            tile_loop(lt, ntiles);
         }
     }
     if (HF && hf.probe && lane == 0) atomicMax(&hf.probe[4], global_ns());

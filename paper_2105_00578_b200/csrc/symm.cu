@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 namespace spb {
@@ -31,6 +32,10 @@ namespace {
 __global__ void halo_push_kernel(View X, int m, HaloFuse hf) {
     halo_push_part(hf, m, [&](int64_t r, int c) { return &X.at(r, c); });
     if (blockIdx.x == 0 && threadIdx.x < 32) halo_wait_warp(hf);
+}
+
+__global__ void halo_wait_kernel(HaloFuse hf) {
+    if (threadIdx.x < 32) halo_wait_warp(hf);
 }
 
 __global__ void sum_p2p_kernel(double* dev, int count, int world, int me, PeerAddr slot, const double* my_slots,
@@ -182,6 +187,13 @@ static void fill_fuse(Comm& cm, const View& X, HaloFuse& hf) {
     hf.world = cm.world;
     hf.rot = hp.rot_tiles;
     hf.n_int = hp.n_int_tiles;
+    // halo tiles after ~80% of the interior (the peers' rows arrive ~10-15 us after
+    // launch), interior work after them keeps the tail free of waits
+    static const int bnd_pct = [] {
+        const char* e = std::getenv("SPB_HALO_BND_PCT");
+        return e ? std::atoi(e) : 60;
+    }();
+    hf.bnd = hp.n_int_tiles * bnd_pct / 100;
     hf.total = hp.total_send;
     // pairs are 16-byte aligned only in column-major blocks with even leading dimension
     hf.vec2 = (hp.vec2 && X.rs == 1 && (X.cols == 1 || X.cs % 2 == 0) &&
@@ -212,6 +224,61 @@ bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_
     fill_fuse(cm, X, hf);
     cm.bytes_moved += cm.halo.total_send * m * 8;
     return true;
+}
+
+using WriteValue64Fn = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+
+bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s) {
+    static const bool off = [] {
+        const char* e = std::getenv("SPB_HALO_CE");
+        return e && e[0] == '0';
+    }();
+    if (off || !cm.sym.on || !cm.halo.on || !cm.halo.ce_ok || X.rs != 1) return false;
+    if (cm.sym_delta(X.ptr, cm.rank) == INT64_MIN) return false;
+    if (!cm.sym.side) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            cudaGetLastError();
+            return false;
+        }
+        cm.sym.write_value64 = fn;
+        SPB_CUDA(cudaStreamCreateWithFlags(&cm.sym.side, cudaStreamNonBlocking));
+        SPB_CUDA(cudaEventCreateWithFlags(&cm.sym.ev_ready, cudaEventDisableTiming));
+        SPB_CUDA(cudaEventCreateWithFlags(&cm.sym.ev_done, cudaEventDisableTiming));
+    }
+    if (cm.sym.last_halo_src == X.ptr) cm.barrier_p2p(s);
+    cm.sym.last_halo_src = X.ptr;
+    HaloPlan& hp = cm.halo;
+    fill_fuse(cm, X, hf);
+    hf.nopush = 1;
+    hf.total = 0;
+    SPB_CUDA(cudaEventRecord(cm.sym.ev_ready, s));
+    SPB_CUDA(cudaStreamWaitEvent(cm.sym.side, cm.sym.ev_ready, 0));
+    for (const auto& sg : hp.ce) {
+        // one column: any pitch >= the width (cudaMemcpy2D requires width <= pitch)
+        const size_t pitch = sizeof(double) * static_cast<size_t>(m > 1 ? X.cs : sg.rows);
+        const double* src = X.ptr + sg.src_row;
+        char* dst = reinterpret_cast<char*>(X.ptr + sg.dst_row) + hf.xd.d[sg.peer];
+        SPB_CUDA(cudaMemcpy2DAsync(dst, pitch, src, pitch, sizeof(double) * sg.rows, m, cudaMemcpyDeviceToDevice,
+                                   cm.sym.side));
+    }
+    auto wv = reinterpret_cast<WriteValue64Fn>(cm.sym.write_value64);
+    for (int p = 0; p < cm.world; ++p)
+        if ((hp.send_mask >> p) & 1u) {
+            const int r = wv(cm.sym.side, reinterpret_cast<unsigned long long>(hf.remote_flag.p[p]), hf.epoch, 0);
+            if (r != 0) throw SpError(8, "cuStreamWriteValue64 failed: " + std::to_string(r));
+        }
+    SPB_CUDA(cudaEventRecord(cm.sym.ev_done, cm.sym.side));
+    cm.bytes_moved += hp.total_send * m * 8;
+    return true;
+}
+
+void halo_ce_finish(Comm& cm, cudaStream_t s) { SPB_CUDA(cudaStreamWaitEvent(s, cm.sym.ev_done, 0)); }
+
+void halo_wait_flags(const HaloFuse& hf, cudaStream_t s) {
+    halo_wait_kernel<<<1, 32, 0, s>>>(hf);
+    SPB_LAUNCH_CHECK();
 }
 
 // P2P halo push (called by Comm::halo_exchange when X lives in the heap)
@@ -254,6 +321,12 @@ void sym_release(Comm& cm) {
         if (g.base) cudaFree(g.base);
         g = SymSeg{};
     };
+    if (cm.sym.side) cudaStreamSynchronize(cm.sym.side);
+    if (cm.sym.ev_ready) cudaEventDestroy(cm.sym.ev_ready);
+    if (cm.sym.ev_done) cudaEventDestroy(cm.sym.ev_done);
+    if (cm.sym.side) cudaStreamDestroy(cm.sym.side);
+    cm.sym.side = nullptr;
+    cm.sym.ev_ready = cm.sym.ev_done = nullptr;
     for (SymSeg& g : cm.sym.segs) drop(g);
     cm.sym.segs.clear();
     drop(cm.sym.ctrl);

@@ -18,10 +18,11 @@ def _ngpus():
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("p2p", ["1", "0"])  # NVLink peer-memory halo/sums, or the NCCL fallback
-def test_row_partitioned_matches_reference(p2p):
+# copy-engine halo + P2P sums (default), SM-issued halo pushes fused into the SpMM, NCCL fallback
+@pytest.mark.parametrize("path", ["ce", "fused", "nccl"])
+def test_row_partitioned_matches_reference(path):
     import os
-    env = dict(os.environ, SPB_P2P=p2p)
+    env = dict(os.environ, SPB_P2P="0" if path == "nccl" else "1", SPB_HALO_CE="0" if path == "fused" else "1")
     n = min(_ngpus(), 4)
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
