@@ -316,7 +316,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     DevLaplacian A;
     build_laplacian(operator_kind(R.problem), g, false, A, s);
     A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
-    if (!kind.regular) collect_long_rows(g, A, kLongRow, s);
+    if (!kind.regular) build_row_bins(A.op, kLongRow, A.bins, s);  // length bins + long-row list
     localize_operator(ctx->comm, g, A, s);  // multi-GPU: halo numbering + exchange plan
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {

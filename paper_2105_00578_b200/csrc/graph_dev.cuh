@@ -46,6 +46,7 @@ struct DevLaplacian {
     DBuf<int32_t> cols_L;
     DBuf<double> vals_L;
     DBuf<int32_t> long_rows;
+    RowBins bins;  // irregular graphs in the solver (spmm_vec.cu)
     DBuf<int32_t> cols_halo;  // multi-GPU: op columns in local halo numbering
     DBuf<double> isd_halo;    // multi-GPU normalized: isd of own + halo rows
     DBuf<int32_t> dpos;       // multi-GPU: per-row diagonal storage slot

@@ -42,6 +42,16 @@ struct DevOp {
     // dpos[i] is the storage slot of the diagonal (count of global cols < global i)
     const int32_t* dpos = nullptr;
     int64_t x_rows = 0;         // rows of the SpMM input block the columns address
+    // irregular graphs in the solver (spmm_vec.cu): rows grouped by length into
+    // bins 0..3 (<= 16, <= 64, <= 256, <= long threshold entries) and bin 4 (long rows)
+    const int32_t* bin_rows = nullptr;
+    int64_t bin_off[6] = {0, 0, 0, 0, 0, 0};
+    // long rows in chunks (one CTA each) and their per-chunk column partials
+    int64_t long_nchunks = 0;
+    const int64_t* long_row_chunk0 = nullptr;  // n_long + 1
+    const int32_t* long_chunk_row = nullptr;
+    const int64_t* long_chunk_k0 = nullptr;
+    double* long_part = nullptr;               // nchunks x 32
     // fixed-slot ELL of a mesh Laplacian (spmm_ell_kernel), built by the solver;
     // slot s of row i at ell[s*ell_ld + i]; padding slots hold ell_zero_row
     const int32_t* ell = nullptr;
@@ -100,6 +110,16 @@ struct EllPatStore {
     DBuf<double> deg;
 };
 bool build_ell_patterns(DevOp& op, EllPatStore& st, cudaStream_t s);
+// Row-length bins for the vector SpMM (spmm_vec.cu); also sets the long-row list.
+struct RowBins {
+    DBuf<int32_t> rows;
+    DBuf<int64_t> row_chunk0, chunk_k0;
+    DBuf<int32_t> chunk_row;
+    DBuf<double> part;
+};
+void build_row_bins(DevOp& op, int64_t long_thr, RowBins& st, cudaStream_t s);
+bool spmm_vec_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+int spmm_vec_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
 // Reduce partial[rows x m] over rows in fixed order into out[m] (device).
 void reduce_partials(const double* partial, int rows, int m, double* out, cudaStream_t s);
 

@@ -113,7 +113,7 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
     cmat_.alloc(static_cast<size_t>(m3) * m3 + 64);
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
-    partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 + A.n_long + 64) * 64);
+    partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 * 5 + A.n_long + 64) * 64);
     norms_.alloc(64);
     H_.alloc(block_elems(max_cols));
     P_.alloc(block_elems(max_cols));

@@ -15,6 +15,7 @@
 // bit-identical to the sequential sum).
 #include "ops.cuh"
 #include "p2p.cuh"
+#include "spmm_epilogue.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -93,35 +94,6 @@ struct RowAcc {
         return acc;
     }
 };
-
-// H accumulation of the product-form polynomial (preconditioners.cpp:184-185),
-// in the reference's order: h_terms == 2 adds inv_cur*p_i then inv_next*p_{i+1};
-// h_terms == 1 adds inv_next*p_{i+1} only; `first` starts from H = 0.
-__device__ __forceinline__ double poly_h(const EpiArgs& ea, double hold, double xi, double pn) {
-    double h = hold;
-    if (ea.h_terms == 2) h = ea.first ? __dmul_rn(ea.inv_cur, xi) : __dadd_rn(h, __dmul_rn(ea.inv_cur, xi));
-    return __dadd_rn(h, __dmul_rn(ea.inv_next, pn));
-}
-
-template <int EPI>
-__device__ __forceinline__ void epilogue(const EpiArgs& ea, int64_t row, int c, double acc,
-                                         double xi, double& sq) {
-    if (EPI == EPI_STORE) {
-        ea.Y.at(row, c) = acc;
-    } else if (EPI == EPI_RESIDUAL) {
-        // R = AX - BX * diag(theta)   (eigensolver.cpp:212-218): bx = d_i*x_i, r = ax - t*bx
-        const double bx = ea.bdiag ? __dmul_rn(ea.bdiag[row], xi) : xi;
-        const double r = __dsub_rn(acc, __dmul_rn(ea.theta[c], bx));
-        ea.Y.at(row, c) = r;
-        sq = fma(r, r, sq);
-    } else {
-        // prod_{i+1} = prod_i - inv_i * (A prod_i); H += inv_{i+1} * prod_{i+1}
-        // (preconditioners.cpp:183-190, unrolled one step ahead)
-        const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
-        ea.Y.at(row, c) = pn;
-        if (ea.h_terms) ea.H.at(row, c) = poly_h(ea, ea.first ? 0.0 : ea.H.at(row, c), xi, pn);
-    }
-}
 
 template <int G, int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads) spmm_group_kernel(const DevOp op, const View X,
@@ -979,6 +951,10 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
 #undef SPB_TILE_CASES
         SPB_LAUNCH_CHECK();
         return grid;
+    }
+    if (MODE != OP_DIAGONAL && spmm_vec_ok(op, X, m, ea)) {
+        // binned vector kernels + chunked long rows (solver path on irregular graphs)
+        return spmm_vec_launch(op, X, m, ea, s);
     }
     const int groups_per_block = kThreads / G;
     const int grid = grid_for(op.n, groups_per_block, 8);
