@@ -191,6 +191,42 @@ void sp_graph_free(sp_device_graph* dg);
 sp_status sp_partition_resident(sp_context* ctx, sp_device_graph* dg, const sp_config* cfg,
                                 int32_t* assignment_out, sp_report* report, const double* x0_colmajor);
 
+/* ---- ingestion (graph.cpp:44-182; what tools/specpart.cpp:89-104 runs before
+ *      partition_graph) ------------------------------------------------------- */
+
+/* GraphKind (graph.hpp:35-41) plus sizes. nnz counts stored entries (2 x edges). */
+typedef struct sp_graph_info {
+    int64_t n;
+    int64_t nnz;
+    int64_t n_symmetrized;    /* ingested graphs: before the component cut */
+    int64_t nnz_symmetrized;
+    int64_t max_degree;
+    double avg_degree;
+    double degree_ratio;
+    int32_t regular;          /* 1 = Regularity::Regular (ratio <= 10) */
+    int32_t pad;
+} sp_graph_info;
+
+/* symmetrize (graph.cpp:44-64: pattern of A + A^T, diagonal dropped, rows
+ * sorted, unit costs and weights) of the square n x n pattern (values are
+ * ignored, as in the reference) and, with lcc != 0, largest_connected_component
+ * (graph.cpp:118-171: ties go to the component holding the smallest vertex id;
+ * vertices keep their relative order). Runs on the device; the result stays in
+ * HBM as a device graph ready for sp_partition_resident. Replaces
+ *     Graph symmetrize(const SparseMatrix&)                          graph.hpp:53
+ *     std::pair<Graph, std::vector<int64_t>> largest_connected_component(const Graph&)  graph.hpp:62
+ * Errors: SP_INVALID for n == 0 or a column index outside [0, n). */
+sp_status sp_ingest(sp_context* ctx, int64_t n, const int64_t* row_offsets, const int32_t* col_indices,
+                    int32_t lcc, sp_device_graph** out);
+/* Sizes and classify (graph.hpp:65, graph.cpp:173-182) of a device graph. */
+sp_status sp_device_graph_info(sp_context* ctx, sp_device_graph* dg, sp_graph_info* info);
+/* Copies a device graph to host buffers (n+1 offsets, nnz columns; any may be
+ * NULL); old_ids_out (n int64, the LCC's old_ids) only for ingested graphs. */
+sp_status sp_device_graph_download(sp_context* ctx, sp_device_graph* dg, int64_t* offsets_out,
+                                   int32_t* cols_out, int64_t* old_ids_out);
+/* classify (graph.cpp:173-182) of a host graph. Errors: SP_INVALID for n == 0. */
+sp_status sp_classify(sp_context* ctx, const sp_graph* g, sp_graph_info* info);
+
 /* ---- kernel-level entry points (parity seams) ------------------------------ */
 
 /* Laplacian assembly (laplacian.cpp:53-144): writes the CSR of L (offsets n+1,

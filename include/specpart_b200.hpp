@@ -16,6 +16,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace specpart {
@@ -59,6 +60,16 @@ struct Graph {
     std::vector<double> vertex_weights;
     std::int64_t n() const { return adjacency.nrows; }
     std::int64_t edge_count() const { return adjacency.nnz() / 2; }
+};
+
+enum class Regularity { Regular, Irregular };
+
+// graph.hpp:35-41
+struct GraphKind {
+    Regularity kind = Regularity::Regular;
+    std::int64_t max_degree = 0;
+    double avg_degree = 0.0;
+    double ratio = 0.0;
 };
 
 enum class ProblemChoice { Auto, Combinatorial, Generalized, Normalized };
@@ -186,6 +197,61 @@ inline RunResult partition_graph(const Graph& g, const RunConfig& cfg) {
         R.warnings.emplace_back("imbalance " + std::to_string(r.imbalance) + " exceeds 1+epsilon = " +
                                 std::to_string(1.0 + cfg.epsilon));
     return out;
+}
+
+namespace b200 {
+inline Graph download(sp_context* c, sp_device_graph* dg, std::vector<std::int64_t>* old_ids) {
+    sp_graph_info info{};
+    rethrow(sp_device_graph_info(c, dg, &info), c);
+    Graph g;
+    g.adjacency.nrows = g.adjacency.ncols = info.n;
+    g.adjacency.row_offsets.resize(static_cast<size_t>(info.n + 1));
+    g.adjacency.col_indices.resize(static_cast<size_t>(info.nnz));
+    if (old_ids) old_ids->resize(static_cast<size_t>(info.n));
+    rethrow(sp_device_graph_download(c, dg, g.adjacency.row_offsets.data(), g.adjacency.col_indices.data(),
+                                     old_ids ? old_ids->data() : nullptr), c);
+    g.adjacency.values.assign(static_cast<size_t>(info.nnz), 1.0);  // unit edge costs, as graph.cpp:61
+    g.vertex_weights.assign(static_cast<size_t>(info.n), 1.0);
+    return g;
+}
+
+struct DeviceGraphHolder {
+    sp_device_graph* p = nullptr;
+    ~DeviceGraphHolder() { sp_graph_free(p); }
+};
+} // namespace b200
+
+// graph.hpp:53 (graph.cpp:44-64), on the device
+inline Graph symmetrize(const SparseMatrix& A) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("symmetrize: matrix not square");
+    sp_context* c = b200::context();
+    b200::DeviceGraphHolder h;
+    b200::rethrow(sp_ingest(c, A.nrows, A.row_offsets.data(), A.col_indices.data(), 0, &h.p), c);
+    return b200::download(c, h.p, nullptr);
+}
+
+// graph.hpp:62 (graph.cpp:118-171), on the device
+inline std::pair<Graph, std::vector<std::int64_t>> largest_connected_component(const Graph& g) {
+    sp_context* c = b200::context();
+    b200::DeviceGraphHolder h;
+    b200::rethrow(sp_ingest(c, g.n(), g.adjacency.row_offsets.data(), g.adjacency.col_indices.data(), 1, &h.p), c);
+    std::vector<std::int64_t> old;
+    Graph sub = b200::download(c, h.p, &old);
+    return {std::move(sub), std::move(old)};
+}
+
+// graph.hpp:65 (graph.cpp:173-182)
+inline GraphKind classify(const Graph& g) {
+    sp_context* c = b200::context();
+    sp_graph cg{g.n(), g.adjacency.row_offsets.data(), g.adjacency.col_indices.data(), nullptr, nullptr};
+    sp_graph_info info{};
+    b200::rethrow(sp_classify(c, &cg, &info), c);
+    GraphKind k;
+    k.kind = info.regular ? Regularity::Regular : Regularity::Irregular;
+    k.max_degree = info.max_degree;
+    k.avg_degree = info.avg_degree;
+    k.ratio = info.degree_ratio;
+    return k;
 }
 
 } // namespace specpart

@@ -105,6 +105,12 @@ class SpReport(C.Structure):
                 ("trace_capacity", C.c_int32), ("trace_len", C.c_int32)]
 
 
+class SpGraphInfo(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("n_symmetrized", C.c_int64),
+                ("nnz_symmetrized", C.c_int64), ("max_degree", C.c_int64), ("avg_degree", C.c_double),
+                ("degree_ratio", C.c_double), ("regular", C.c_int32), ("pad", C.c_int32)]
+
+
 P = C.c_void_p
 I32, I64, U64, F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
 
@@ -132,6 +138,10 @@ SIGNATURES = {
     "sp_poly_apply": (I32, [P, I32, C.POINTER(SpGraph), U64, I32, P, I32, P, P, C.POINTER(I32)]),
     "sp_mj_partition": (I32, [P, I64, I32, P, P, I64, P, P, C.POINTER(F64)]),
     "sp_cut_imbalance": (I32, [P, C.POINTER(SpGraph), P, I64, I32, C.POINTER(F64), C.POINTER(F64), P]),
+    "sp_ingest": (I32, [P, I64, P, P, I32, C.POINTER(P)]),
+    "sp_device_graph_info": (I32, [P, P, C.POINTER(SpGraphInfo)]),
+    "sp_device_graph_download": (I32, [P, P, P, P, P]),
+    "sp_classify": (I32, [P, C.POINTER(SpGraph), C.POINTER(SpGraphInfo)]),
 }
 
 LIB_PATH = Path(__file__).resolve().parent / "libspecpart_b200.so"

@@ -9,6 +9,7 @@ Names, argument meaning and error behaviour follow the reference:
     polynomial_build(...).apply                          preconditioners.hpp:45-46
     mj_partition                                         partitioner.hpp:39-42
     make_partition / cutsize / imbalance                 graph.hpp:63-75
+    symmetrize / largest_connected_component / classify  graph.hpp:53-65
 Every call runs the CUDA library (libspecpart_b200.so); a missing library raises
 ImportError — there is no CPU path.
 """
@@ -86,6 +87,28 @@ class RunConfig:
         c.doubled_cut = int(bool(self.doubled_cut))
         c.record_trace = int(bool(self.record_trace))
         return c
+
+
+@dataclass
+class GraphKind:
+    """GraphKind (graph.hpp:35-41) plus the sizes sp_graph_info carries."""
+    regular: bool
+    max_degree: int
+    avg_degree: float
+    ratio: float
+    n: int = 0
+    nnz: int = 0
+    n_symmetrized: int = 0
+    nnz_symmetrized: int = 0
+
+    @property
+    def kind(self) -> str:
+        return "regular" if self.regular else "irregular"
+
+
+def _kind_from_c(i: abi.SpGraphInfo) -> GraphKind:
+    return GraphKind(bool(i.regular), int(i.max_degree), float(i.avg_degree), float(i.degree_ratio),
+                     int(i.n), int(i.nnz), int(i.n_symmetrized), int(i.nnz_symmetrized))
 
 
 @dataclass
@@ -401,9 +424,64 @@ class Context:
         return Partition(a, num_parts, pw, cut.value, imb.value)
 
 
+    # graph.cpp:44-182 on the device (ingest.cu)
+    def ingest(self, row_offsets, col_indices, lcc: bool = True) -> "DeviceGraph":
+        """symmetrize(A) and, with lcc, largest_connected_component of it, left in HBM
+        (sp_ingest). A is the square pattern (row_offsets, col_indices); values are
+        ignored as in the reference (graph.cpp:44-64)."""
+        offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(col_indices, dtype=np.int32)
+        h = C.c_void_p()
+        self._check(self.lib.sp_ingest(self._h, offs.shape[0] - 1, offs.ctypes.data, cols.ctypes.data,
+                                       int(lcc), C.byref(h)))
+        dg = DeviceGraph(self, h, 0, ingested=True)
+        dg.n = dg.info().n
+        return dg
+
+    def symmetrize(self, row_offsets, col_indices) -> Graph:
+        """symmetrize (graph.hpp:53, graph.cpp:44-64), values=None = unit costs."""
+        dg = self.ingest(row_offsets, col_indices, lcc=False)
+        try:
+            return dg.download()[0]
+        finally:
+            dg.free()
+
+    def largest_connected_component(self, g: Graph):
+        """largest_connected_component (graph.hpp:62, graph.cpp:118-171) of a symmetric
+        unit-cost graph: (Graph, old_ids)."""
+        dg = self.ingest(g.row_offsets, g.col_indices, lcc=True)
+        try:
+            return dg.download()
+        finally:
+            dg.free()
+
+    def classify(self, g: Graph) -> GraphKind:
+        """classify (graph.hpp:65, graph.cpp:173-182)."""
+        i = abi.SpGraphInfo()
+        gc = g.as_c()
+        self._check(self.lib.sp_classify(self._h, C.byref(gc), C.byref(i)))
+        return _kind_from_c(i)
+
+
 class DeviceGraph:
-    def __init__(self, ctx: Context, handle: C.c_void_p, n: int):
-        self.ctx, self.handle, self.n = ctx, handle, n
+    def __init__(self, ctx: Context, handle: C.c_void_p, n: int, ingested: bool = False):
+        self.ctx, self.handle, self.n, self.ingested = ctx, handle, n, ingested
+
+    def info(self) -> GraphKind:
+        """Sizes and classify (graph.cpp:173-182) on the device (sp_device_graph_info)."""
+        i = abi.SpGraphInfo()
+        self.ctx._check(self.ctx.lib.sp_device_graph_info(self.ctx._h, self.handle, C.byref(i)))
+        return _kind_from_c(i)
+
+    def download(self):
+        """(Graph, old_ids) for an ingested graph, (Graph, None) otherwise."""
+        i = self.info()
+        offs = np.empty(i.n + 1, dtype=np.int64)
+        cols = np.empty(max(i.nnz, 1), dtype=np.int32)
+        old = np.empty(max(i.n, 1), dtype=np.int64) if self.ingested else None
+        self.ctx._check(self.ctx.lib.sp_device_graph_download(self.ctx._h, self.handle, offs.ctypes.data,
+                                                              cols.ctypes.data, _ptr(old)))
+        return Graph(offs, cols[: i.nnz]), (old[: i.n] if old is not None else None)
 
     def free(self):
         if self.handle:

@@ -3,6 +3,7 @@
 #include "specpart_b200.h"
 
 #include "context.hpp"
+#include "ingest.hpp"
 #include "metrics.hpp"
 #include "mj.hpp"
 #include "solver.hpp"
@@ -418,6 +419,67 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
         }
         *rep = R;
     }
+}
+
+// The row block of an ingested whole graph that this rank owns (copy_graph's
+// slicing, on device-resident arrays); one GPU takes the arrays over.
+void adopt_ingested(sp_context* ctx, IngestResult& r, sp_device_graph& h) {
+    Comm& cm = ctx->comm;
+    cudaStream_t s = ctx->stream;
+    DevGraph& g = h.g;
+    g.n_global = r.n;
+    g.nnz_global = r.nnz;
+    g.unit_values = true;
+    g.vals.release();
+    g.vw_all.release();
+    h.old_ids = std::move(r.old_ids);
+    h.n_sym = r.n_sym;
+    h.nnz_sym = r.nnz_sym;
+    h.ingested = true;
+    cm.setup(r.n);
+    if (!cm.active()) {
+        g.row0 = 0;
+        g.n_local = r.n;
+        g.nnz_local = r.nnz;
+        g.offs = std::move(r.offs);
+        g.cols = std::move(r.cols);
+    } else {
+        g.row0 = cm.row0();
+        g.n_local = cm.nloc();
+        int64_t k[2] = {0, 0};
+        SPB_CUDA(cudaMemcpyAsync(&k[0], r.offs.p + g.row0, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaMemcpyAsync(&k[1], r.offs.p + g.row0 + g.n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        g.nnz_local = k[1] - k[0];
+        g.offs.alloc(g.n_local + 1);
+        g.cols.alloc(std::max<int64_t>(g.nnz_local, 1));
+        SPB_CUDA(cudaMemcpyAsync(g.offs.p, r.offs.p + g.row0, sizeof(int64_t) * (g.n_local + 1),
+                                 cudaMemcpyDeviceToDevice, s));
+        if (k[0] != 0) {
+            rebase_kernel<<<grid_for(g.n_local + 1, 256, 4), 256, 0, s>>>(g.n_local + 1, g.offs.p, k[0]);
+            SPB_LAUNCH_CHECK();
+        }
+        if (g.nnz_local)
+            SPB_CUDA(cudaMemcpyAsync(g.cols.p, r.cols.p + k[0], sizeof(int32_t) * g.nnz_local,
+                                     cudaMemcpyDeviceToDevice, s));
+        h.full_offs = std::move(r.offs);
+        h.full_cols = std::move(r.cols);
+    }
+    g.prepared = false;
+}
+
+void fill_info(sp_context* ctx, DevGraph& g, sp_graph_info* info) {
+    prepare_graph(ctx, g);
+    const GraphKindInfo k = classify(g);
+    info->n = g.n_global;
+    info->nnz = g.nnz_global;
+    info->n_symmetrized = g.n_global;
+    info->nnz_symmetrized = g.nnz_global;
+    info->max_degree = k.max_degree;
+    info->avg_degree = k.avg;
+    info->degree_ratio = k.ratio;
+    info->regular = k.regular ? 1 : 0;
+    info->pad = 0;
 }
 
 } // namespace
@@ -873,6 +935,76 @@ sp_status sp_cut_imbalance(sp_context* ctx, const sp_graph* hg, const int32_t* a
         if (cut_out) *cut_out = pm.cut;
         if (imbalance_out) *imbalance_out = pm.imbalance;
         if (part_weights_out) std::memcpy(part_weights_out, pm.part_weights.data(), sizeof(double) * K);
+    });
+}
+
+sp_status sp_ingest(sp_context* ctx, int64_t n, const int64_t* row_offsets, const int32_t* col_indices,
+                    int32_t lcc, sp_device_graph** out) {
+    return guarded(ctx, [&] {
+        if (!out) throw_invalid("sp_ingest: null out");
+        *out = nullptr;
+        if (n < 0 || (n > 0 && (!row_offsets || !col_indices))) throw_invalid("sp_ingest: null arrays");
+        cudaStream_t s = ctx->stream;
+        const int64_t nnz = n > 0 ? row_offsets[n] : 0;
+        if (n > 0 && row_offsets[0] != 0) throw_invalid("sp_ingest: row_offsets[0] != 0");
+        DBuf<int64_t> offs(std::max<int64_t>(n + 1, 1));
+        DBuf<int32_t> cols(std::max<int64_t>(nnz, 1));
+        h2d(offs.p, row_offsets, n + 1, s);
+        h2d(cols.p, col_indices, nnz, s);
+        IngestResult r;
+        ingest_graph(n, offs.p, cols.p, nnz, lcc != 0, r, s);
+        offs.release();
+        cols.release();
+        auto h = std::make_unique<sp_device_graph>();
+        h->ctx = ctx;
+        adopt_ingested(ctx, r, *h);
+        SPB_CUDA(cudaStreamSynchronize(s));
+        *out = h.release();
+    });
+}
+
+sp_status sp_device_graph_info(sp_context* ctx, sp_device_graph* h, sp_graph_info* info) {
+    return guarded(ctx, [&] {
+        if (!h || !info) throw_invalid("sp_device_graph_info: null argument");
+        fill_info(ctx, h->g, info);
+        if (h->ingested) {
+            info->n_symmetrized = h->n_sym;
+            info->nnz_symmetrized = h->nnz_sym;
+        }
+    });
+}
+
+sp_status sp_device_graph_download(sp_context* ctx, sp_device_graph* h, int64_t* offsets_out, int32_t* cols_out,
+                                   int64_t* old_ids_out) {
+    return guarded(ctx, [&] {
+        if (!h) throw_invalid("sp_device_graph_download: null graph");
+        cudaStream_t s = ctx->stream;
+        const DevGraph& g = h->g;
+        const bool whole = !ctx->comm.active();
+        if (!whole && !h->ingested) throw_invalid("sp_device_graph_download: row-block graph");
+        const int64_t* offs = whole ? g.offs.p : h->full_offs.p;
+        const int32_t* cols = whole ? g.cols.p : h->full_cols.p;
+        if (whole && g.row0 != 0) throw_invalid("sp_device_graph_download: row-block graph");
+        if (offsets_out)
+            SPB_CUDA(cudaMemcpyAsync(offsets_out, offs, sizeof(int64_t) * (g.n_global + 1), cudaMemcpyDeviceToHost, s));
+        if (cols_out && g.nnz_global)
+            SPB_CUDA(cudaMemcpyAsync(cols_out, cols, sizeof(int32_t) * g.nnz_global, cudaMemcpyDeviceToHost, s));
+        if (old_ids_out) {
+            if (!h->ingested) throw_invalid("sp_device_graph_download: old ids exist for ingested graphs only");
+            SPB_CUDA(cudaMemcpyAsync(old_ids_out, h->old_ids.p, sizeof(int64_t) * g.n_global,
+                                     cudaMemcpyDeviceToHost, s));
+        }
+        SPB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+sp_status sp_classify(sp_context* ctx, const sp_graph* hg, sp_graph_info* info) {
+    return guarded(ctx, [&] {
+        if (!info) throw_invalid("sp_classify: null info");
+        if (!hg || hg->n == 0) throw_invalid("classify: empty graph");
+        DevGraph g;
+        copy_graph(ctx, hg, g);
+        fill_info(ctx, g, info);
     });
 }
 

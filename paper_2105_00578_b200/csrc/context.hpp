@@ -228,4 +228,11 @@ struct sp_device_graph {
     sp_context* ctx = nullptr;
     spb::DevGraph g;
     spb::DBuf<int32_t> assignment;  // last partition result (device)
+    // sp_ingest only: original vertex id of every vertex (n_global); multi-GPU
+    // also keeps the whole CSR (the DevGraph holds this rank's row block)
+    spb::DBuf<int64_t> old_ids;
+    spb::DBuf<int64_t> full_offs;
+    spb::DBuf<int32_t> full_cols;
+    int64_t n_sym = 0, nnz_sym = 0;
+    bool ingested = false;
 };

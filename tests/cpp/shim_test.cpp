@@ -44,6 +44,17 @@ int main() {
         ++fails;
     } catch (const InfeasibleError&) {
     }
+    // CLI ingestion (tools/specpart.cpp:89-90): a directed 3-cycle with a self-loop and a
+    // directed path 3 -> 5 -> 4; two components of 3 vertices, the tie goes to {0, 1, 2}
+    SparseMatrix raw;
+    raw.nrows = raw.ncols = 6;
+    raw.row_offsets = {0, 2, 3, 4, 5, 5, 6};
+    raw.col_indices = {1, 0, 2, 0, 5, 4};
+    Graph whole = symmetrize(raw);
+    auto [lcc, old] = largest_connected_component(whole);
+    if (whole.adjacency.nnz() != 10 || lcc.n() != 3 || lcc.adjacency.nnz() != 6 || old != std::vector<std::int64_t>{0, 1, 2})
+        ++fails;
+    if (classify(lcc).kind != Regularity::Regular || classify(lcc).max_degree != 2) ++fails;
     std::printf("shim_test: cut %.0f, %d boundaries, %d failures\n", r.report.cutsize, boundaries, fails);
     return fails ? 1 : 0;
 }

@@ -36,6 +36,7 @@ def test_struct_layouts_match_header():
 int main(void) {
   printf("%zu %zu %zu %zu\\n", sizeof(sp_graph), sizeof(sp_config), sizeof(sp_report), sizeof(sp_trace_record));
   printf("%zu %zu %zu\\n", offsetof(sp_report, cutsize), offsetof(sp_report, part_weights), offsetof(sp_report, poly_ms));
+  printf("%zu %zu\\n", sizeof(sp_graph_info), offsetof(sp_graph_info, regular));
   return 0;
 }
 """
@@ -53,6 +54,8 @@ int main(void) {
     assert sizes[4] == abi.SpReport.cutsize.offset
     assert sizes[5] == abi.SpReport.part_weights.offset
     assert sizes[6] == abi.SpReport.poly_ms.offset
+    assert sizes[7] == ctypes.sizeof(abi.SpGraphInfo)
+    assert sizes[8] == abi.SpGraphInfo.regular.offset
 
 
 def test_enums_follow_reference_order():
