@@ -13,6 +13,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace spb {
@@ -91,6 +92,78 @@ __global__ void __launch_bounds__(kVThreads) spmm_vec_kernel(const DevOp op, con
     }
 }
 
+// Rows of the two longest bins (65-512 entries), lanes over columns: one warp
+// per row, G = pow2(m) lanes per entry (lane = column), E = 32 / G entries per
+// warp instruction, U instructions in flight; the E slot sums combine by a fixed
+// butterfly (deterministic). Coalesced whole-row gathers: 1-2 L1 wavefronts per
+// entry instead of one per column (SPB_VEC_COLS=0 restores the per-lane form).
+template <int G, int MODE, int EPI>
+__global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op, const View X, const EpiArgs ea,
+                                                                 const int m, const int32_t* rows,
+                                                                 const int64_t nrows, const int partial_base) {
+    constexpr int E = 32 / G;
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / G, c = lane % G;
+    const bool act = c < m;
+    const int64_t w0 = (blockIdx.x * static_cast<int64_t>(kVThreads) + threadIdx.x) >> 5;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * (kVThreads / 32);
+    double sq = 0.0;
+    for (int64_t r = w0; r < nrows; r += nw) {
+        const int64_t row = rows[r];
+        const int64_t grow = op.row0 + row;
+        const int64_t k0 = op.offs[row], k1 = op.offs[row + 1];
+        double nisdi = 0.0;
+        if (MODE == OP_NORMAL_UNIT) nisdi = -op.isd[grow];
+        double acc = 0.0;
+        int64_t k = k0 + sub;
+        for (; k + (U - 1) * E < k1; k += U * E) {
+            int64_t j[U];
+            double w[U], x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) j[u] = op.cols[k + u * E];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (MODE == OP_EXPLICIT) w[u] = op.vals[k + u * E];
+                else if (MODE == OP_NORMAL_UNIT) w[u] = nisdi * op.isd[j[u]];
+                else w[u] = -1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + j[u] * X.rs + c) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = fma(w[u], x[u], acc);
+        }
+        for (; k < k1; k += E) {
+            const int64_t j = op.cols[k];
+            double w;
+            if (MODE == OP_EXPLICIT) w = op.vals[k];
+            else if (MODE == OP_NORMAL_UNIT) w = nisdi * op.isd[j];
+            else w = -1.0;
+            const double x = act ? __ldg(X.ptr + j * X.rs + c) : 0.0;
+            acc = fma(w, x, acc);
+        }
+#pragma unroll
+        for (int off = 16; off >= G; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (sub == 0 && act) {
+            const double xi = X.at(grow, c);
+            double v = acc;
+            if (MODE == OP_LAPLACE_UNIT) v = __dadd_rn(v, __dmul_rn(op.diag[row], xi));
+            if (MODE == OP_NORMAL_UNIT) v = __dadd_rn(v, xi);
+            epilogue<EPI>(ea, row, c, v, xi, sq);
+        }
+    }
+    if (EPI == EPI_RESIDUAL) {
+        __shared__ double s_sq[kVThreads / 32][32];
+        s_sq[warp][lane] = (sub == 0) ? sq : 0.0;
+        __syncthreads();
+        if (threadIdx.x < m) {
+            double t = 0.0;
+            for (int w = 0; w < kVThreads / 32; ++w) t += s_sq[w][threadIdx.x];
+            ea.partial[static_cast<int64_t>(partial_base + blockIdx.x) * m + threadIdx.x] = t;
+        }
+    }
+}
+
 // Long rows (bin 4) in chunks of kChunk entries, one CTA per chunk: every thread
 // strides over the chunk's entries gathering whole X rows; the CTA combines its
 // 256 partial rows (warp butterfly, then warps in order) into one partial per
@@ -136,6 +209,68 @@ __global__ void __launch_bounds__(kVThreads) long_chunk_kernel(const DevOp op, c
     if (threadIdx.x < m) {
         double v = 0.0;
         for (int w = 0; w < kVThreads / 32; ++w) v += red[w][threadIdx.x];
+        chunk_part[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x] = v;
+    }
+}
+
+// Long rows, lanes over columns: G = pow2(m) lanes per entry (lane = column),
+// E = 32 / G entries per warp instruction, U instructions in flight per warp.
+// One warp instruction gathers E whole X rows coalesced (an m*8-byte row is 1-2
+// L1 wavefronts), where the thread-per-entry form above spends one wavefront
+// per thread and column — that form is L1-request bound on the long rows.
+// Deterministic: entry k of the chunk goes to slot (k - kb) mod (NW*E), the slots
+// combine in slot order.
+template <int G, int MODE>
+__global__ void __launch_bounds__(kVThreads) long_chunk_cols_kernel(const DevOp op, const View X, const int m,
+                                                                    const int32_t* chunk_row,
+                                                                    const int64_t* chunk_k0, double* chunk_part) {
+    constexpr int E = 32 / G;
+    constexpr int NW = kVThreads / 32;
+    constexpr int STRIDE = NW * E;
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / G, c = lane % G;
+    const int slot = warp * E + sub;
+    const int64_t row = chunk_row[blockIdx.x];
+    const int64_t grow = op.row0 + row;
+    const int64_t kb = chunk_k0[blockIdx.x];
+    const int64_t ke = min(kb + kChunk, op.offs[row + 1]);
+    const bool act = c < m;
+    double nisdi = 0.0;
+    if (MODE == OP_NORMAL_UNIT) nisdi = -op.isd[grow];
+    double acc = 0.0;
+    int64_t k = kb + slot;
+    for (; k + (U - 1) * STRIDE < ke; k += U * STRIDE) {
+        int64_t j[U];
+        double w[U], x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = op.cols[k + u * STRIDE];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (MODE == OP_EXPLICIT) w[u] = op.vals[k + u * STRIDE];
+            else if (MODE == OP_NORMAL_UNIT) w[u] = nisdi * op.isd[j[u]];
+            else w[u] = -1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + j[u] * X.rs + c) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = fma(w[u], x[u], acc);
+    }
+    for (; k < ke; k += STRIDE) {
+        const int64_t j = op.cols[k];
+        double w;
+        if (MODE == OP_EXPLICIT) w = op.vals[k];
+        else if (MODE == OP_NORMAL_UNIT) w = nisdi * op.isd[j];
+        else w = -1.0;
+        const double x = act ? __ldg(X.ptr + j * X.rs + c) : 0.0;
+        acc = fma(w, x, acc);
+    }
+    __shared__ double red[STRIDE][G];
+    red[slot][c] = acc;
+    __syncthreads();
+    if (threadIdx.x < m) {
+        double v = 0.0;
+        for (int t = 0; t < STRIDE; ++t) v += red[t][threadIdx.x];
         chunk_part[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x] = v;
     }
 }
@@ -205,6 +340,18 @@ __global__ void bin_keys_kernel(int64_t n, const int64_t* offs, int64_t long_thr
 template <int S, int MODE, int EPI>
 int launch_bin(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const int32_t* rows,
                int64_t nrows, int partial_base) {
+    static const bool cols_form = [] {
+        const char* e = std::getenv("SPB_VEC_COLS");
+        return !(e && e[0] == '0');
+    }();
+    if (S >= 16 && cols_form) {
+        const int grid = grid_for(nrows, kVThreads / 32, 8);
+        if (m <= 8) spmm_rowcols_kernel<8, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        else if (m <= 16) spmm_rowcols_kernel<16, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        else spmm_rowcols_kernel<32, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        SPB_LAUNCH_CHECK();
+        return grid;
+    }
     const int grid = grid_for(nrows, kVThreads / S, 8);
     if (m <= 8) spmm_vec_kernel<S, 8, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
     else if (m <= 16) spmm_vec_kernel<S, 16, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
@@ -236,7 +383,15 @@ template <int MODE, int EPI>
 int launch_long(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, int partial_base) {
     if (op.n_long <= 0) return 0;
     const int nch = static_cast<int>(op.long_nchunks);
-    if (m <= 8) long_chunk_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+    static const bool cols_form = [] {
+        const char* e = std::getenv("SPB_LONG_COLS");
+        return !(e && e[0] == '0');
+    }();
+    if (cols_form) {
+        if (m <= 8) long_chunk_cols_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+        else if (m <= 16) long_chunk_cols_kernel<16, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+        else long_chunk_cols_kernel<32, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+    } else if (m <= 8) long_chunk_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
     else if (m <= 16) long_chunk_kernel<16, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
     else long_chunk_kernel<32, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
     SPB_LAUNCH_CHECK();
