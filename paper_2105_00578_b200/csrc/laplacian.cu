@@ -140,10 +140,23 @@ __global__ void normal_bound_kernel(int64_t n, int64_t row0, const int64_t* offs
         const double nisdi = -isd[row0 + i];
         const int64_t k0 = offs[i], k1 = offs[i + 1];
         double off = 0.0;
+        // the next 32 terms are loaded while the current ones are folded in; full
+        // groups issue their 32 shuffles back to back so only the adds form the chain
+        double term = (k0 + lane < k1) ? fabs(__dmul_rn(nisdi, isd[cols[k0 + lane]])) : 0.0;
         for (int64_t kb = k0; kb < k1; kb += 32) {
             const int cnt = static_cast<int>(min(static_cast<int64_t>(32), k1 - kb));
-            const double term = lane < cnt ? fabs(__dmul_rn(nisdi, isd[cols[kb + lane]])) : 0.0;
-            for (int t = 0; t < cnt; ++t) off = __dadd_rn(off, __shfl_sync(0xffffffffu, term, t));
+            const int64_t kn = kb + 32 + lane;
+            const double next = kn < k1 ? fabs(__dmul_rn(nisdi, isd[cols[kn]])) : 0.0;
+            if (cnt == 32) {
+                double t[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) t[q] = __shfl_sync(0xffffffffu, term, q);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) off = __dadd_rn(off, t[q]);
+            } else {
+                for (int q = 0; q < cnt; ++q) off = __dadd_rn(off, __shfl_sync(0xffffffffu, term, q));
+            }
+            term = next;
         }
         best = fmax(best, __dadd_rn(1.0, off));
     }

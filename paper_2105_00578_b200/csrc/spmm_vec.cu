@@ -92,29 +92,36 @@ __global__ void __launch_bounds__(kVThreads) spmm_vec_kernel(const DevOp op, con
     }
 }
 
-// Rows of the two longest bins (65-512 entries), lanes over columns: one warp
-// per row, G = pow2(m) lanes per entry (lane = column), E = 32 / G entries per
-// warp instruction, U instructions in flight; the E slot sums combine by a fixed
-// butterfly (deterministic). Coalesced whole-row gathers: 1-2 L1 wavefronts per
-// entry instead of one per column (SPB_VEC_COLS=0 restores the per-lane form).
-template <int G, int MODE, int EPI>
+// Binned rows (all four bins by default), lanes over columns: R rows per warp,
+// L = 32 / R lanes per row, G = pow2(m) lanes per entry (lane = column),
+// E = L / G entries per instruction, U instructions in flight; the E slot sums
+// combine by a fixed butterfly (deterministic). Coalesced whole-row gathers: 1-2
+// L1 wavefronts per entry instead of one per column and entry
+// (SPB_VEC_COLS=0 restores the per-lane form).
+template <int G, int R, int MODE, int EPI>
 __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op, const View X, const EpiArgs ea,
                                                                  const int m, const int32_t* rows,
                                                                  const int64_t nrows, const int partial_base) {
-    constexpr int E = 32 / G;
+    constexpr int L = 32 / R;
+    static_assert(L >= G, "a row group must hold one entry's columns");
+    constexpr int E = L / G;
     constexpr int U = 4;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane / G, c = lane % G;
+    const int grp = lane / L, gl = lane % L;
+    const int sub = gl / G, c = gl % G;
     const bool act = c < m;
+    // warp-uniform row loop (the butterfly below is a full-warp shuffle)
     const int64_t w0 = (blockIdx.x * static_cast<int64_t>(kVThreads) + threadIdx.x) >> 5;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * (kVThreads / 32);
     double sq = 0.0;
-    for (int64_t r = w0; r < nrows; r += nw) {
-        const int64_t row = rows[r];
+    for (int64_t rb = w0 * R; rb < nrows; rb += nw * R) {
+        const int64_t r = rb + grp;
+        const bool valid = r < nrows;
+        const int64_t row = valid ? rows[r] : 0;
         const int64_t grow = op.row0 + row;
-        const int64_t k0 = op.offs[row], k1 = op.offs[row + 1];
+        const int64_t k0 = valid ? op.offs[row] : 0, k1 = valid ? op.offs[row + 1] : 0;
         double nisdi = 0.0;
-        if (MODE == OP_NORMAL_UNIT) nisdi = -op.isd[grow];
+        if (MODE == OP_NORMAL_UNIT && valid) nisdi = -op.isd[grow];
         double acc = 0.0;
         int64_t k = k0 + sub;
         for (; k + (U - 1) * E < k1; k += U * E) {
@@ -143,8 +150,8 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
             acc = fma(w, x, acc);
         }
 #pragma unroll
-        for (int off = 16; off >= G; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-        if (sub == 0 && act) {
+        for (int off = L / 2; off >= G; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (valid && sub == 0 && act) {
             const double xi = X.at(grow, c);
             double v = acc;
             if (MODE == OP_LAPLACE_UNIT) v = __dadd_rn(v, __dmul_rn(op.diag[row], xi));
@@ -154,11 +161,12 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
     }
     if (EPI == EPI_RESIDUAL) {
         __shared__ double s_sq[kVThreads / 32][32];
-        s_sq[warp][lane] = (sub == 0) ? sq : 0.0;
+        s_sq[warp][lane] = sq;  // zero on lanes that never ran an epilogue
         __syncthreads();
         if (threadIdx.x < m) {
             double t = 0.0;
-            for (int w = 0; w < kVThreads / 32; ++w) t += s_sq[w][threadIdx.x];
+            for (int w = 0; w < kVThreads / 32; ++w)
+                for (int g = 0; g < R; ++g) t += s_sq[w][g * L + threadIdx.x];
             ea.partial[static_cast<int64_t>(partial_base + blockIdx.x) * m + threadIdx.x] = t;
         }
     }
@@ -346,11 +354,35 @@ int launch_bin(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t 
     }();
     if (S >= 16 && cols_form) {
         const int grid = grid_for(nrows, kVThreads / 32, 8);
-        if (m <= 8) spmm_rowcols_kernel<8, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-        else if (m <= 16) spmm_rowcols_kernel<16, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-        else spmm_rowcols_kernel<32, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        if (m <= 8) spmm_rowcols_kernel<8, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        else if (m <= 16) spmm_rowcols_kernel<16, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+        else spmm_rowcols_kernel<32, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
         SPB_LAUNCH_CHECK();
         return grid;
+    }
+    static const bool cols_short = [] {
+        const char* e = std::getenv("SPB_VEC_COLS_SHORT");
+        return !(e && e[0] == '0');
+    }();
+    if (S < 16 && cols_form && cols_short) {
+        // short rows: several rows per warp, L = 8 (S = 4) or 16 (S = 8) lanes per row when m fits
+        constexpr int RS = S == 4 ? 4 : 2;
+        if (m <= 8) {
+            const int grid = grid_for(nrows, (kVThreads / 32) * RS, 8);
+            spmm_rowcols_kernel<8, RS, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+            SPB_LAUNCH_CHECK();
+            return grid;
+        } else if (m <= 16) {
+            const int grid = grid_for(nrows, (kVThreads / 32) * 2, 8);
+            spmm_rowcols_kernel<16, 2, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+            SPB_LAUNCH_CHECK();
+            return grid;
+        } else {
+            const int grid = grid_for(nrows, kVThreads / 32, 8);
+            spmm_rowcols_kernel<32, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+            SPB_LAUNCH_CHECK();
+            return grid;
+        }
     }
     const int grid = grid_for(nrows, kVThreads / S, 8);
     if (m <= 8) spmm_vec_kernel<S, 8, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);

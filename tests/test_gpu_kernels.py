@@ -26,6 +26,9 @@ def _graphs():
     yield "st27", gen.stencil3d(6, 7, 5, 27)
     for s in range(4):
         yield f"rand{s}", gen.random_connected_graph(30 + 17 * s, 60 + 40 * s, seed=s)
+    # rows longer than one warp's 32-term group (normal_bound_kernel's unrolled path)
+    yield "star100", gen.graph_from_edges(101, [(0, i) for i in range(1, 101)] + [(i, i + 1) for i in range(1, 100)])
+    yield "rmat10", gen.rmat(10, 16, seed=3)[0]
     # weighted costs: laplacian_test.cpp:173-211 style
     g = gen.random_connected_graph(50, 120, seed=9)
     rng = np.random.default_rng(3)
@@ -85,7 +88,7 @@ def test_spmm_bit_exact(ctx, ref, kind, m):
     assert ctx.spmm(kind, g, X).tobytes() == ref.spmm(kind, g, X).tobytes()
 
 
-@pytest.mark.parametrize("name,g", GRAPHS[-5:], ids=[n for n, _ in GRAPHS[-5:]])
+@pytest.mark.parametrize("name,g", GRAPHS[-7:], ids=[n for n, _ in GRAPHS[-7:]])
 def test_spmm_bit_exact_irregular(ctx, ref, name, g):
     X = np.random.default_rng(1).uniform(-1, 1, (g.n, 7))
     for kind in ("combinatorial", "normalized"):
