@@ -80,7 +80,29 @@ def build(verbose: bool = False) -> Path:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     _build_shim_test(verbose)
+    _build_cli(verbose)
     return LIB
+
+
+NLOHMANN = Path(os.environ.get(
+    "NLOHMANN_DIR", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"))
+CLI = ROOT / "build" / "specpart_b200"
+
+
+def _build_cli(verbose: bool) -> None:
+    """build/specpart_b200: the reference CLI (tools/specpart.cpp) on the C-ABI
+    (paper_2105_00578_b200/tools/specpart_cli.cpp); nlohmann/json serializes the report as in
+    pipeline.cpp:169-215."""
+    src = PKG / "tools" / "specpart_cli.cpp"
+    if CLI.exists() and CLI.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime,
+                                                   (ROOT / "include" / "specpart_b200.h").stat().st_mtime):
+        return
+    CLI.parent.mkdir(parents=True, exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), "-I", str(NLOHMANN), str(src), "-L", str(PKG),
+           "-lspecpart_b200", "-Wl,-rpath,$ORIGIN/../paper_2105_00578_b200", "-o", str(CLI)]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
 
 
 def _build_shim_test(verbose: bool) -> None:

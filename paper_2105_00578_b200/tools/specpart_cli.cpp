@@ -1,0 +1,576 @@
+// specpart_b200 — the reference's command-line front end (tools/specpart.cpp) on the B200 C-ABI.
+//
+// Same options, subcommand `gen`, output formats and exit codes as tools/specpart.cpp:
+//   * Matrix Market parsing (sparse.cpp:105-171) on the host — file I/O, no device work;
+//   * symmetrize + largest_connected_component (graph.cpp:44-171) on the device (sp_ingest);
+//   * partition_graph (pipeline.cpp:47-167) on the device graph (sp_partition_resident), or the
+//     --init-file warm start (tools/specpart.cpp:94-157, x0 passed to the same call);
+//   * write_partition "origId partId" lines (graph.cpp:232-238) and the JSON run report
+//     (pipeline.cpp:169-215, docs/report_schema.md: nlohmann::json::dump(2) layout, keys sorted).
+// Exit codes (tools/specpart.cpp:19-22, 335-350): 0 ok, 1 other error, 2 parse error, 3 solver
+// breakdown, 4 infeasible configuration / degenerate degree. Option errors use CLI11's codes.
+#include "specpart_b200.h"
+
+#include <json.hpp>  // nlohmann/json (header-only; the reference's report serializer)
+
+#include <algorithm>
+#include <cctype>
+#include <charconv>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+namespace {
+
+constexpr int kExitParse = 2, kExitBreakdown = 3, kExitInfeasible = 4;
+// CLI11 exit codes for option errors (CLI11 ExitCodes)
+constexpr int kCliConversion = 101, kCliValidation = 105, kCliRequired = 106, kCliExtras = 109;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& m) { throw Fail{code, m}; }
+
+// ---- Matrix Market (sparse.cpp:79-171) --------------------------------------------------------
+std::string lower(std::string s) {
+    for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    return s;
+}
+
+bool blank_or_comment(const std::string& line) {
+    for (char c : line) {
+        if (c == '%') return true;
+        if (!std::isspace(static_cast<unsigned char>(c))) return false;
+    }
+    return true;
+}
+
+// ParseError::what() (errors.hpp:10-19)
+std::string perr(const std::string& m, std::size_t line) {
+    return "line " + std::to_string(line) + ": " + m;
+}
+
+// Pattern CSR of the parsed matrix, rows bucketed in file order (duplicates kept: sp_ingest's
+// sort + unique is from_triplets(sum_duplicates=false), and symmetrize ignores values).
+struct Pattern {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> offsets;
+    std::vector<int32_t> cols;
+};
+
+Pattern parse_matrix_market(std::istream& in) {
+    std::string line;
+    std::size_t lineno = 0;
+    if (!std::getline(in, line)) fail(kExitParse, perr("empty input", 1));
+    ++lineno;
+    std::istringstream banner(line);
+    std::string tag, object, format, field, symmetry;
+    banner >> tag >> object >> format >> field >> symmetry;
+    if (lower(tag) != "%%matrixmarket" || lower(object) != "matrix")
+        fail(kExitParse, perr("malformed MatrixMarket banner", lineno));
+    format = lower(format);
+    field = lower(field);
+    symmetry = lower(symmetry);
+    if (format != "coordinate")
+        fail(kExitParse, perr("unsupported format '" + format + "' (coordinate only)", lineno));
+    const bool pattern = field == "pattern";
+    if (!pattern && field != "real" && field != "integer")
+        fail(kExitParse, perr("unsupported field '" + field + "'", lineno));
+    const bool symmetric = symmetry == "symmetric";
+    if (!symmetric && symmetry != "general")
+        fail(kExitParse, perr("unsupported symmetry '" + symmetry + "'", lineno));
+
+    int64_t nrows = 0, ncols = 0, declared = 0;
+    for (;;) {
+        if (!std::getline(in, line)) fail(kExitParse, perr("missing size line", lineno + 1));
+        ++lineno;
+        if (blank_or_comment(line)) continue;
+        std::istringstream sz(line);
+        if (!(sz >> nrows >> ncols >> declared) || nrows < 0 || ncols < 0 || declared < 0)
+            fail(kExitParse, perr("malformed size line", lineno));
+        std::string extra;
+        if (sz >> extra) fail(kExitParse, perr("trailing tokens on size line", lineno));
+        break;
+    }
+    std::vector<int32_t> rr, cc;
+    rr.reserve(static_cast<size_t>(symmetric ? 2 * declared : declared));
+    cc.reserve(rr.capacity());
+    int64_t seen = 0;
+    while (seen < declared) {
+        if (!std::getline(in, line))
+            fail(kExitParse, perr("entry list truncated: expected " + std::to_string(declared) +
+                                      " entries, got " + std::to_string(seen),
+                                  lineno + 1));
+        ++lineno;
+        if (blank_or_comment(line)) continue;
+        std::istringstream es(line);
+        int64_t r = 0, c = 0;
+        double v = 1.0;
+        if (!(es >> r >> c)) fail(kExitParse, perr("malformed entry", lineno));
+        if (!pattern && !(es >> v)) fail(kExitParse, perr("missing value", lineno));
+        std::string extra;
+        if (es >> extra) fail(kExitParse, perr("trailing tokens on entry", lineno));
+        if (r < 1 || r > nrows || c < 1 || c > ncols)
+            fail(kExitParse, perr("index out of range: (" + std::to_string(r) + ", " + std::to_string(c) + ")",
+                                  lineno));
+        rr.push_back(static_cast<int32_t>(r - 1));
+        cc.push_back(static_cast<int32_t>(c - 1));
+        if (symmetric && r != c) {
+            rr.push_back(static_cast<int32_t>(c - 1));
+            cc.push_back(static_cast<int32_t>(r - 1));
+        }
+        ++seen;
+    }
+    Pattern p;
+    p.nrows = nrows;
+    p.ncols = ncols;
+    p.offsets.assign(static_cast<size_t>(nrows + 1), 0);
+    for (int32_t r : rr) ++p.offsets[static_cast<size_t>(r) + 1];
+    for (int64_t i = 0; i < nrows; ++i) p.offsets[i + 1] += p.offsets[i];
+    std::vector<int64_t> pos(p.offsets.begin(), p.offsets.end() - 1);
+    p.cols.resize(rr.size());
+    for (size_t k = 0; k < rr.size(); ++k) p.cols[static_cast<size_t>(pos[rr[k]]++)] = cc[k];
+    return p;
+}
+
+std::vector<double> vec(const double* v, int n) { return std::vector<double>(v, v + n); }
+
+const char* problem_name(int p) {
+    switch (p) {
+    case SP_PROBLEM_COMBINATORIAL: return "combinatorial";
+    case SP_PROBLEM_GENERALIZED: return "generalized";
+    case SP_PROBLEM_NORMALIZED: return "normalized";
+    default: return "auto";
+    }
+}
+const char* precond_name(int p) {
+    switch (p) {
+    case SP_PRECOND_JACOBI: return "jacobi";
+    case SP_PRECOND_POLYNOMIAL: return "polynomial";
+    case SP_PRECOND_AMG: return "amg";
+    case SP_PRECOND_NONE: return "none";
+    default: return "auto";
+    }
+}
+const char* init_name(int p) {
+    switch (p) {
+    case SP_INIT_RANDOM: return "random";
+    case SP_INIT_PIECEWISE: return "piecewise";
+    default: return "auto";
+    }
+}
+
+// RunReport::to_json (pipeline.cpp:169-215), serialized with the same header-only library the
+// reference uses (nlohmann::json, sorted keys, dump(2)), so reports compare byte-for-byte.
+std::string report_json(const sp_report& r, const std::vector<double>& part_weights, int64_t dropped,
+                        const std::vector<std::string>& warnings, bool with_trace) {
+    using nlohmann::json;
+    json j;
+    j["graph"] = {{"n", r.n},
+                  {"edges", r.edges},
+                  {"max_degree", r.max_degree},
+                  {"avg_degree", r.avg_degree},
+                  {"degree_ratio", r.degree_ratio},
+                  {"kind", r.graph_regular ? "regular" : "irregular"},
+                  {"dropped_vertices", dropped}};
+    j["config"] = {{"parts", r.num_parts},
+                   {"problem", problem_name(r.problem)},
+                   {"preconditioner", precond_name(r.precond)},
+                   {"tolerance", r.tol},
+                   {"initial_vectors", init_name(r.init)},
+                   {"eigenvectors", r.eigenvectors},
+                   {"seed", r.seed},
+                   {"max_iters", r.max_iters},
+                   {"epsilon", r.epsilon},
+                   {"doubled_cut", r.doubled_cut != 0}};
+    std::vector<bool> conv;
+    for (int k = 0; k < r.eigenvectors; ++k) conv.push_back(r.converged[k] != 0);
+    j["solver"] = {{"iterations", r.iterations},
+                   {"theta", vec(r.theta, r.eigenvectors)},
+                   {"residual_norms", vec(r.residual_norms, r.eigenvectors)},
+                   {"converged", conv}};
+    if (with_trace && r.trace_len > 0) {
+        json tr = json::array();
+        for (int t = 0; t < r.trace_len; ++t) {
+            const sp_trace_record& rec = r.trace[t];
+            tr.push_back({{"iter", rec.iter},
+                          {"min_residual", rec.min_residual},
+                          {"max_residual", rec.max_residual},
+                          {"theta", vec(rec.theta, rec.ntheta)}});
+        }
+        j["solver"]["trace"] = tr;
+    }
+    j["times"] = {{"laplacian_s", r.laplacian_s},
+                  {"eigensolve_s", r.eigensolve_s},
+                  {"partition_s", r.partition_s},
+                  {"total_s", r.total_s}};
+    j["partition"] = {{"cutsize", r.cutsize}, {"imbalance", r.imbalance}, {"part_weights", part_weights}};
+    j["warnings"] = warnings;
+    return j.dump(2);
+}
+
+// ---- status → the reference's exception classes (tools/specpart.cpp:335-350) ----------------
+void check(sp_status st, sp_context* ctx) {
+    if (st == SP_OK) return;
+    const std::string m = sp_last_error(ctx) ? sp_last_error(ctx) : "";
+    switch (st) {
+    case SP_PARSE: fail(kExitParse, "parse error: " + m);
+    case SP_BREAKDOWN: fail(kExitBreakdown, "solver breakdown: " + m);
+    case SP_INFEASIBLE:
+    case SP_DEGENERATE: fail(kExitInfeasible, "infeasible: " + m);
+    default: fail(1, "error: " + m);
+    }
+}
+
+// ---- gen (generators.cpp:126-175 + write_matrix_market_pattern_symmetric, sparse.cpp:179-191)
+void write_lower(std::ostream& out, int64_t n, int64_t lower_count,
+                 const std::function<void(int64_t, std::vector<int64_t>&)>& lower_nbrs) {
+    out << "%%MatrixMarket matrix coordinate pattern symmetric\n";
+    out << n << ' ' << n << ' ' << lower_count << '\n';
+    std::vector<int64_t> nb;
+    for (int64_t i = 0; i < n; ++i) {
+        nb.clear();
+        lower_nbrs(i, nb);
+        for (int64_t j : nb) out << i + 1 << ' ' << j + 1 << '\n';
+    }
+}
+
+int run_gen(const std::string& kind, const std::vector<int64_t>& dims, int stencil, std::ostream& out) {
+    auto dim = [&](size_t i) -> int64_t {
+        if (i >= dims.size()) fail(kExitInfeasible, "infeasible: gen: missing dimension for " + kind);
+        return dims[i];
+    };
+    if (kind == "grid2d") {
+        const int64_t w = dim(0), h = dim(1);
+        if (w < 1 || h < 1) fail(kExitInfeasible, "infeasible: grid2d: dimensions must be positive");
+        const int64_t cnt = w * (h - 1) + h * (w - 1);
+        write_lower(out, w * h, cnt, [&](int64_t i, std::vector<int64_t>& nb) {
+            const int64_t x = i % w, y = i / w;
+            if (y > 0) nb.push_back(i - w);
+            if (x > 0) nb.push_back(i - 1);
+        });
+    } else if (kind == "stencil3d") {
+        const int64_t nx = dim(0), ny = dim(1), nz = dim(2);
+        if (nx < 1 || ny < 1 || nz < 1) fail(kExitInfeasible, "infeasible: stencil3d: dimensions must be positive");
+        if (stencil != 7 && stencil != 27) fail(kExitInfeasible, "infeasible: stencil3d: stencil must be 7 or 27");
+        auto nbrs = [&](int64_t i, std::vector<int64_t>& nb) {
+            const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+            for (int64_t dz = -1; dz <= 1; ++dz)
+                for (int64_t dy = -1; dy <= 1; ++dy)
+                    for (int64_t dx = -1; dx <= 1; ++dx) {
+                        if (dx == 0 && dy == 0 && dz == 0) continue;
+                        if (stencil == 7 && std::abs(dx) + std::abs(dy) + std::abs(dz) != 1) continue;
+                        const int64_t X = x + dx, Y = y + dy, Z = z + dz;
+                        if (X < 0 || X >= nx || Y < 0 || Y >= ny || Z < 0 || Z >= nz) continue;
+                        const int64_t j = (Z * ny + Y) * nx + X;
+                        if (j < i) nb.push_back(j);  // ascending: (dz, dy, dx) order is id order
+                    }
+        };
+        int64_t cnt = 0;
+        std::vector<int64_t> nb;
+        for (int64_t i = 0; i < nx * ny * nz; ++i) {
+            nb.clear();
+            nbrs(i, nb);
+            cnt += static_cast<int64_t>(nb.size());
+        }
+        write_lower(out, nx * ny * nz, cnt, nbrs);
+    } else if (kind == "ring") {
+        const int64_t n = dim(0);
+        if (n < 3) fail(kExitInfeasible, "infeasible: ring: need n >= 3");
+        write_lower(out, n, n, [&](int64_t i, std::vector<int64_t>& nb) {
+            if (i == n - 1) nb.push_back(0);
+            if (i > 0) nb.push_back(i - 1);
+        });
+    } else if (kind == "path") {
+        const int64_t n = dim(0);
+        if (n < 1) fail(kExitInfeasible, "infeasible: path: need n >= 1");
+        write_lower(out, n, n - 1, [&](int64_t i, std::vector<int64_t>& nb) {
+            if (i > 0) nb.push_back(i - 1);
+        });
+    } else if (kind == "randomregular" || kind == "scalefree") {
+        fail(1, "error: gen: '" + kind + "' is not provided by this build (seeded host generators, "
+                "generators.cpp:176-300, are outside the B200 hot path)");
+    } else {
+        fail(kExitInfeasible, "infeasible: gen: unknown kind '" + kind + "'");
+    }
+    return 0;
+}
+
+// ---- partition (tools/specpart.cpp:62-196) ---------------------------------------------------
+struct Args {
+    std::string input, problem = "auto", precond = "auto", init = "auto", output, report, init_file;
+    int64_t parts = 0;
+    double tolerance = -1.0;
+    int max_iters = 1000;
+    uint64_t seed = 42;
+    double epsilon = 0.01;
+    bool doubled_cut = false, trace = false;
+};
+
+std::vector<double> load_dense_block_colmajor(const std::string& path, int64_t* rows, int64_t* cols) {
+    std::ifstream in(path);
+    if (!in) fail(kExitParse, "parse error: " + perr("cannot open '" + path + "'", 0));
+    if (!(in >> *rows >> *cols) || *rows < 1 || *cols < 1)
+        fail(kExitParse, "parse error: " + perr("malformed block header in '" + path + "'", 1));
+    std::vector<double> X(static_cast<size_t>(*rows * *cols));
+    for (int64_t i = 0; i < *rows; ++i)
+        for (int64_t j = 0; j < *cols; ++j)
+            if (!(in >> X[static_cast<size_t>(j * *rows + i)]))
+                fail(kExitParse, "parse error: " + perr("truncated block data in '" + path + "'", 0));
+    return X;
+}
+
+int eigenvector_count(int64_t K) {  // partitioner.cpp:13-17: bit_width(K)
+    int b = 0;
+    for (uint64_t k = static_cast<uint64_t>(K); k; k >>= 1) ++b;
+    return b;
+}
+
+int run_partition(const Args& a) {
+    Pattern raw;
+    {
+        std::ifstream in(a.input);
+        if (!in) fail(kExitParse, "parse error: " + perr("cannot open '" + a.input + "'", 0));
+        try {
+            raw = parse_matrix_market(in);
+        } catch (const Fail& f) {
+            fail(f.code, "parse error: " + f.msg);
+        }
+    }
+    if (raw.nrows != raw.ncols) fail(1, "error: symmetrize: matrix not square");
+
+    sp_context* ctx = nullptr;
+    if (sp_context_create(0, &ctx) != SP_OK) fail(1, "error: cannot create the CUDA context");
+    struct Guard {
+        sp_context* c;
+        sp_device_graph* g = nullptr;
+        ~Guard() {
+            if (g) sp_graph_free(g);
+            sp_context_destroy(c);
+        }
+    } guard{ctx};
+
+    check(sp_ingest(ctx, raw.nrows, raw.offsets.data(), raw.cols.data(), 1, &guard.g), ctx);
+    sp_graph_info info{};
+    check(sp_device_graph_info(ctx, guard.g, &info), ctx);
+    const int64_t dropped = info.n_symmetrized - info.n;
+    std::vector<int64_t> old_ids(static_cast<size_t>(std::max<int64_t>(info.n, 1)));
+    check(sp_device_graph_download(ctx, guard.g, nullptr, nullptr, old_ids.data()), ctx);
+
+    sp_config cfg{};
+    cfg.num_parts = a.parts;
+    cfg.problem = a.problem == "combinatorial" ? SP_PROBLEM_COMBINATORIAL
+                  : a.problem == "generalized" ? SP_PROBLEM_GENERALIZED
+                  : a.problem == "normalized"  ? SP_PROBLEM_NORMALIZED
+                                               : SP_PROBLEM_AUTO;
+    cfg.precond = a.precond == "jacobi"       ? SP_PRECOND_JACOBI
+                  : a.precond == "polynomial" ? SP_PRECOND_POLYNOMIAL
+                  : a.precond == "amg"        ? SP_PRECOND_AMG
+                  : a.precond == "none"       ? SP_PRECOND_NONE
+                                              : SP_PRECOND_AUTO;
+    cfg.init = a.init == "random" ? SP_INIT_RANDOM : a.init == "piecewise" ? SP_INIT_PIECEWISE : SP_INIT_AUTO;
+    cfg.tol = a.tolerance > 0.0 ? a.tolerance : -1.0;
+    cfg.max_iters = a.max_iters;
+    cfg.seed = a.seed;
+    cfg.epsilon = a.epsilon;
+    cfg.doubled_cut = a.doubled_cut;
+    cfg.record_trace = a.trace;
+
+    std::vector<double> x0;
+    if (!a.init_file.empty()) {
+        int64_t rows = 0, cols = 0;
+        x0 = load_dense_block_colmajor(a.init_file, &rows, &cols);
+        if (rows != info.n)
+            fail(kExitInfeasible, "infeasible: initial block has " + std::to_string(rows) +
+                                      " rows but the graph has " + std::to_string(info.n) + " vertices");
+        if (cols != eigenvector_count(a.parts))
+            fail(kExitInfeasible, "infeasible: initial block must have d=" +
+                                      std::to_string(eigenvector_count(a.parts)) + " columns");
+    }
+
+    std::vector<int32_t> assignment(static_cast<size_t>(info.n));
+    std::vector<double> part_weights(static_cast<size_t>(std::max<int64_t>(a.parts, 1)));
+    std::vector<sp_trace_record> trace(a.trace ? static_cast<size_t>(a.max_iters) + 2 : 0);
+    sp_report rep{};
+    rep.part_weights = part_weights.data();
+    rep.trace = trace.empty() ? nullptr : trace.data();
+    rep.trace_capacity = static_cast<int32_t>(trace.size());
+    check(sp_partition_resident(ctx, guard.g, &cfg, assignment.data(), &rep, x0.empty() ? nullptr : x0.data()),
+          ctx);
+
+    // pipeline.cpp:140-163 warnings; the --init-file path reports only its own (specpart.cpp:156)
+    std::vector<std::string> warnings;
+    if (!a.init_file.empty()) {
+        rep.init = SP_INIT_RANDOM;
+        warnings.push_back("initial vectors loaded from " + a.init_file);
+    } else {
+        if (rep.warnings & SP_WARN_BREAKDOWN_RECOVERED)
+            warnings.emplace_back("eigensolver recovered from a basis breakdown by clearing the search directions");
+        if (rep.warnings & SP_WARN_UNCONVERGED)
+            warnings.emplace_back("eigensolver reached max_iters with unconverged columns; "
+                                  "partitioning on partially converged eigenvectors");
+        if (rep.warnings & SP_WARN_IMBALANCE)
+            warnings.emplace_back("imbalance " + std::to_string(rep.imbalance) + " exceeds 1+epsilon = " +
+                                  std::to_string(1.0 + a.epsilon));
+    }
+    if (dropped > 0)
+        warnings.push_back("input graph was disconnected; kept the largest component (" + std::to_string(info.n) +
+                           " of " + std::to_string(info.n_symmetrized) + " vertices)");
+
+    // write_partition (graph.cpp:232-238): "origId partId" per vertex
+    {
+        std::string buf;
+        buf.reserve(assignment.size() * 16);
+        char line[48];
+        for (size_t v = 0; v < assignment.size(); ++v) {
+            const int len = std::snprintf(line, sizeof line, "%lld %d\n", static_cast<long long>(old_ids[v]),
+                                          assignment[v]);
+            buf.append(line, static_cast<size_t>(len));
+        }
+        if (!a.output.empty()) {
+            std::ofstream out(a.output, std::ios::binary);
+            out << buf;
+        } else {
+            std::cout << buf;
+        }
+    }
+    if (!a.report.empty()) {
+        std::ofstream out(a.report);
+        out << report_json(rep, part_weights, dropped, warnings, a.trace) << '\n';
+    }
+    std::ostringstream imb;
+    imb << rep.imbalance;  // default ostream formatting, as specpart.cpp:189-191
+    std::cerr << "n=" << rep.n << " K=" << rep.num_parts << " cutsize=" << rep.cutsize << " imbalance=" << imb.str()
+              << " iters=" << rep.iterations << '\n';
+    for (const std::string& w : warnings) std::cerr << "warning: " << w << '\n';
+    return 0;
+}
+
+// ---- option parsing (the CLI11 surface of tools/specpart.cpp:200-235) ------------------------
+bool take(int argc, char** argv, int& i, const char* name, std::string& val) {
+    const size_t L = std::strlen(name);
+    if (std::strncmp(argv[i], name, L) != 0) return false;
+    if (argv[i][L] == '=') {
+        val = argv[i] + L + 1;
+        return true;
+    }
+    if (argv[i][L] != '\0') return false;
+    if (i + 1 >= argc) fail(kCliConversion, std::string(name) + " requires an argument");
+    val = argv[++i];
+    return true;
+}
+
+template <class T>
+T num(const std::string& s, const char* name) {
+    T v{};
+    auto r = std::from_chars(s.data(), s.data() + s.size(), v);
+    if (r.ec != std::errc() || r.ptr != s.data() + s.size())
+        fail(kCliConversion, std::string("Could not convert: ") + name + " = " + s);
+    return v;
+}
+
+void member(const std::string& v, const char* name, std::initializer_list<const char*> allowed) {
+    for (const char* a : allowed)
+        if (v == a) return;
+    fail(kCliValidation, std::string(name) + ": " + v + " not in allowed set");
+}
+
+void usage() {
+    std::cout << "spectral graph partitioner (B200)\n"
+                 "Usage: specpart_b200 [OPTIONS] [SUBCOMMAND]\n"
+                 "  --input FILE        Matrix Market graph file\n"
+                 "  --parts K           number of parts K\n"
+                 "  --problem P         auto|combinatorial|generalized|normalized\n"
+                 "  --precond P         auto|jacobi|polynomial|amg|none\n"
+                 "  --init I            auto|random|piecewise\n"
+                 "  --tolerance T       eigensolver residual tolerance\n"
+                 "  --max-iters N       eigensolver iteration cap\n"
+                 "  --seed S            random seed\n"
+                 "  --epsilon E         allowed imbalance ratio (default 0.01)\n"
+                 "  --threads N         accepted for compatibility (the solve runs on the GPU)\n"
+                 "  --doubled-cut       report cut edges counted twice\n"
+                 "  --trace             record per-iteration solver trace in the report\n"
+                 "  --output FILE       partition file (default stdout)\n"
+                 "  --report FILE       write a JSON run report\n"
+                 "  --init-file FILE    dense initial block: 'rows cols' header, row-major values\n"
+                 "Subcommands:\n"
+                 "  gen KIND DIMS... [--stencil 7|27] [--seed S] [--out FILE]   grid2d|stencil3d|ring|path\n";
+}
+
+int main_impl(int argc, char** argv) {
+    Args a;
+    int i = 1;
+    if (argc > 1 && std::strcmp(argv[1], "gen") == 0) {
+        std::string kind, out, v;
+        std::vector<int64_t> dims;
+        int stencil = 27;
+        for (i = 2; i < argc; ++i) {
+            if (take(argc, argv, i, "--stencil", v)) stencil = num<int>(v, "--stencil");
+            else if (take(argc, argv, i, "--seed", v)) (void)num<uint64_t>(v, "--seed");
+            else if (take(argc, argv, i, "--out", out)) {
+            } else if (argv[i][0] == '-' && argv[i][1] == '-') fail(kCliExtras, std::string("The following argument was not expected: ") + argv[i]);
+            else if (kind.empty()) kind = argv[i];
+            else dims.push_back(num<int64_t>(argv[i], "dims"));
+        }
+        if (kind.empty() || dims.empty()) fail(kCliRequired, "gen: kind and dims are required");
+        if (!out.empty()) {
+            std::ofstream f(out);
+            return run_gen(kind, dims, stencil, f);
+        }
+        return run_gen(kind, dims, stencil, std::cout);
+    }
+    for (; i < argc; ++i) {
+        std::string v;
+        if (!std::strcmp(argv[i], "--help") || !std::strcmp(argv[i], "-h")) {
+            usage();
+            return 0;
+        }
+        if (!std::strcmp(argv[i], "--doubled-cut")) a.doubled_cut = true;
+        else if (!std::strcmp(argv[i], "--trace")) a.trace = true;
+        else if (take(argc, argv, i, "--input", a.input)) {
+        } else if (take(argc, argv, i, "--parts", v)) a.parts = num<int64_t>(v, "--parts");
+        else if (take(argc, argv, i, "--problem", a.problem))
+            member(a.problem, "--problem", {"auto", "combinatorial", "generalized", "normalized"});
+        else if (take(argc, argv, i, "--precond", a.precond))
+            member(a.precond, "--precond", {"auto", "jacobi", "polynomial", "amg", "none"});
+        else if (take(argc, argv, i, "--init", a.init)) member(a.init, "--init", {"auto", "random", "piecewise"});
+        else if (take(argc, argv, i, "--tolerance", v)) a.tolerance = num<double>(v, "--tolerance");
+        else if (take(argc, argv, i, "--max-iters", v)) a.max_iters = num<int>(v, "--max-iters");
+        else if (take(argc, argv, i, "--seed", v)) a.seed = num<uint64_t>(v, "--seed");
+        else if (take(argc, argv, i, "--epsilon", v)) a.epsilon = num<double>(v, "--epsilon");
+        else if (take(argc, argv, i, "--threads", v)) (void)num<int>(v, "--threads");
+        else if (take(argc, argv, i, "--output", a.output)) {
+        } else if (take(argc, argv, i, "--report", a.report)) {
+        } else if (take(argc, argv, i, "--init-file", a.init_file)) {
+        } else fail(kCliExtras, std::string("The following argument was not expected: ") + argv[i]);
+    }
+    if (a.input.empty() || a.parts < 2) {
+        std::cerr << "error: --input and --parts >= 2 are required (see --help)\n";
+        return kExitInfeasible;
+    }
+    return run_partition(a);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        return main_impl(argc, argv);
+    } catch (const Fail& f) {
+        std::cerr << f.msg << '\n';
+        return f.code;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << '\n';
+        return 1;
+    }
+}
