@@ -4,6 +4,7 @@
 // the partition files, reports and .mtx outputs the B200 CLI must reproduce.
 //   cli_ref gen KIND STENCIL DIMS...              -> .mtx on stdout
 //   cli_ref part MTX K PROBLEM PRECOND SEED OUT REPORT
+//   cli_ref sweep K SEED SPEC,SPEC PRECOND,PRECOND PROBLEM,PROBLEM   (tools/specpart.cpp:265-327)
 #include "specpart/generators.hpp"
 #include "specpart/graph.hpp"
 #include "specpart/pipeline.hpp"
@@ -32,6 +33,43 @@ int main(int argc, char** argv) {
         else if (kind == "path") spec.kind = GeneratorSpec::Kind::Path, spec.a = d[0];
         else return 1;
         write_matrix_market_pattern_symmetric(std::cout, generate(spec).adjacency);
+        return 0;
+    }
+    if (mode == "sweep") {
+        auto split = [](const std::string& t) {
+            std::vector<std::string> v;
+            std::size_t p = 0;
+            while (p <= t.size()) {
+                const std::size_t q = t.find(';', p);
+                v.push_back(t.substr(p, q == std::string::npos ? std::string::npos : q - p));
+                if (q == std::string::npos) break;
+                p = q + 1;
+            }
+            return v;
+        };
+        std::vector<Graph> storage;
+        std::vector<std::pair<std::string, const Graph*>> graphs;
+        const auto specs = split(argv[4]);
+        storage.reserve(specs.size());
+        for (const std::string& t : specs) {
+            storage.push_back(generate(GeneratorSpec::parse(t)));
+            graphs.emplace_back(t, &storage.back());
+        }
+        std::vector<std::pair<std::string, RunConfig>> configs;
+        for (const std::string& pc : split(argv[5]))
+            for (const std::string& pr : split(argv[6])) {
+                RunConfig c;
+                c.num_parts = std::atoll(argv[2]);
+                c.seed = std::strtoull(argv[3], nullptr, 10);
+                c.precond = pc == "polynomial" ? PrecondChoice::Polynomial
+                            : pc == "none"     ? PrecondChoice::None
+                                               : PrecondChoice::Jacobi;
+                if (pr == "combinatorial") c.problem = ProblemChoice::Combinatorial;
+                else if (pr == "generalized") c.problem = ProblemChoice::Generalized;
+                else if (pr == "normalized") c.problem = ProblemChoice::Normalized;
+                configs.emplace_back(pc + "/" + pr + "/tol=auto", c);
+            }
+        std::cout << run_sweep(graphs, configs).to_tsv();
         return 0;
     }
     const std::string problem = argv[4], precond = argv[5];

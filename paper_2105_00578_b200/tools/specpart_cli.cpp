@@ -1,6 +1,6 @@
 // specpart_b200 — the reference's command-line front end (tools/specpart.cpp) on the B200 C-ABI.
 //
-// Same options, subcommand `gen`, output formats and exit codes as tools/specpart.cpp:
+// Same options, subcommands `gen` and `sweep`, output formats and exit codes as tools/specpart.cpp:
 //   * Matrix Market parsing (sparse.cpp:105-171) on the host — file I/O, no device work;
 //   * symmetrize + largest_connected_component (graph.cpp:44-171) on the device (sp_ingest);
 //   * partition_graph (pipeline.cpp:47-167) on the device graph (sp_partition_resident), or the
@@ -22,7 +22,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
-#include <functional>
 #include <iostream>
 #include <sstream>
 #include <string>
@@ -232,77 +231,212 @@ void check(sp_status st, sp_context* ctx) {
     }
 }
 
-// ---- gen (generators.cpp:126-175 + write_matrix_market_pattern_symmetric, sparse.cpp:179-191)
-void write_lower(std::ostream& out, int64_t n, int64_t lower_count,
-                 const std::function<void(int64_t, std::vector<int64_t>&)>& lower_nbrs) {
-    out << "%%MatrixMarket matrix coordinate pattern symmetric\n";
-    out << n << ' ' << n << ' ' << lower_count << '\n';
-    std::vector<int64_t> nb;
-    for (int64_t i = 0; i < n; ++i) {
-        nb.clear();
-        lower_nbrs(i, nb);
-        for (int64_t j : nb) out << i + 1 << ' ' << j + 1 << '\n';
+// ---- generators (generators.cpp:126-175) ----------------------------------------------------
+// Deterministic meshes only; nbrs(i) lists every neighbour of vertex i in ascending id order, the
+// row of graph_from_edges' CSR.
+struct MeshGen {
+    std::string kind;
+    int64_t a = 0, b = 0, c = 0;
+    int stencil = 27;
+    int64_t n() const {
+        return kind == "grid2d" ? a * b : kind == "stencil3d" ? a * b * c : a;
     }
-}
-
-int run_gen(const std::string& kind, const std::vector<int64_t>& dims, int stencil, std::ostream& out) {
-    auto dim = [&](size_t i) -> int64_t {
-        if (i >= dims.size()) fail(kExitInfeasible, "infeasible: gen: missing dimension for " + kind);
-        return dims[i];
-    };
-    if (kind == "grid2d") {
-        const int64_t w = dim(0), h = dim(1);
-        if (w < 1 || h < 1) fail(kExitInfeasible, "infeasible: grid2d: dimensions must be positive");
-        const int64_t cnt = w * (h - 1) + h * (w - 1);
-        write_lower(out, w * h, cnt, [&](int64_t i, std::vector<int64_t>& nb) {
-            const int64_t x = i % w, y = i / w;
-            if (y > 0) nb.push_back(i - w);
+    void nbrs(int64_t i, std::vector<int64_t>& nb) const {
+        if (kind == "grid2d") {
+            const int64_t x = i % a, y = i / a;
+            if (y > 0) nb.push_back(i - a);
             if (x > 0) nb.push_back(i - 1);
-        });
-    } else if (kind == "stencil3d") {
-        const int64_t nx = dim(0), ny = dim(1), nz = dim(2);
-        if (nx < 1 || ny < 1 || nz < 1) fail(kExitInfeasible, "infeasible: stencil3d: dimensions must be positive");
-        if (stencil != 7 && stencil != 27) fail(kExitInfeasible, "infeasible: stencil3d: stencil must be 7 or 27");
-        auto nbrs = [&](int64_t i, std::vector<int64_t>& nb) {
-            const int64_t x = i % nx, y = (i / nx) % ny, z = i / (nx * ny);
+            if (x + 1 < a) nb.push_back(i + 1);
+            if (y + 1 < b) nb.push_back(i + a);
+        } else if (kind == "stencil3d") {
+            const int64_t x = i % a, y = (i / a) % b, z = i / (a * b);
             for (int64_t dz = -1; dz <= 1; ++dz)
                 for (int64_t dy = -1; dy <= 1; ++dy)
                     for (int64_t dx = -1; dx <= 1; ++dx) {
                         if (dx == 0 && dy == 0 && dz == 0) continue;
                         if (stencil == 7 && std::abs(dx) + std::abs(dy) + std::abs(dz) != 1) continue;
                         const int64_t X = x + dx, Y = y + dy, Z = z + dz;
-                        if (X < 0 || X >= nx || Y < 0 || Y >= ny || Z < 0 || Z >= nz) continue;
-                        const int64_t j = (Z * ny + Y) * nx + X;
-                        if (j < i) nb.push_back(j);  // ascending: (dz, dy, dx) order is id order
+                        if (X < 0 || X >= a || Y < 0 || Y >= b || Z < 0 || Z >= c) continue;
+                        nb.push_back((Z * b + Y) * a + X);  // (dz, dy, dx) order is id order
                     }
-        };
-        int64_t cnt = 0;
-        std::vector<int64_t> nb;
-        for (int64_t i = 0; i < nx * ny * nz; ++i) {
-            nb.clear();
-            nbrs(i, nb);
-            cnt += static_cast<int64_t>(nb.size());
+        } else if (kind == "ring") {
+            const int64_t p = (i + a - 1) % a, q = (i + 1) % a;
+            nb.push_back(std::min(p, q));
+            nb.push_back(std::max(p, q));
+        } else {  // path
+            if (i > 0) nb.push_back(i - 1);
+            if (i + 1 < a) nb.push_back(i + 1);
         }
-        write_lower(out, nx * ny * nz, cnt, nbrs);
+    }
+};
+
+// generate() argument checks (generators.cpp:126-175)
+MeshGen make_gen(const std::string& kind, const std::vector<int64_t>& dims, int stencil) {
+    auto dim = [&](size_t i) -> int64_t {
+        if (i >= dims.size()) fail(kExitInfeasible, "infeasible: gen: missing dimension for " + kind);
+        return dims[i];
+    };
+    MeshGen g;
+    g.kind = kind;
+    g.stencil = stencil;
+    if (kind == "grid2d") {
+        g.a = dim(0), g.b = dim(1);
+        if (g.a < 1 || g.b < 1) fail(kExitInfeasible, "infeasible: grid2d: dimensions must be positive");
+    } else if (kind == "stencil3d") {
+        g.a = dim(0), g.b = dim(1), g.c = dim(2);
+        if (g.a < 1 || g.b < 1 || g.c < 1) fail(kExitInfeasible, "infeasible: stencil3d: dimensions must be positive");
+        if (stencil != 7 && stencil != 27) fail(kExitInfeasible, "infeasible: stencil3d: stencil must be 7 or 27");
     } else if (kind == "ring") {
-        const int64_t n = dim(0);
-        if (n < 3) fail(kExitInfeasible, "infeasible: ring: need n >= 3");
-        write_lower(out, n, n, [&](int64_t i, std::vector<int64_t>& nb) {
-            if (i == n - 1) nb.push_back(0);
-            if (i > 0) nb.push_back(i - 1);
-        });
+        g.a = dim(0);
+        if (g.a < 3) fail(kExitInfeasible, "infeasible: ring: need n >= 3");
     } else if (kind == "path") {
-        const int64_t n = dim(0);
-        if (n < 1) fail(kExitInfeasible, "infeasible: path: need n >= 1");
-        write_lower(out, n, n - 1, [&](int64_t i, std::vector<int64_t>& nb) {
-            if (i > 0) nb.push_back(i - 1);
-        });
+        g.a = dim(0);
+        if (g.a < 1) fail(kExitInfeasible, "infeasible: path: need n >= 1");
     } else if (kind == "randomregular" || kind == "scalefree") {
         fail(1, "error: gen: '" + kind + "' is not provided by this build (seeded host generators, "
-                "generators.cpp:176-300, are outside the B200 hot path)");
+                "generators.cpp:176-280, are outside the B200 hot path)");
     } else {
         fail(kExitInfeasible, "infeasible: gen: unknown kind '" + kind + "'");
     }
+    return g;
+}
+
+// write_matrix_market_pattern_symmetric (sparse.cpp:179-191): the lower triangle, row order
+int run_gen(const MeshGen& g, std::ostream& out) {
+    const int64_t n = g.n();
+    std::vector<int64_t> nb;
+    int64_t lower = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        nb.clear();
+        g.nbrs(i, nb);
+        for (int64_t j : nb) lower += j < i;
+    }
+    std::string buf = "%%MatrixMarket matrix coordinate pattern symmetric\n" + std::to_string(n) + ' ' +
+                      std::to_string(n) + ' ' + std::to_string(lower) + '\n';
+    char line[48];
+    for (int64_t i = 0; i < n; ++i) {
+        nb.clear();
+        g.nbrs(i, nb);
+        for (int64_t j : nb)
+            if (j < i) buf.append(line, static_cast<size_t>(std::snprintf(line, sizeof line, "%lld %lld\n",
+                                                                           static_cast<long long>(i + 1),
+                                                                           static_cast<long long>(j + 1))));
+    }
+    out << buf;
+    return 0;
+}
+
+// ---- sweep (tools/specpart.cpp:265-327, run_sweep + SweepTable::to_tsv, generators.cpp:283-315)
+// GeneratorSpec::parse (generators.cpp:64-105) of "kind:a,b[,c][,p7|p27]"
+MeshGen parse_spec(const std::string& text) {
+    const size_t colon = text.find(':');
+    const std::string head = text.substr(0, colon);
+    std::vector<std::string> args;
+    if (colon != std::string::npos) {
+        std::istringstream rest(text.substr(colon + 1));
+        std::string tok;
+        while (std::getline(rest, tok, ',')) args.push_back(tok);
+    }
+    std::vector<int64_t> dims;
+    int stencil = 27;
+    const size_t need = head == "grid2d" ? 2 : head == "stencil3d" ? 3 : 1;
+    for (size_t i = 0; i < args.size(); ++i) {
+        if (i < need) dims.push_back(std::stoll(args[i]));
+        else if (args[i] == "p7") stencil = 7;
+        else if (args[i] == "p27") stencil = 27;
+    }
+    if (dims.size() < need) fail(1, "error: generator spec '" + text + "': missing argument");
+    return make_gen(head, dims, stencil);
+}
+
+struct SweepArgs {
+    std::vector<std::string> graphs, preconds, problems;
+    std::vector<double> tols;
+    int64_t parts = 8;
+    uint64_t seed = 42;
+    int max_iters = 1000;
+};
+
+int run_sweep(const SweepArgs& s) {
+    auto precond_of = [](const std::string& v) {
+        if (v == "jacobi") return SP_PRECOND_JACOBI;
+        if (v == "polynomial") return SP_PRECOND_POLYNOMIAL;
+        if (v == "amg") return SP_PRECOND_AMG;
+        if (v == "none") return SP_PRECOND_NONE;
+        fail(kExitInfeasible, "infeasible: sweep: unknown preconditioner '" + v + "'");
+    };
+    auto problem_of = [](const std::string& v) {
+        if (v == "combinatorial") return SP_PROBLEM_COMBINATORIAL;
+        if (v == "generalized") return SP_PROBLEM_GENERALIZED;
+        if (v == "normalized") return SP_PROBLEM_NORMALIZED;
+        fail(kExitInfeasible, "infeasible: sweep: unknown problem '" + v + "'");
+    };
+    struct Csr {
+        std::string name;
+        std::vector<int64_t> off;
+        std::vector<int32_t> col;
+    };
+    std::vector<Csr> graphs;
+    for (const std::string& spec : s.graphs) {
+        const MeshGen g = parse_spec(spec);
+        Csr c;
+        c.name = spec;
+        c.off.push_back(0);
+        std::vector<int64_t> nb;
+        for (int64_t i = 0; i < g.n(); ++i) {
+            nb.clear();
+            g.nbrs(i, nb);
+            for (int64_t j : nb) c.col.push_back(static_cast<int32_t>(j));
+            c.off.push_back(static_cast<int64_t>(c.col.size()));
+        }
+        graphs.push_back(std::move(c));
+    }
+    struct Cfg {
+        std::string label;
+        sp_config c;
+    };
+    std::vector<Cfg> cfgs;
+    const std::vector<std::string> preconds = s.preconds.empty() ? std::vector<std::string>{"jacobi"} : s.preconds;
+    const std::vector<std::string> problems = s.problems.empty() ? std::vector<std::string>{"auto"} : s.problems;
+    const std::vector<double> tols = s.tols.empty() ? std::vector<double>{0.0} : s.tols;
+    for (const std::string& pc : preconds)
+        for (const std::string& pr : problems)
+            for (double t : tols) {
+                sp_config c{};
+                c.num_parts = s.parts;
+                c.seed = s.seed;
+                c.max_iters = s.max_iters;
+                c.epsilon = 0.01;
+                c.precond = precond_of(pc);
+                c.problem = pr != "auto" ? problem_of(pr) : SP_PROBLEM_AUTO;
+                c.init = SP_INIT_AUTO;
+                c.tol = t > 0.0 ? t : -1.0;
+                cfgs.push_back({pc + "/" + pr + "/tol=" + (t > 0.0 ? std::to_string(t) : "auto"), c});
+            }
+    sp_context* ctx = nullptr;
+    if (sp_context_create(0, &ctx) != SP_OK) fail(1, "error: cannot create the CUDA context");
+    std::ostringstream os;
+    os << "graph\tconfig\titerations\tcut\timbalance\tseconds\terror\n";
+    for (const Csr& g : graphs) {
+        const int64_t n = static_cast<int64_t>(g.off.size()) - 1;
+        const sp_graph sg{n, g.off.data(), g.col.data(), nullptr, nullptr};
+        std::vector<int32_t> asg(static_cast<size_t>(n));
+        for (const Cfg& c : cfgs) {
+            std::vector<double> pw(static_cast<size_t>(std::max<int64_t>(c.c.num_parts, 1)));
+            sp_report rep{};
+            rep.part_weights = pw.data();
+            const sp_status st = sp_partition(ctx, &sg, &c.c, asg.data(), &rep, nullptr);
+            int iters = 0;
+            double cut = 0.0, imb = 0.0, secs = 0.0;
+            std::string err;
+            if (st == SP_OK) iters = rep.iterations, cut = rep.cutsize, imb = rep.imbalance, secs = rep.total_s;
+            else err = sp_last_error(ctx) ? sp_last_error(ctx) : "error";
+            os << g.name << '\t' << c.label << '\t' << iters << '\t' << cut << '\t' << imb << '\t' << secs << '\t'
+               << err << '\n';
+        }
+    }
+    sp_context_destroy(ctx);
+    std::cout << os.str();
     return 0;
 }
 
@@ -504,7 +638,9 @@ void usage() {
                  "  --report FILE       write a JSON run report\n"
                  "  --init-file FILE    dense initial block: 'rows cols' header, row-major values\n"
                  "Subcommands:\n"
-                 "  gen KIND DIMS... [--stencil 7|27] [--seed S] [--out FILE]   grid2d|stencil3d|ring|path\n";
+                 "  gen KIND DIMS... [--stencil 7|27] [--seed S] [--out FILE]   grid2d|stencil3d|ring|path\n"
+                 "  sweep --gen SPEC... [--parts K] [--tolerances T...] [--preconds P...] [--problems P...]\n"
+                 "        [--seed S] [--max-iters N]   TSV table (graph, config, iterations, cut, imbalance, s)\n";
 }
 
 int main_impl(int argc, char** argv) {
@@ -523,11 +659,35 @@ int main_impl(int argc, char** argv) {
             else dims.push_back(num<int64_t>(argv[i], "dims"));
         }
         if (kind.empty() || dims.empty()) fail(kCliRequired, "gen: kind and dims are required");
+        const MeshGen g = make_gen(kind, dims, stencil);
         if (!out.empty()) {
             std::ofstream f(out);
-            return run_gen(kind, dims, stencil, f);
+            return run_gen(g, f);
         }
-        return run_gen(kind, dims, stencil, std::cout);
+        return run_gen(g, std::cout);
+    }
+    if (argc > 1 && std::strcmp(argv[1], "sweep") == 0) {
+        SweepArgs s;
+        std::string v;
+        // CLI11 vector options: values follow the flag until the next option
+        auto many = [&](int& k, std::vector<std::string>& dst) {
+            while (k + 1 < argc && std::strncmp(argv[k + 1], "--", 2) != 0) dst.push_back(argv[++k]);
+        };
+        for (i = 2; i < argc; ++i) {
+            std::vector<std::string> tmp;
+            if (!std::strcmp(argv[i], "--gen")) many(i, s.graphs);
+            else if (!std::strcmp(argv[i], "--preconds")) many(i, s.preconds);
+            else if (!std::strcmp(argv[i], "--problems")) many(i, s.problems);
+            else if (!std::strcmp(argv[i], "--tolerances")) {
+                many(i, tmp);
+                for (const std::string& t : tmp) s.tols.push_back(num<double>(t, "--tolerances"));
+            } else if (take(argc, argv, i, "--parts", v)) s.parts = num<int64_t>(v, "--parts");
+            else if (take(argc, argv, i, "--seed", v)) s.seed = num<uint64_t>(v, "--seed");
+            else if (take(argc, argv, i, "--max-iters", v)) s.max_iters = num<int>(v, "--max-iters");
+            else fail(kCliExtras, std::string("The following argument was not expected: ") + argv[i]);
+        }
+        if (s.graphs.empty()) fail(kCliRequired, "--gen is required");
+        return run_sweep(s);
     }
     for (; i < argc; ++i) {
         std::string v;
