@@ -147,6 +147,10 @@ typedef struct sp_report {
     int64_t halo_launches;
     double halo_bytes;
     double halo_ms;
+    /* spmm_bytes / poly_bytes count each operator in its own stored format (pattern ELL:
+     * 1 B/row); these count the same launches as pattern CSR (4 B/nnz + offsets) */
+    double spmm_eff_bytes;
+    double poly_eff_bytes;
     /* caller-provided outputs (may be NULL) */
     double* part_weights;          /* num_parts */
     sp_trace_record* trace;        /* trace_capacity records */

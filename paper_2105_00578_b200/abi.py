@@ -101,6 +101,7 @@ class SpReport(C.Structure):
                 ("kernel_launches", C.c_int32), ("n_gpus", C.c_int32),
                 ("poly_launches", C.c_int64), ("poly_bytes", C.c_double), ("poly_ms", C.c_double),
                 ("halo_launches", C.c_int64), ("halo_bytes", C.c_double), ("halo_ms", C.c_double),
+                ("spmm_eff_bytes", C.c_double), ("poly_eff_bytes", C.c_double),
                 ("part_weights", C.POINTER(C.c_double)), ("trace", C.POINTER(SpTraceRecord)),
                 ("trace_capacity", C.c_int32), ("trace_len", C.c_int32)]
 

@@ -215,7 +215,8 @@ def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> 
         device={"spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
                 "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus,
                 "poly_launches": r.poly_launches, "poly_bytes": r.poly_bytes, "poly_ms": r.poly_ms,
-                "halo_launches": r.halo_launches, "halo_bytes": r.halo_bytes, "halo_ms": r.halo_ms})
+                "halo_launches": r.halo_launches, "halo_bytes": r.halo_bytes, "halo_ms": r.halo_ms,
+                "spmm_eff_bytes": r.spmm_eff_bytes, "poly_eff_bytes": r.poly_eff_bytes})
 
 
 def _ptr(a):

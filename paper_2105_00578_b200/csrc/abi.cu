@@ -397,6 +397,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     R.halo_launches = ctx->timers.halo_launches;
     R.halo_bytes = ctx->timers.halo_bytes;
     R.halo_ms = ctx->timers.halo_ms;
+    R.spmm_eff_bytes = ctx->timers.spmm_eff_bytes;
+    R.poly_eff_bytes = ctx->timers.poly_eff_bytes;
     R.kernel_launches = static_cast<int32_t>(launch_counter() - launches0 + ctx->timers.kernel_launches);
     R.n_gpus = ctx->comm.world;
     if (rep) {

@@ -154,6 +154,9 @@ struct Timers {
     double halo_ms = 0.0;
     int64_t poly_launches = 0;
     double poly_bytes = 0.0;
+    // the same launches in pattern-CSR-equivalent bytes (4 B/nnz + offsets), "effective"
+    double spmm_eff_bytes = 0.0;
+    double poly_eff_bytes = 0.0;
 };
 
 // symm.cu: P2P fast paths; return false when not applicable (caller uses NCCL)

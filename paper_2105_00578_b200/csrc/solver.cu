@@ -256,18 +256,29 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     }
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;
-    // algorithmic bytes of this launch: index stream,
-    // offsets, X read once per referenced row, Y written once, epilogue blocks
+    // algorithmic bytes of this launch: the operator's own
+    // format (pattern ELL: one byte per row + the slot table; plain ELL: 4 B per slot
+    // + diagonal; CSR: index stream + offsets), X read once per referenced row, Y
+    // written once, epilogue blocks. `eff` counts the operator as pattern CSR
+    // (4 B/nnz + offsets) whatever the format: the "effective" figure.
     const double idx_b = A_.mode == OP_EXPLICIT ? 12.0 : (A_.mode == OP_DIAGONAL ? 0.0 : 4.0);
     const double nrows = static_cast<double>(A_.n);
-    double bytes = idx_b * static_cast<double>(A_.nnz) + (A_.mode == OP_DIAGONAL ? 8.0 : 8.0) * (nrows + 1) +
-                   8.0 * m * nrows /*X (own rows; halo counted by comm)*/ + 8.0 * m * nrows /*Y*/;
-    if (A_.mode == OP_NORMAL_UNIT) bytes += 8.0 * nrows;  // isd
-    if (ea.mode == EPI_RESIDUAL && ea.bdiag) bytes += 8.0 * nrows;
-    if (ea.mode == EPI_POLY && ea.h_terms) bytes += (ea.first ? 1.0 : 2.0) * 8.0 * m * nrows;
+    const double csr_b = idx_b * static_cast<double>(A_.nnz) + 8.0 * (nrows + 1);
+    double op_b = csr_b;
+    if (A_.ell_pat)
+        op_b = nrows + 4.0 * A_.ell_npat * (A_.ell_kl + A_.ell_ku) + 8.0 * A_.ell_npat;
+    else if (A_.ell)
+        op_b = 4.0 * (A_.ell_kl + A_.ell_ku) * nrows + 8.0 * nrows;
+    double vec_b = 8.0 * m * nrows /*X (own rows; halo counted by comm)*/ + 8.0 * m * nrows /*Y*/;
+    if (A_.mode == OP_NORMAL_UNIT) vec_b += 8.0 * nrows;  // isd
+    if (ea.mode == EPI_RESIDUAL && ea.bdiag) vec_b += 8.0 * nrows;
+    if (ea.mode == EPI_POLY && ea.h_terms) vec_b += (ea.first ? 1.0 : 2.0) * 8.0 * m * nrows;
+    const double bytes = op_b + vec_b, eff = csr_b + vec_b;
     ctx_->timers.spmm_bytes += bytes;
+    ctx_->timers.spmm_eff_bytes += eff;
     if (ea.mode == EPI_POLY) {
         ctx_->timers.poly_bytes += bytes;
+        ctx_->timers.poly_eff_bytes += eff;
         ctx_->timers.poly_launches += 1;
     }
     (void)rows;
