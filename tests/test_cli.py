@@ -132,8 +132,8 @@ def test_partition_matches_reference(tmp_path, case):
 
 @pytest.mark.gpu
 def test_sweep_matches_reference():
-    """`sweep` (tools/specpart.cpp:265-327): same rows and labels as the reference's table; per
-    cell the cut within 2% and the iteration count within 2 of the reference's."""
+    """`sweep` (tools/specpart.cpp:265-327): same rows and labels as the reference's table, and
+    per cell the reference's iterations, cut and imbalance (seconds differ)."""
     r = run("sweep", "--gen", "grid2d:16,16", "stencil3d:6,6,6,p7", "ring:40", "--parts", 4, "--preconds",
             "jacobi", "polynomial", "--problems", "auto", "normalized")
     assert r.returncode == 0, r.stderr
@@ -142,6 +142,6 @@ def test_sweep_matches_reference():
     assert mine[0] == ref[0] and len(mine) == len(ref)
     for a, b in zip(mine[1:], ref[1:]):
         assert a[:2] == b[:2] and a[6] == b[6] == ""
-        assert abs(int(a[2]) - int(b[2])) <= 2, (a, b)
-        assert float(a[3]) <= float(b[3]) * 1.02 and float(a[4]) <= max(float(b[4]), 1.01), (a, b)
+        # measured: the reference's iteration count, cut and imbalance in every cell
+        assert a[2:5] == b[2:5], (a, b)
         print("\t".join(a[:5]), "| ref", b[2], b[3])
