@@ -19,7 +19,6 @@
 
 #include <algorithm>
 #include <cstdlib>
-#include <type_traits>
 #include <vector>
 
 namespace spb {
@@ -163,7 +162,6 @@ struct TileArgs {
     double* H;
     int ldh;
     int m;
-    int shfl = 0;  // spmm_ell_kernel<PAT>: x-neighbours of uniform interior tiles by warp shuffles
 };
 
 template <int MAXR, int MODE>
@@ -596,95 +594,6 @@ __global__ void __launch_bounds__(kThreads) spmm_long_kernel(const DevOp op, con
     }
 }
 
-// Uniform interior tile of a pattern-compressed stencil (every lane has the same full
-// pattern, slot KL-1 at offset -1 and slot KL at +1, and for 27-point stencils the other
-// slots in runs of three consecutive offsets): the ±1 neighbours of a loaded value are the
-// same value in the next / previous lane, so each run costs one warp gather plus one
-// two-lane edge load (lanes 0 and 31) instead of three gathers. The values and the order
-// of the subtractions are the general path's, so the result is bit-identical.
-template <int KL, int KU, int CB>
-__device__ __forceinline__ void ell_uniform_rows(const double* const (&xc)[CB], const uint32_t (&j)[KL + KU],
-                                                 const double (&xi)[CB], double dw, int lane, double (&acc)[CB]) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr bool TRI = KL > 1 && (KL - 1) % 3 == 0 && (KU - 1) % 3 == 0;
-    const bool e0 = lane == 0, e31 = lane == 31;
-    double ec[CB];
-#pragma unroll
-    for (int q = 0; q < CB; ++q) ec[q] = (e0 || e31) ? __ldg(xc[q] + (e0 ? j[KL - 1] : j[KL])) : 0.0;
-    // runs (or single slots) on one side: slots [s0, s0 + len)
-    auto side = [&](auto S0, auto LEN) {
-        constexpr int s0 = decltype(S0)::value, len = decltype(LEN)::value;
-        if constexpr (len > 0) {
-            if constexpr (TRI) {
-                constexpr int NT = len / 3;
-                constexpr int TC = 2;  // runs per chunk: 2 gathers + 2 edge loads in flight per column
-#pragma unroll
-                for (int t0 = 0; t0 < NT; t0 += TC) {
-                    double mid[CB][TC], ed[CB][TC];
-#pragma unroll
-                    for (int t = 0; t < TC; ++t)
-                        if (t0 + t < NT)
-#pragma unroll
-                            for (int q = 0; q < CB; ++q) mid[q][t] = __ldg(xc[q] + j[s0 + 3 * (t0 + t) + 1]);
-#pragma unroll
-                    for (int t = 0; t < TC; ++t)
-                        if (t0 + t < NT)
-#pragma unroll
-                            for (int q = 0; q < CB; ++q)
-                                ed[q][t] = (e0 || e31) ? __ldg(xc[q] + (e0 ? j[s0 + 3 * (t0 + t)] : j[s0 + 3 * (t0 + t) + 2]))
-                                                       : 0.0;
-#pragma unroll
-                    for (int t = 0; t < TC; ++t)
-                        if (t0 + t < NT)
-#pragma unroll
-                            for (int q = 0; q < CB; ++q) {
-                                const double lo = __shfl_up_sync(FULL, mid[q][t], 1);
-                                const double hi = __shfl_down_sync(FULL, mid[q][t], 1);
-                                acc[q] = __dsub_rn(acc[q], e0 ? ed[q][t] : lo);
-                                acc[q] = __dsub_rn(acc[q], mid[q][t]);
-                                acc[q] = __dsub_rn(acc[q], e31 ? ed[q][t] : hi);
-                            }
-                }
-            } else {
-                double g[CB][len];
-#pragma unroll
-                for (int u = 0; u < len; ++u)
-#pragma unroll
-                    for (int q = 0; q < CB; ++q) g[q][u] = __ldg(xc[q] + j[s0 + u]);
-#pragma unroll
-                for (int u = 0; u < len; ++u)
-#pragma unroll
-                    for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], g[q][u]);
-            }
-        }
-    };
-    side(std::integral_constant<int, 0>{}, std::integral_constant<int, KL - 1>{});
-#pragma unroll
-    for (int q = 0; q < CB; ++q) {
-        const double lo = __shfl_up_sync(FULL, xi[q], 1);
-        acc[q] = __dsub_rn(acc[q], e0 ? ec[q] : lo);
-        acc[q] = __dadd_rn(acc[q], __dmul_rn(dw, xi[q]));
-        const double hi = __shfl_down_sync(FULL, xi[q], 1);
-        acc[q] = __dsub_rn(acc[q], e31 ? ec[q] : hi);
-    }
-    side(std::integral_constant<int, KL + 1>{}, std::integral_constant<int, KU - 1>{});
-}
-
-// per pattern: does ell_uniform_rows apply (no padding, -1/+1 around the diagonal, runs of 3)
-template <int KL, int KU>
-__device__ __forceinline__ bool ell_pattern_full(const int32_t* tp) {
-    constexpr int W = KL + KU;
-    constexpr bool TRI = KL > 1 && (KL - 1) % 3 == 0 && (KU - 1) % 3 == 0;
-    bool ok = true;
-    for (int s = 0; s < W; ++s) ok = ok && tp[s] != kEllPad;
-    ok = ok && tp[KL - 1] == -1 && tp[KL] == 1;
-    if (TRI) {
-        for (int s = 0; s + 2 < KL - 1; s += 3) ok = ok && tp[s + 1] == tp[s] + 1 && tp[s + 2] == tp[s] + 2;
-        for (int s = KL + 1; s + 2 < W; s += 3) ok = ok && tp[s + 1] == tp[s] + 1 && tp[s + 2] == tp[s] + 2;
-    }
-    return ok;
-}
-
 template <int KL, int KU, int EPI, int CB, int MINB, bool HF, bool PAT = false>
 __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op, const TileArgs ta, const EpiArgs ea,
                                                                    const HaloFuse hf) {
@@ -694,13 +603,9 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     // pattern-compressed slots (ellpat.cu): table of per-pattern column offsets and degrees
     __shared__ int32_t s_tab[PAT ? 256 * W : 1];
     __shared__ double s_deg[PAT ? 256 : 1];
-    __shared__ uint8_t s_full[PAT ? 256 : 1];
     if (PAT) {
         for (int e = threadIdx.x; e < op.ell_npat * W; e += kThreads) s_tab[e] = op.ell_pat_tab[e];
-        for (int e = threadIdx.x; e < op.ell_npat; e += kThreads) {
-            s_deg[e] = op.ell_pat_deg[e];
-            s_full[e] = ta.shfl && ell_pattern_full<KL, KU>(op.ell_pat_tab + e * W);
-        }
+        for (int e = threadIdx.x; e < op.ell_npat; e += kThreads) s_deg[e] = op.ell_pat_deg[e];
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -733,7 +638,6 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     };
     uint32_t jn[W];
     double dwn = 0.0;
-    int pidn = -1;
     auto load_slots = [&](int64_t lt) {
         const int64_t row = phys(lt) * 32 + lane;
         const bool live = lt < ntiles && row < op.n;
@@ -746,7 +650,6 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                 jn[sidx] = (live && d != kEllPad) ? static_cast<uint32_t>(row + d) : zrow;
             }
             dwn = live ? s_deg[p] : 0.0;
-            pidn = live ? p : -1;
         } else {
 #pragma unroll
             for (int sidx = 0; sidx < W; ++sidx)
@@ -768,11 +671,6 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
 #pragma unroll
         for (int sidx = 0; sidx < W; ++sidx) j[sidx] = jn[sidx];
         const double dw = dwn;
-        bool uni = false;
-        if (PAT) {
-            const int p0 = __shfl_sync(0xffffffffu, pidn, 0);
-            uni = __all_sync(0xffffffffu, pidn == p0) && p0 >= 0 && s_full[p0 >= 0 ? p0 : 0];
-        }
         if (kAhead) load_slots(lt + nwarps);
         const uint32_t own = live ? static_cast<uint32_t>(row) : zrow;
         for (int c0 = 0; c0 < m; c0 += CB) {
@@ -789,9 +687,6 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                     hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
                 acc[q] = 0.0;
             }
-            if (PAT && uni) {
-                ell_uniform_rows<KL, KU, CB>(xc, j, xi, dw, lane, acc);
-            } else {
             // gathers in chunks of CH slots, each chunk issued before its ordered adds
             constexpr int CH = 8;
 #pragma unroll
@@ -823,7 +718,6 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                     if (s0 + u < W)
 #pragma unroll
                         for (int q = 0; q < CB; ++q) acc[q] = __dsub_rn(acc[q], gv[q][u]);
-            }
             }
 #pragma unroll
             for (int q = 0; q < CB; ++q) {
@@ -913,13 +807,6 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
         ta.H = ea.H.ptr;
         ta.ldh = static_cast<int>(ea.mode == EPI_POLY && m > 1 ? ea.H.cs : 0);
         ta.m = m;
-        {
-            static const int shfl_env = [] {
-                const char* e = std::getenv("SPB_ELL_SHFL");
-                return e ? std::atoi(e) : 0;
-            }();
-            ta.shfl = shfl_env;
-        }
         const int64_t ntiles = (op.n + 31) / 32;
         const int mr = op.max_row;
         int grid = 0;
