@@ -20,7 +20,10 @@ CASES = json.loads((GOLD / "cases.json").read_text())
 
 def run(*args, **kw):
     if not CLI.exists():
-        pytest.fail("build/specpart_b200 missing: run __graft_entry__.build()")
+        from paper_2105_00578_b200 import build as B
+        if not B.LIB.exists():
+            pytest.fail("libspecpart_b200.so missing: run __graft_entry__.build()")
+        B._build_cli(False)  # host-only g++ link against the built library
     return subprocess.run([str(CLI), *map(str, args)], capture_output=True, text=True, timeout=600, **kw)
 
 
