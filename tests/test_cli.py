@@ -148,3 +148,34 @@ def test_sweep_matches_reference():
         # measured: the reference's iteration count, cut and imbalance in every cell
         assert a[2:5] == b[2:5], (a, b)
         print("\t".join(a[:5]), "| ref", b[2], b[3])
+
+
+@pytest.mark.gpu
+def test_init_file_and_trace(tmp_path):
+    """--init-file warm start (tools/specpart.cpp:94-157): row/column checks with exit 4, the
+    "initial vectors loaded from" warning, resolved init "random"; --trace adds solver.trace."""
+    import numpy as np
+    mtx = GOLD / "grid32.mtx"
+    n, d = 32 * 32, 3  # K = 4 -> d = bit_width(4) = 3
+    X0 = np.random.default_rng(5).uniform(-1, 1, (n, d))
+    init = tmp_path / "x0.txt"
+    init.write_text(f"{n} {d}\n" + "\n".join(" ".join(f"{v:.17g}" for v in row) for row in X0) + "\n")
+    rep = tmp_path / "r.json"
+    r = run("--input", mtx, "--parts", 4, "--precond", "jacobi", "--problem", "combinatorial",
+            "--init-file", init, "--trace", "--report", rep, "--output", tmp_path / "p.txt")
+    assert r.returncode == 0, r.stderr
+    j = json.loads(rep.read_text())
+    assert j["warnings"] == [f"initial vectors loaded from {init}"]
+    assert j["config"]["initial_vectors"] == "random"
+    assert all(j["solver"]["converged"]) and j["partition"]["cutsize"] <= 76 * 1.1
+    tr = j["solver"]["trace"]
+    assert len(tr) >= j["solver"]["iterations"] and all(len(t["theta"]) == d for t in tr)
+    bad = tmp_path / "bad.txt"
+    bad.write_text(f"{n - 1} {d}\n" + "0 " * ((n - 1) * d) + "\n")
+    r = run("--input", mtx, "--parts", 4, "--precond", "jacobi", "--init-file", bad)
+    assert r.returncode == 4 and f"initial block has {n - 1} rows but the graph has {n} vertices" in r.stderr
+    bad.write_text(f"{n} 2\n" + "0 " * (n * 2) + "\n")
+    r = run("--input", mtx, "--parts", 4, "--precond", "jacobi", "--init-file", bad)
+    assert r.returncode == 4 and "initial block must have d=3 columns" in r.stderr
+    bad.write_text(f"{n} {d}\n1 2\n")
+    assert run("--input", mtx, "--parts", 4, "--precond", "jacobi", "--init-file", bad).returncode == 2
