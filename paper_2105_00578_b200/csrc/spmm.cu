@@ -867,8 +867,11 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             case 303: SPB_ELL(3, 3); break;
             case 404: SPB_ELL(4, 4); break;
             case 1313:
-                if (pat) go(hf ? spmm_ell_kernel<13, 13, EPI, 1, 4, true, true>
-                               : spmm_ell_kernel<13, 13, EPI, 1, 4, false, true>, 0);
+                // cfg4 A/B (profiles/r01_cfg4_pat_variants.json): 3 CTAs/SM (80 registers)
+                // 1.318 ms/launch, 4 CTAs/SM (64) 1.348, two columns per pass 1.765
+                if (pat && !hf && evariant == 3) go(spmm_ell_kernel<13, 13, EPI, 1, 4, false, true>, 0);
+                else if (pat && !hf) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false, true>, 0);
+                else if (pat) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true, true>, 0);
                 else if (hf) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true>, 0);
                 else if (evariant == 1) go(spmm_ell_kernel<13, 13, EPI, 2, 2, false>, 0);
                 else if (evariant == 2) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false>, 0);
