@@ -2,7 +2,7 @@
 // (tools/specpart.cpp:62-196, 237-263) without CLI11 (absent here), linked against the
 // unmodified reference objects in oracle/_ref. Used by tests/golden/make_cli_golden.py to record
 // the partition files, reports and .mtx outputs the B200 CLI must reproduce.
-//   cli_ref gen KIND STENCIL DIMS...              -> .mtx on stdout
+//   cli_ref gen KIND STENCIL DIMS... [SEED]       -> .mtx on stdout (SEED: randomregular/scalefree)
 //   cli_ref part MTX K PROBLEM PRECOND SEED OUT REPORT
 //   cli_ref sweep K SEED SPEC,SPEC PRECOND,PRECOND PROBLEM,PROBLEM   (tools/specpart.cpp:265-327)
 #include "specpart/generators.hpp"
@@ -31,6 +31,8 @@ int main(int argc, char** argv) {
         else if (kind == "stencil3d") spec = GeneratorSpec::stencil3d(d[0], d[1], d[2], stencil);
         else if (kind == "ring") spec.kind = GeneratorSpec::Kind::Ring, spec.a = d[0];
         else if (kind == "path") spec.kind = GeneratorSpec::Kind::Path, spec.a = d[0];
+        else if (kind == "randomregular") spec = GeneratorSpec::random_regular(d[0], d[1], static_cast<std::uint64_t>(d[2]));
+        else if (kind == "scalefree") spec = GeneratorSpec::scale_free(d[0], d[1], static_cast<std::uint64_t>(d[2]));
         else return 1;
         write_matrix_market_pattern_symmetric(std::cout, generate(spec).adjacency);
         return 0;

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <fstream>
 #include <iostream>
+#include <random>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -238,11 +239,14 @@ struct MeshGen {
     std::string kind;
     int64_t a = 0, b = 0, c = 0;
     int stencil = 27;
+    std::vector<std::vector<int64_t>> adj;  // seeded random graphs: explicit sorted rows
     int64_t n() const {
         return kind == "grid2d" ? a * b : kind == "stencil3d" ? a * b * c : a;
     }
     void nbrs(int64_t i, std::vector<int64_t>& nb) const {
-        if (kind == "grid2d") {
+        if (!adj.empty()) {
+            nb.insert(nb.end(), adj[static_cast<size_t>(i)].begin(), adj[static_cast<size_t>(i)].end());
+        } else if (kind == "grid2d") {
             const int64_t x = i % a, y = i / a;
             if (y > 0) nb.push_back(i - a);
             if (x > 0) nb.push_back(i - 1);
@@ -270,8 +274,100 @@ struct MeshGen {
     }
 };
 
+// graph_from_edges (graph.cpp:66-81): both directions, self-loops dropped, rows sorted and unique
+std::vector<std::vector<int64_t>> rows_from_edges(int64_t n, const std::vector<std::pair<int32_t, int32_t>>& edges) {
+    std::vector<std::vector<int64_t>> adj(static_cast<size_t>(n));
+    for (const auto& [u, v] : edges)
+        if (u != v) {
+            adj[static_cast<size_t>(u)].push_back(v);
+            adj[static_cast<size_t>(v)].push_back(u);
+        }
+    for (auto& r : adj) {
+        std::sort(r.begin(), r.end());
+        r.erase(std::unique(r.begin(), r.end()), r.end());
+    }
+    return adj;
+}
+
+bool connected(const std::vector<std::vector<int64_t>>& adj) {
+    std::vector<char> seen(adj.size(), 0);
+    std::vector<int64_t> todo{0};
+    seen[0] = 1;
+    size_t count = 1;
+    while (!todo.empty()) {
+        const int64_t v = todo.back();
+        todo.pop_back();
+        for (int64_t u : adj[static_cast<size_t>(v)])
+            if (!seen[static_cast<size_t>(u)]) {
+                seen[static_cast<size_t>(u)] = 1;
+                ++count;
+                todo.push_back(u);
+            }
+    }
+    return count == adj.size();
+}
+
+// random_regular_graph (generators.cpp:201-234): configuration model on a std::mt19937_64
+// stream; a pairing with a self-loop or a repeated edge is redrawn (200 draws per stream),
+// a disconnected one too; the stream is reseeded (seed + attempt * golden ratio) after 200.
+std::vector<std::vector<int64_t>> random_regular_rows(int64_t n, int64_t deg, uint64_t seed) {
+    if (n < 2 || deg < 1 || deg >= n) fail(kExitInfeasible, "infeasible: randomregular: need 1 <= deg < n >= 2");
+    if ((n * deg) % 2 != 0) fail(kExitInfeasible, "infeasible: randomregular: n*deg must be even");
+    std::vector<int32_t> stubs(static_cast<size_t>(n * deg));
+    std::vector<std::pair<int32_t, int32_t>> pairs;
+    for (uint64_t attempt = 0;; ++attempt) {
+        std::mt19937_64 rng(seed + attempt * 0x9e3779b97f4a7c15ULL);
+        for (int draw = 0; draw < 200; ++draw) {
+            for (size_t k = 0; k < stubs.size(); ++k) stubs[k] = static_cast<int32_t>(k / static_cast<size_t>(deg));
+            std::shuffle(stubs.begin(), stubs.end(), rng);
+            pairs.clear();
+            bool loop = false;
+            for (size_t k = 0; k + 1 < stubs.size(); k += 2) {
+                if (stubs[k] == stubs[k + 1]) {
+                    loop = true;
+                    break;
+                }
+                pairs.emplace_back(std::min(stubs[k], stubs[k + 1]), std::max(stubs[k], stubs[k + 1]));
+            }
+            if (loop) continue;
+            std::sort(pairs.begin(), pairs.end());
+            if (std::adjacent_find(pairs.begin(), pairs.end()) != pairs.end()) continue;
+            auto adj = rows_from_edges(n, pairs);
+            if (connected(adj)) return adj;
+        }
+    }
+}
+
+// scale_free_graph (generators.cpp:238-266): a star on attach+1 vertices, then each new vertex
+// takes `attach` distinct targets drawn uniformly from the endpoint list (degree-proportional).
+std::vector<std::vector<int64_t>> scale_free_rows(int64_t n, int64_t attach, uint64_t seed) {
+    if (attach < 1 || n <= attach) fail(kExitInfeasible, "infeasible: scalefree: need n > attach >= 1");
+    std::mt19937_64 rng(seed);
+    std::vector<std::pair<int32_t, int32_t>> edges;
+    std::vector<int32_t> ends;
+    for (int64_t v = 1; v <= attach; ++v) {
+        edges.emplace_back(0, static_cast<int32_t>(v));
+        ends.push_back(0);
+        ends.push_back(static_cast<int32_t>(v));
+    }
+    std::vector<int32_t> chosen;
+    for (int64_t v = attach + 1; v < n; ++v) {
+        chosen.clear();
+        while (static_cast<int64_t>(chosen.size()) < attach) {
+            const int32_t t = ends[rng() % ends.size()];
+            if (std::find(chosen.begin(), chosen.end(), t) == chosen.end()) chosen.push_back(t);
+        }
+        for (int32_t t : chosen) {
+            edges.emplace_back(t, static_cast<int32_t>(v));
+            ends.push_back(t);
+            ends.push_back(static_cast<int32_t>(v));
+        }
+    }
+    return rows_from_edges(n, edges);
+}
+
 // generate() argument checks (generators.cpp:126-175)
-MeshGen make_gen(const std::string& kind, const std::vector<int64_t>& dims, int stencil) {
+MeshGen make_gen(const std::string& kind, const std::vector<int64_t>& dims, int stencil, uint64_t seed = 0) {
     auto dim = [&](size_t i) -> int64_t {
         if (i >= dims.size()) fail(kExitInfeasible, "infeasible: gen: missing dimension for " + kind);
         return dims[i];
@@ -292,9 +388,12 @@ MeshGen make_gen(const std::string& kind, const std::vector<int64_t>& dims, int 
     } else if (kind == "path") {
         g.a = dim(0);
         if (g.a < 1) fail(kExitInfeasible, "infeasible: path: need n >= 1");
-    } else if (kind == "randomregular" || kind == "scalefree") {
-        fail(1, "error: gen: '" + kind + "' is not provided by this build (seeded host generators, "
-                "generators.cpp:176-280, are outside the B200 hot path)");
+    } else if (kind == "randomregular") {
+        g.a = dim(0);
+        g.adj = random_regular_rows(g.a, dim(1), seed);
+    } else if (kind == "scalefree") {
+        g.a = dim(0);
+        g.adj = scale_free_rows(g.a, dim(1), seed);
     } else {
         fail(kExitInfeasible, "infeasible: gen: unknown kind '" + kind + "'");
     }
@@ -339,14 +438,16 @@ MeshGen parse_spec(const std::string& text) {
     }
     std::vector<int64_t> dims;
     int stencil = 27;
-    const size_t need = head == "grid2d" ? 2 : head == "stencil3d" ? 3 : 1;
+    uint64_t seed = 0;
+    const size_t need = head == "stencil3d" ? 3 : (head == "ring" || head == "path") ? 1 : 2;
     for (size_t i = 0; i < args.size(); ++i) {
         if (i < need) dims.push_back(std::stoll(args[i]));
         else if (args[i] == "p7") stencil = 7;
         else if (args[i] == "p27") stencil = 27;
+        else if (!args[i].empty() && args[i][0] == 's') seed = std::stoull(args[i].substr(1));
     }
     if (dims.size() < need) fail(1, "error: generator spec '" + text + "': missing argument");
-    return make_gen(head, dims, stencil);
+    return make_gen(head, dims, stencil, seed);
 }
 
 struct SweepArgs {
@@ -638,7 +739,8 @@ void usage() {
                  "  --report FILE       write a JSON run report\n"
                  "  --init-file FILE    dense initial block: 'rows cols' header, row-major values\n"
                  "Subcommands:\n"
-                 "  gen KIND DIMS... [--stencil 7|27] [--seed S] [--out FILE]   grid2d|stencil3d|ring|path\n"
+                 "  gen KIND DIMS... [--stencil 7|27] [--seed S] [--out FILE]\n"
+                 "        grid2d W H | stencil3d X Y Z | ring N | path N | randomregular N DEG | scalefree N ATTACH\n"
                  "  sweep --gen SPEC... [--parts K] [--tolerances T...] [--preconds P...] [--problems P...]\n"
                  "        [--seed S] [--max-iters N]   TSV table (graph, config, iterations, cut, imbalance, s)\n";
 }
@@ -650,16 +752,17 @@ int main_impl(int argc, char** argv) {
         std::string kind, out, v;
         std::vector<int64_t> dims;
         int stencil = 27;
+        uint64_t gseed = 0;
         for (i = 2; i < argc; ++i) {
             if (take(argc, argv, i, "--stencil", v)) stencil = num<int>(v, "--stencil");
-            else if (take(argc, argv, i, "--seed", v)) (void)num<uint64_t>(v, "--seed");
+            else if (take(argc, argv, i, "--seed", v)) gseed = num<uint64_t>(v, "--seed");
             else if (take(argc, argv, i, "--out", out)) {
             } else if (argv[i][0] == '-' && argv[i][1] == '-') fail(kCliExtras, std::string("The following argument was not expected: ") + argv[i]);
             else if (kind.empty()) kind = argv[i];
             else dims.push_back(num<int64_t>(argv[i], "dims"));
         }
         if (kind.empty() || dims.empty()) fail(kCliRequired, "gen: kind and dims are required");
-        const MeshGen g = make_gen(kind, dims, stencil);
+        const MeshGen g = make_gen(kind, dims, stencil, gseed);
         if (!out.empty()) {
             std::ofstream f(out);
             return run_gen(g, f);

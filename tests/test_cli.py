@@ -31,6 +31,8 @@ def run(*args, **kw):
     ("grid32", ["grid2d", 32, 32]),
     ("stencil7_12", ["stencil3d", 12, 12, 12, "--stencil", 7]),
     ("ring64", ["ring", 64]),
+    ("rr200_3_s7", ["randomregular", 200, 3, "--seed", 7]),
+    ("sf300_2_s5", ["scalefree", 300, 2, "--seed", 5]),
 ])
 def test_gen_matches_reference(name, args):
     r = run("gen", *args)
