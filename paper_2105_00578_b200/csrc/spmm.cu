@@ -786,11 +786,18 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
 
 // PAT instantiations exist only for the pattern-compressed stencil classes
 template <int KL, int KU, int EPI>
-auto pat_ell_kernel(bool hf) -> decltype(&spmm_ell_kernel<KL, KU, EPI, 2, 4, false>) {
-    if constexpr (KL == KU && (KL == 2 || KL == 3))
-        return hf ? &spmm_ell_kernel<KL, KU, EPI, 2, 4, true, true> : &spmm_ell_kernel<KL, KU, EPI, 2, 4, false, true>;
-    else
+auto pat_ell_kernel(bool hf, int v = 0) -> decltype(&spmm_ell_kernel<KL, KU, EPI, 2, 4, false>) {
+    if constexpr (KL == KU && (KL == 2 || KL == 3)) {
+        if (hf) return &spmm_ell_kernel<KL, KU, EPI, 2, 4, true, true>;
+        switch (v) {  // SPB_ELL_VARIANT: columns per pass / CTAs per SM
+        case 1: return &spmm_ell_kernel<KL, KU, EPI, 2, 5, false, true>;
+        case 2: return &spmm_ell_kernel<KL, KU, EPI, 1, 6, false, true>;
+        case 3: return &spmm_ell_kernel<KL, KU, EPI, 4, 3, false, true>;
+        default: return &spmm_ell_kernel<KL, KU, EPI, 2, 4, false, true>;
+        }
+    } else {
         return nullptr;
+    }
 }
 
 template <int MODE, int EPI>
@@ -855,7 +862,7 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
         else if (wide) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 8, 1, true>                                   \
                              : spmm_ell_kernel<KL_, KU_, EPI, 8, 1, false>, 0);                             \
         else if (pat && pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr) != nullptr)                            \
-            go(pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr), 0);                                           \
+            go(pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr, evariant), 0);                                 \
         else if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                     \
         else if (evariant == 1) go(spmm_ell_kernel<KL_, KU_, EPI, 1, 6, false>, 0);                         \
         else if (evariant == 2) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 5, false>, 0);                         \
