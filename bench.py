@@ -12,10 +12,12 @@ partition over NCCL).
           D2H inside the timed region
   roofline : SpMM (the dominant kernel) algorithmic bytes / CUDA-event time of
           every SpMM launch inside the timed resident steps
-  cpu_baseline : the compiled reference (oracle/_ref) on this host, bounded sample
+  cpu_baseline : the compiled reference (oracle/_ref) on this host: 3 full
+          partition_graph runs (min / median), OMP_WAIT_POLICY=active, at the best
+          thread count of the committed sweep (scripts/cpu_thread_sweep.py)
 
 `--impl reference` times the reference's own CPU implementation instead (rank 0
-only), one bounded sample per step.
+only): every timed step is one full partition_graph of the same workload.
 """
 from __future__ import annotations
 
@@ -36,27 +38,22 @@ METRIC = "time-to-partition (s) + edge cut/imbalance at 1/2/4/8 B200; SpMM HBM G
 
 CONFIGS = {
     "cfg1": dict(desc="2D 5-point grid 256x256, K=4, combinatorial, Jacobi", gen=("grid2d", 256, 256),
-                 K=4, problem="combinatorial", precond="jacobi", ref_iters=448),
+                 K=4, problem="combinatorial", precond="jacobi"),
     "cfg2": dict(desc="3D 7-point mesh 128^3, K=64, combinatorial, GMRES polynomial (degree 25)",
-                 gen=("stencil3d", 128, 128, 128, 7), K=64, problem="combinatorial", precond="polynomial",
-                 ref_iters=18),
+                 gen=("stencil3d", 128, 128, 128, 7), K=64, problem="combinatorial", precond="polynomial"),
     "cfg3": dict(desc="R-MAT scale 22 ef16 (LCC), K=64, normalized, Jacobi", gen=("rmat", 22, 16, 1),
-                 K=64, problem="normalized", precond="jacobi", ref_iters=20),
+                 K=64, problem="normalized", precond="jacobi"),
     "cfg4": dict(desc="3D 27-point Brick mesh 256^3, K=256, generalized, GMRES polynomial",
-                 gen=("stencil3d", 256, 256, 256, 27), K=256, problem="generalized", precond="polynomial",
-                 ref_iters=12),
+                 gen=("stencil3d", 256, 256, 256, 27), K=256, problem="generalized", precond="polynomial"),
     # diagnostics: the per-GPU row block of cfg2 at 4 and 8 GPUs, on one GPU
     "cfg2q": dict(desc="3D 7-point mesh 128x128x32 (cfg2 / 4), K=64, combinatorial, GMRES polynomial",
-                  gen=("stencil3d", 128, 128, 32, 7), K=64, problem="combinatorial", precond="polynomial",
-                  ref_iters=18),
+                  gen=("stencil3d", 128, 128, 32, 7), K=64, problem="combinatorial", precond="polynomial"),
     "cfg2h": dict(desc="3D 7-point mesh 128x128x64 (cfg2 / 2), K=64, combinatorial, GMRES polynomial",
-                  gen=("stencil3d", 128, 128, 64, 7), K=64, problem="combinatorial", precond="polynomial",
-                  ref_iters=18),
+                  gen=("stencil3d", 128, 128, 64, 7), K=64, problem="combinatorial", precond="polynomial"),
     "cfg2e": dict(desc="3D 7-point mesh 128x128x16 (cfg2 / 8), K=64, combinatorial, GMRES polynomial",
-                  gen=("stencil3d", 128, 128, 16, 7), K=64, problem="combinatorial", precond="polynomial",
-                  ref_iters=18),
+                  gen=("stencil3d", 128, 128, 16, 7), K=64, problem="combinatorial", precond="polynomial"),
     "cfg5": dict(desc="R-MAT scale 24 ef16 (LCC), K=256, normalized, Jacobi", gen=("rmat", 24, 16, 1),
-                 K=256, problem="normalized", precond="jacobi", ref_iters=20),
+                 K=256, problem="normalized", precond="jacobi"),
 }
 
 
@@ -165,30 +162,37 @@ def traffic_from_profiles(cfg_name):
 
 
 # ------------------------------------------------------------ CPU baseline ----
+SWEEP = ROOT / "profiles" / "cpu_thread_sweep.json"
+
+
 def cpu_sample_main(args):
-    """Runs in a subprocess: the reference pipeline with max_iters in {1, 3, 2...}."""
+    """Runs in a subprocess (OMP_NUM_THREADS fixed before libgomp loads): the
+    reference's partition_graph, full runs (max_iters 1000) unless asked otherwise."""
     from oracle.ref import RefLib
     c = CONFIGS[args.config]
     g = make_graph(c["gen"])
     ref = RefLib()
-    out = {"kind": ref.kind, "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))}
-    times = {}
-    for mi in args.cpu_iters:
+    out = {"kind": ref.kind, "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "runs": []}
+    for k in range(args.cpu_warmup + args.cpu_runs):
+        mi = 1 if k < args.cpu_warmup else args.cpu_max_iters
         t0 = time.perf_counter()
         r = ref.partition_graph(g, run_config(c, max_iters=mi))
-        times[mi] = {"wall": time.perf_counter() - t0, "total_s": r.report.times["total_s"],
-                     "iterations": r.report.iterations, "cut": r.report.cutsize}
-    out["times"] = times
+        wall = time.perf_counter() - t0
+        if k >= args.cpu_warmup:
+            out["runs"].append({"wall": wall, "total_s": r.report.times["total_s"], "times": r.report.times,
+                                "iterations": r.report.iterations, "cut": r.report.cutsize,
+                                "imbalance": r.report.imbalance})
+            print("CPU_RUN " + json.dumps(out["runs"][-1]), flush=True)
     print("CPU_SAMPLE " + json.dumps(out), flush=True)
 
 
-def cpu_sample(config, iters, timeout=900):
+def cpu_sample(config, runs, threads, max_iters=1000, warmup=0, timeout=3600):
     env = dict(os.environ)
-    env.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    env["OMP_NUM_THREADS"] = str(threads)
     env.setdefault("OMP_WAIT_POLICY", "active")
     env["OMP_PROC_BIND"] = env.get("OMP_PROC_BIND", "false")
     cmd = [sys.executable, str(Path(__file__).resolve()), "--cpu-sample", "--config", config,
-           "--cpu-iters", *map(str, iters)]
+           "--cpu-runs", str(runs), "--cpu-max-iters", str(max_iters), "--cpu-warmup", str(warmup)]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
     for ln in r.stdout.splitlines():
         if ln.startswith("CPU_SAMPLE "):
@@ -196,12 +200,24 @@ def cpu_sample(config, iters, timeout=900):
     raise RuntimeError(f"cpu sample failed: {r.stderr[-2000:]}")
 
 
-def extrapolate(sample, ref_iters):
-    """time(full) = T(1) + (ref_iters - 1) * t_iter, t_iter = (T(3) - T(1)) / 2."""
-    t = sample["times"]
-    t1, t3 = t["1"]["total_s"], t["3"]["total_s"]
-    t_iter = max(0.0, (t3 - t1) / 2.0)
-    return t1 + (ref_iters - 1) * t_iter, t_iter, t1 - t_iter
+def best_threads():
+    """Thread count for the reference: the best of the committed OMP_NUM_THREADS sweep
+    (scripts/cpu_thread_sweep.py) when it was taken on a host with this core count,
+    else every core."""
+    nproc = os.cpu_count() or 1
+    try:
+        sw = json.loads(SWEEP.read_text())
+        if int(sw.get("nproc", -1)) == nproc and sw.get("best_threads"):
+            return int(sw["best_threads"]), sw
+    except (OSError, ValueError):
+        pass
+    return nproc, None
+
+
+def summarize_runs(s):
+    t = [r["total_s"] for r in s["runs"]]
+    return {"min": round(min(t), 3), "median": round(statistics.median(t), 3), "mean": round(statistics.mean(t), 3),
+            "runs_s": [round(x, 3) for x in t]}
 
 
 # ------------------------------------------------------------------ main ------
@@ -214,7 +230,9 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, nargs="*", default=[1, 3])
+    ap.add_argument("--cpu-runs", type=int, default=3)
+    ap.add_argument("--cpu-max-iters", type=int, default=1000)
+    ap.add_argument("--cpu-warmup", type=int, default=0)
     args = ap.parse_args()
     if args.cpu_sample:
         return cpu_sample_main(args)
@@ -324,9 +342,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(value * 1e3, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: " + c["desc"] + " (reference generator semantics, unit weights)",
-        "config": {"workload": f"{args.config}: {c['desc']}", "n": g.n, "nnz_A": int(g.row_offsets[-1]),
-                   "K": c["K"], "seed": 42, "parallelism": f"rows1d x{world}" if world > 1 else "single",
-                   "l2": "flushed between steps (256 MiB write)"},
+        "config": config_dict(args, c, g, world),
         "e2e": {"value": round(e2e, 6), "unit": "s", "h2d_bytes_per_step": int(h2d_bytes),
                 "d2h_bytes_per_step": int(d2h_bytes)},
         "roofline": {"kernel": kname, "bound": "hbm",
@@ -359,13 +375,18 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = cpu_sample(args.config, [1, 3])
-            full, t_iter, setup = extrapolate(s, c["ref_iters"])
+            thr, sw = best_threads()
+            s = cpu_sample(args.config, 3, thr)
+            st = summarize_runs(s)
             line["cpu_baseline"] = {
-                "value": round(full, 3), "unit": "s", "cores": s["cores"], "kind": s["kind"],
-                "sample": (f"reference partition_graph with max_iters=1 and 3 on this host "
-                           f"(setup {setup:.2f} s, {t_iter:.2f} s/iter), extrapolated to the reference's "
-                           f"{c['ref_iters']} iterations (SURVEY §6, seed 42)")}
+                "value": st["median"], "unit": "s", "cores": s["cores"], "kind": s["kind"],
+                "min": st["min"], "median": st["median"], "runs_s": st["runs_s"],
+                "iterations": s["runs"][-1]["iterations"], "cut": s["runs"][-1]["cut"],
+                "imbalance": s["runs"][-1]["imbalance"],
+                "threads_from": "profiles/cpu_thread_sweep.json" if sw else "all cores (no sweep for this host)",
+                "sample": (f"3 full runs of the reference partition_graph (oracle/_ref, max_iters 1000, "
+                           f"OMP_WAIT_POLICY=active, {s['cores']} of {os.cpu_count()} host threads) on this "
+                           f"workload; value = median")}
         except Exception as e:  # noqa: BLE001 - reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(e)[:300]}
     if rank == 0:
@@ -377,27 +398,41 @@ def main():
 
 
 def reference_arm(args, c, rank, world):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    /root/reference/proj/src compiled in-tree) timed on this host: every timed step
+    is one full partition_graph (max_iters 1000) of the workload; warm-up steps run
+    max_iters=1 (untimed). Rank 0 only."""
     if rank != 0:
         return
-    s = cpu_sample(args.config, [1, 3])
-    full, t_iter, setup = extrapolate(s, c["ref_iters"])
-    vals = []
-    for _ in range(args.steps):
-        s2 = cpu_sample(args.config, [2])
-        t2 = s2["times"]["2"]["total_s"]
-        vals.append(t2 + (c["ref_iters"] - 2) * t_iter)
-    value = statistics.mean(vals)
-    cores = s["cores"]
-    sample = (f"each step: reference partition_graph with max_iters=2 on {cores} host threads, extrapolated "
-              f"to {c['ref_iters']} iterations at {t_iter:.2f} s/iter (calibrated with max_iters=1,3)")
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "s", "n_gpus": world,
+    thr, sw = best_threads()
+    s = cpu_sample(args.config, args.steps, thr, warmup=args.warmup, timeout=6 * 3600)
+    st = summarize_runs(s)
+    value = st["mean"]
+    from paper_2105_00578_b200 import generators  # noqa: F401 (graph sizes for the config dict)
+    g = make_graph(c["gen"])
+    last = s["runs"][-1]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(value * 1e3, 1),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: " + c["desc"], "config": {"workload": f"{args.config}: {c['desc']}"},
-            "cpu_baseline": {"value": round(value, 3), "unit": "s", "cores": cores, "kind": s["kind"],
-                             "sample": sample},
-            "e2e": {"value": round(value, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "data": "synthetic: " + c["desc"] + " (reference generator semantics, unit weights)",
+            "config": config_dict(args, c, g, world),
+            "cpu_baseline": {"value": value, "unit": "s", "cores": s["cores"], "kind": s["kind"],
+                             "min": st["min"], "median": st["median"], "runs_s": st["runs_s"],
+                             "threads_from": "profiles/cpu_thread_sweep.json" if sw else "all cores",
+                             "sample": (f"each timed step = one full reference partition_graph (max_iters 1000, "
+                                        f"OMP_WAIT_POLICY=active, {s['cores']} of {os.cpu_count()} host "
+                                        f"threads); warm-up steps ran max_iters=1")},
+            "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "result": {"cut": last["cut"], "imbalance": last["imbalance"], "iterations": last["iterations"],
+                       "times": last["times"]}}
     print(json.dumps(line), flush=True)
+
+
+def config_dict(args, c, g, world):
+    return {"workload": f"{args.config}: {c['desc']}", "n": int(g.n), "nnz_A": int(g.row_offsets[-1]),
+            "K": c["K"], "problem": c["problem"], "precond": c["precond"], "seed": 42,
+            "parallelism": f"rows1d x{world}" if world > 1 else "single",
+            "l2": "flushed between steps (256 MiB write)"}
 
 
 if __name__ == "__main__":

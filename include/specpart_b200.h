@@ -156,6 +156,10 @@ typedef struct sp_report {
     sp_trace_record* trace;        /* trace_capacity records */
     int32_t trace_capacity;
     int32_t trace_len;
+    /* the eigenvectors the partition was computed from (EigenResult::X,
+     * eigensolver.hpp:28-35): n x d column-major, B-orthonormal; column 0 is the
+     * one embed() drops (partitioner.cpp:19-25). NULL = not wanted. */
+    double* eigenvectors_out;
 } sp_report;
 
 typedef struct sp_context sp_context;
@@ -177,8 +181,9 @@ sp_status sp_context_set_timing(sp_context* ctx, int on);
 
 /* ---- end to end (pipeline.cpp:47-167) --------------------------------------
  * assignment_out: n int32 part ids in [0, K). x0_colmajor: optional n x d
- * initial block replacing the init selection (the CLI's --init-file warm
- * start, tools/specpart.cpp:94-157); pass NULL for the reference behaviour.
+ * initial block (d = floor(log2 K) + 1 = report->eigenvectors, n*d doubles)
+ * replacing the init selection (the CLI's --init-file warm start,
+ * tools/specpart.cpp:94-157); pass NULL for the reference behaviour.
  * With world > 1 every rank passes the same full graph; every rank receives
  * the full assignment. */
 sp_status sp_partition(sp_context* ctx, const sp_graph* g, const sp_config* cfg,
@@ -244,6 +249,15 @@ sp_status sp_build_laplacian(sp_context* ctx, int32_t kind, const sp_graph* g,
 sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* g, const double* X, int32_t m,
                   double* Y);
 
+/* Y = L * X through the kernels the eigensolver runs on this graph (kind 0
+ * combinatorial or 1 normalized): on irregular graphs (classify) the
+ * row-length-binned kernels with chunked long rows, whose sums are
+ * deterministic but not in storage order (compare within
+ * |y - y_ref| <= c * eps * sum_k |a_ik x_k|); on meshes the same kernels as
+ * sp_spmm (bit-exact). */
+sp_status sp_spmm_solver(sp_context* ctx, int32_t kind, const sp_graph* g, const double* X, int32_t m,
+                         double* Y);
+
 /* Y = A * X for an explicit CSR operator (spmv_block, kernels.cpp:36-62). */
 sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64_t* offsets,
                       const int32_t* cols, const double* vals, const double* X, int32_t m,
@@ -265,6 +279,12 @@ sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const
 /* Initial blocks (eigensolver.cpp:20-51), n x d column-major, bit-identical. */
 sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed,
                            double* X_out);
+
+/* Rows [row0, row0 + nloc) of the same n x d block (nloc x d column-major):
+ * the slice a rank of a row-partitioned run generates for itself (the
+ * mt19937_64 stream is jumped ahead to the slice, rng.cu). */
+sp_status sp_initial_guess_rows(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed,
+                                int64_t row0, int64_t nloc, double* X_out);
 
 /* LOBPCG (eigensolver.cpp:177-337) on the problem built from g. precond is
  * SP_PRECOND_JACOBI, SP_PRECOND_POLYNOMIAL (poly_seed feeds PolyConfig.seed) or

@@ -103,7 +103,8 @@ class SpReport(C.Structure):
                 ("halo_launches", C.c_int64), ("halo_bytes", C.c_double), ("halo_ms", C.c_double),
                 ("spmm_eff_bytes", C.c_double), ("poly_eff_bytes", C.c_double),
                 ("part_weights", C.POINTER(C.c_double)), ("trace", C.POINTER(SpTraceRecord)),
-                ("trace_capacity", C.c_int32), ("trace_len", C.c_int32)]
+                ("trace_capacity", C.c_int32), ("trace_len", C.c_int32),
+                ("eigenvectors_out", C.POINTER(C.c_double))]
 
 
 class SpGraphInfo(C.Structure):
@@ -130,10 +131,12 @@ SIGNATURES = {
     "sp_partition_resident": (I32, [P, P, C.POINTER(SpConfig), P, C.POINTER(SpReport), P]),
     "sp_build_laplacian": (I32, [P, I32, C.POINTER(SpGraph), P, P, P, P, C.POINTER(F64), C.POINTER(I32)]),
     "sp_spmm": (I32, [P, I32, C.POINTER(SpGraph), P, I32, P]),
+    "sp_spmm_solver": (I32, [P, I32, C.POINTER(SpGraph), P, I32, P]),
     "sp_spmm_csr": (I32, [P, I64, I64, P, P, P, P, I32, P]),
     "sp_gram": (I32, [P, I64, P, I32, P, I32, P, P]),
     "sp_bench_blockop": (I32, [P, I64, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),
     "sp_initial_guess": (I32, [P, I32, I64, I32, U64, P]),
+    "sp_initial_guess_rows": (I32, [P, I32, I64, I32, U64, I64, I64, P]),
     "sp_lobpcg": (I32, [P, C.POINTER(SpGraph), I32, I32, U64, I32, P, I32, F64, I32, I32, P, P, P, P,
                         C.POINTER(I32), C.POINTER(I32)]),
     "sp_poly_apply": (I32, [P, I32, C.POINTER(SpGraph), U64, I32, P, I32, P, P, C.POINTER(I32)]),

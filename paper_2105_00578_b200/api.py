@@ -165,6 +165,7 @@ class RunReport:
 class RunResult:
     partition: Partition
     report: RunReport
+    eigenvectors: np.ndarray | None = None  # n x d (EigenResult::X), when asked for
 
 
 @dataclass
@@ -235,6 +236,27 @@ def _colmajor(X):
     return np.asfortranarray(X)
 
 
+def _check_x0(x0, n: int, cfg: RunConfig):
+    """The C-ABI reads n*d doubles of x0 (d = eigenvector_count(K)): anything else is a
+    DimensionError (errors.hpp:51-54), never an out-of-bounds host read."""
+    if x0 is None:
+        return None
+    d = eigenvector_count(int(cfg.num_parts))
+    X = np.asarray(x0, dtype=np.float64)
+    if X.ndim != 2 or X.shape != (n, d):
+        raise abi.DimensionError(f"partition_graph: x0 must have shape (n, d) = ({n}, {d}), got {X.shape}")
+    return np.asfortranarray(X)
+
+
+def _want_vectors(rep, n: int, cfg: RunConfig, on: bool):
+    if not on:
+        return None
+    d = eigenvector_count(int(cfg.num_parts))
+    ev = np.empty((n, d), dtype=np.float64, order="F")
+    rep.eigenvectors_out = ev.ctypes.data_as(C.POINTER(C.c_double))
+    return ev
+
+
 # ---- context ------------------------------------------------------------------
 class Context:
     """One B200 (one rank). world > 1 needs the same nccl_id on every rank."""
@@ -277,8 +299,10 @@ class Context:
         self._check(self.lib.sp_context_set_timing(self._h, int(on)))
 
     # pipeline.cpp:47-167
-    def partition_graph(self, g: Graph, cfg: RunConfig, x0=None, out=None) -> RunResult:
-        """out: optional caller-owned int32[n] array (e.g. pinned) receiving the assignment."""
+    def partition_graph(self, g: Graph, cfg: RunConfig, x0=None, out=None,
+                        return_eigenvectors: bool = False) -> RunResult:
+        """out: optional caller-owned int32[n] array (e.g. pinned) receiving the assignment.
+        x0: optional n x d initial block, d = eigenvector_count(K) (the CLI's --init-file)."""
         n = g.n
         if out is not None:
             if out.dtype != np.int32 or out.shape != (n,) or not out.flags.c_contiguous:
@@ -295,13 +319,14 @@ class Context:
             trace_buf = (abi.SpTraceRecord * cap)()
             rep.trace = C.cast(trace_buf, C.POINTER(abi.SpTraceRecord))
             rep.trace_capacity = cap
-        x0b = _colmajor(x0) if x0 is not None else None
+        x0b = _check_x0(x0, n, cfg)
+        ev = _want_vectors(rep, n, cfg, return_eigenvectors)
         gc, cc = g.as_c(), cfg.as_c()
         self._check(self.lib.sp_partition(self._h, C.byref(gc), C.byref(cc), assignment.ctypes.data,
                                           C.byref(rep), _ptr(x0b)))
         report = report_from_c(rep, pw, trace_buf)
         part = Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance)
-        return RunResult(part, report)
+        return RunResult(part, report, ev)
 
     def upload(self, g: Graph) -> "DeviceGraph":
         """Copies the graph arrays into HBM (sp_graph_upload)."""
@@ -311,18 +336,19 @@ class Context:
         return DeviceGraph(self, h, g.n)
 
     def partition_resident(self, dg: "DeviceGraph", cfg: RunConfig, copy_assignment: bool = True,
-                           x0=None) -> RunResult:
+                           x0=None, return_eigenvectors: bool = False) -> RunResult:
         """partition_graph on an HBM-resident graph (sp_partition_resident)."""
         assignment = np.empty(dg.n, dtype=np.int32) if copy_assignment else None
         pw = np.zeros(max(int(cfg.num_parts), 1), dtype=np.float64)
         rep = abi.SpReport()
         rep.part_weights = pw.ctypes.data_as(C.POINTER(C.c_double))
-        x0b = _colmajor(x0) if x0 is not None else None
+        x0b = _check_x0(x0, dg.n, cfg)
+        ev = _want_vectors(rep, dg.n, cfg, return_eigenvectors)
         cc = cfg.as_c()
         self._check(self.lib.sp_partition_resident(self._h, dg.handle, C.byref(cc), _ptr(assignment),
                                                    C.byref(rep), _ptr(x0b)))
         report = report_from_c(rep, pw, None)
-        return RunResult(Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance), report)
+        return RunResult(Partition(assignment, int(cfg.num_parts), pw, rep.cutsize, rep.imbalance), report, ev)
 
     # laplacian.cpp:53-144 (explicit CSR, bit-exact)
     def build_laplacian(self, kind: str, g: Graph):
@@ -349,6 +375,16 @@ class Context:
         self._check(self.lib.sp_spmm(self._h, abi.LAP[kind], C.byref(gc), Xc.ctypes.data, m, Y.ctypes.data))
         return Y
 
+    def spmm_solver(self, kind: str, g: Graph, X) -> np.ndarray:
+        """Y = L X through the eigensolver's own kernel dispatch (sp_spmm_solver)."""
+        Xc = _colmajor(X)
+        n, m = Xc.shape
+        Y = np.empty((n, m), dtype=np.float64, order="F")
+        gc = g.as_c()
+        self._check(self.lib.sp_spmm_solver(self._h, abi.LAP[kind], C.byref(gc), Xc.ctypes.data, m,
+                                            Y.ctypes.data))
+        return Y
+
     def spmm_csr(self, row_offsets, col_indices, values, X, ncols=None) -> np.ndarray:
         offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
         cols = np.ascontiguousarray(col_indices, dtype=np.int32)
@@ -373,6 +409,12 @@ class Context:
     def initial_guess(self, init: str, n: int, d: int, seed: int = 0) -> np.ndarray:
         X = np.empty((n, d), dtype=np.float64, order="F")
         self._check(self.lib.sp_initial_guess(self._h, abi.INIT[init], n, d, seed, X.ctypes.data))
+        return X
+
+    def initial_guess_rows(self, init: str, n: int, d: int, seed: int, row0: int, nloc: int) -> np.ndarray:
+        """Rows [row0, row0+nloc) of initial_guess(init, n, d, seed) (sp_initial_guess_rows)."""
+        X = np.empty((nloc, d), dtype=np.float64, order="F")
+        self._check(self.lib.sp_initial_guess_rows(self._h, abi.INIT[init], n, d, seed, row0, nloc, X.ctypes.data))
         return X
 
     def lobpcg(self, g: Graph, problem: str, precond: str, X0, tol: float, max_iters: int = 1000,

@@ -281,6 +281,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     double* pw_out = rep ? rep->part_weights : nullptr;
     sp_trace_record* tr_out = rep ? rep->trace : nullptr;
     const int32_t tr_cap = rep ? rep->trace_capacity : 0;
+    double* ev_out = rep ? rep->eigenvectors_out : nullptr;
 
     // Stage 1: degrees, classification, operators (the copy, if any, is already queued)
     const auto t_lap = Clock::now();
@@ -385,6 +386,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     if (R.imbalance > 1.0 + cfg->epsilon) R.warnings |= SP_WARN_IMBALANCE;
     SPB_CUDA(cudaStreamSynchronize(s));
     ctx->prof.mark(s, "metrics");
+    if (ev_out) download_block(Xg, n, d, ev_out, s);  // EigenResult::X, on request (tests)
     ctx->prof.dump("partition_core");
     ctx->collect_spmm_times();
     R.total_s = since(t_total);
@@ -403,6 +405,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     R.n_gpus = ctx->comm.world;
     if (rep) {
         R.part_weights = pw_out;
+        R.eigenvectors_out = ev_out;
         R.trace = tr_out;
         R.trace_capacity = tr_cap;
         if (pw_out) std::memcpy(pw_out, pm.part_weights.data(), sizeof(double) * K);
@@ -697,6 +700,32 @@ sp_status sp_spmm(sp_context* ctx, int32_t kind, const sp_graph* hg, const doubl
     });
 }
 
+sp_status sp_spmm_solver(sp_context* ctx, int32_t kind, const sp_graph* hg, const double* X, int32_t m,
+                         double* Y) {
+    return guarded(ctx, [&] {
+        if (m < 1 || m > kMaxCols) throw_dimension("sp_spmm_solver: 1 <= m <= 64");
+        if (kind != 0 && kind != 1) throw_invalid("sp_spmm_solver: kind must be combinatorial or normalized");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        const GraphKindInfo k = classify(g);
+        DevLaplacian L;
+        build_laplacian(kind, g, false, L, s);
+        // the operator exactly as partition_core prepares it for the eigensolver
+        if (!k.regular) build_row_bins(L.op, kLongRow, L.bins, s);
+        localize_operator(ctx->comm, g, L, s);
+        const int64_t nloc = g.n_local;
+        Solver solver(ctx, L.op, nullptr, m);
+        DBuf<double> xd, yd(solver.block_elems(m));
+        const View Xv = solver.block(solver.input_block(m, xd), m);
+        upload_block(X, hg->n, g.row0, nloc, m, Xv, s);
+        solver.spmm_store(Xv, m, solver.block(yd.p, m));
+        DBuf<double> keep;
+        const View Yg = gather_block(ctx, solver.block(yd.p, m), m, keep);
+        download_block(Yg, hg->n, m, Y, s);
+    });
+}
+
 sp_status sp_spmm_csr(sp_context* ctx, int64_t nrows, int64_t ncols, const int64_t* offsets, const int32_t* cols,
                       const double* vals, const double* X, int32_t m, double* Y) {
     return guarded(ctx, [&] {
@@ -810,6 +839,19 @@ sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, 
         if (init == SP_INIT_PIECEWISE) initial_block_piecewise(n, d, 0, n, X, s);
         else initial_block_random(n, d, seed, 0, n, X, s);
         download_block(X, n, d, X_out, s);
+    });
+}
+
+sp_status sp_initial_guess_rows(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed, int64_t row0,
+                               int64_t nloc, double* X_out) {
+    return guarded(ctx, [&] {
+        if (row0 < 0 || nloc < 0 || row0 + nloc > n) throw_dimension("sp_initial_guess_rows: slice outside [0, n)");
+        cudaStream_t s = ctx->stream;
+        DBuf<double> xd(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * std::max(d, 1));
+        const View X = rowmajor(xd.p, d, d);
+        if (init == SP_INIT_PIECEWISE) initial_block_piecewise(n, d, row0, nloc, X, s);
+        else initial_block_random(n, d, seed, row0, nloc, X, s);
+        download_block(X, nloc, d, X_out, s);
     });
 }
 

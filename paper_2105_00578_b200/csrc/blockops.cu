@@ -11,6 +11,7 @@
 // blocks, row slices). Per-CTA partials are reduced in a fixed order by a second
 // kernel, so every Gram is bit-reproducible run to run (the reference's
 // chunked-reduction determinism contract, kernels.hpp:10-13).
+#include "bulk.cuh"
 #include "ops.cuh"
 
 #include <algorithm>
@@ -426,40 +427,6 @@ __global__ void __launch_bounds__(kTsThreads) ts_mma_kernel(const TsDev a) {
 constexpr int kBulkMaxBlk = 9;
 constexpr int kBulkThreads = kTsThreads + 32;  // 8 consumer warps + 1 producer warp
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
 // Stage layout (columns of SC doubles): U [0, u) | V [cV, cV+kv) | 3 zero | b.
 // The zero columns pad the transform's k-steps past V (COMBINE) and stand in
 // for Gram fragment rows/columns past P/Q; past U (UPDATE) the k-steps read V
@@ -701,141 +668,6 @@ __global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Column-major blocks (rs == 1): no staging. A warp walks 8-row blocks; MMA
-// fragments are read straight from global memory (a fragment load touches 8
-// columns x 4 consecutive rows = 8 full 32-byte sectors). The transform's C
-// matrix lives in registers as B fragments; W is written from the D fragments
-// and transposed through a 2 KB per-warp scratch for the fused Gram, whose
-// 8x8 fragments are accumulated in registers and reduced in a fixed order.
-template <int KB, int NBW, int MBG, int NBG>  // k-steps of C, n-blocks of W, Gram blocks
-__global__ void __launch_bounds__(kTsThreads) ts_col_mma_kernel(const TsDev a) {
-    extern __shared__ double smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
-    const int u = a.u0 + a.u1;
-    const int inner = a.transform == TS_UPDATE ? u : a.kv;
-    double* ws = smem + warp * 8 * 33;  // W block scratch: 8 rows x kw (stride 33)
-    double* red = smem;                 // reused for the final reduction
-    // B fragments of C: cf[kk][nb] = C[4kk + tig][8nb + gid]
-    double cf[KB][NBW];
-#pragma unroll
-    for (int kk = 0; kk < KB; ++kk)
-#pragma unroll
-        for (int nb = 0; nb < NBW; ++nb) {
-            const int k = 4 * kk + tig, nn = 8 * nb + gid;
-            cf[kk][nb] = (a.transform != TS_NONE && k < inner && nn < a.kw) ? a.C[k + static_cast<int64_t>(nn) * a.ldc] : 0.0;
-        }
-    double g0[MBG][NBG], g1[MBG][NBG];
-#pragma unroll
-    for (int i = 0; i < MBG; ++i)
-#pragma unroll
-        for (int j = 0; j < NBG; ++j) g0[i][j] = g1[i][j] = 0.0;
-
-    const int uL = a.left_u ? u : 0;
-    const bool self_w = a.transform != TS_NONE;  // right block is W (else V)
-    const int rq = self_w ? a.kw : a.kv;
-    // column c of the transform input / the gram operands
-    auto in_col = [&](int c) -> const double* {  // transform input column (global)
-        if (a.transform == TS_UPDATE) return c < a.u0 ? a.U0.ptr + c * a.U0.cs : a.U1.ptr + (c - a.u0) * a.U1.cs;
-        return a.V.ptr + c * a.V.cs;
-    };
-    const int64_t nblocks = (a.n + 7) / 8;
-    const int64_t gw = static_cast<int64_t>(blockIdx.x) * (kTsThreads / 32) + warp;
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * (kTsThreads / 32);
-    for (int64_t blk = gw; blk < nblocks; blk += nw) {
-        const int64_t r0 = blk * 8;
-        const bool rok = r0 + gid < a.n;
-        if (self_w) {
-            // D = Ain[r0:r0+8, :] * C
-            double d0[NBW], d1[NBW];
-#pragma unroll
-            for (int nb = 0; nb < NBW; ++nb) d0[nb] = d1[nb] = 0.0;
-#pragma unroll
-            for (int kk = 0; kk < KB; ++kk) {
-                const int k = 4 * kk + tig;
-                const double av = (k < inner && rok) ? in_col(k)[r0 + gid] : 0.0;
-#pragma unroll
-                for (int nb = 0; nb < NBW; ++nb) dmma(d0[nb], d1[nb], av, cf[kk][nb]);
-            }
-#pragma unroll
-            for (int nb = 0; nb < NBW; ++nb) {
-                const int c = 8 * nb + 2 * tig;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int cc = c + h;
-                    if (cc >= a.kw) continue;
-                    double w = h ? d1[nb] : d0[nb];
-                    if (a.transform == TS_UPDATE) w = (rok ? a.V.ptr[cc * a.V.cs + r0 + gid] : 0.0) - w;
-                    if (!rok) w = 0.0;
-                    ws[gid * 33 + cc] = w;
-                    if (rok) {
-                        if (cc < a.W.cols) a.W.ptr[cc * a.W.cs + r0 + gid] = w;
-                        else a.W2.ptr[(cc - a.W.cols) * a.W2.cs + r0 + gid] = w;
-                    }
-                }
-            }
-            __syncwarp();
-        }
-        if (a.gram) {
-            // two k-steps of 4 rows: G += L^T diag(b) R
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                const int rr = ks * 4 + tig;
-                const int64_t row = r0 + rr;
-                const bool ok = row < a.n;
-                const double bw = (a.b && ok) ? a.b[row] : 1.0;
-                double av[MBG], bv[NBG];
-#pragma unroll
-                for (int mb = 0; mb < MBG; ++mb) {
-                    const int m = 8 * mb + gid;
-                    double v = 0.0;
-                    if (ok && m < a.P) {
-                        if (m < uL) v = m < a.u0 ? a.U0.ptr[m * a.U0.cs + row] : a.U1.ptr[(m - a.u0) * a.U1.cs + row];
-                        else v = self_w ? ws[rr * 33 + (m - uL)] : a.V.ptr[(m - uL) * a.V.cs + row];
-                    }
-                    av[mb] = v;
-                }
-#pragma unroll
-                for (int nb = 0; nb < NBG; ++nb) {
-                    const int nn = 8 * nb + gid;
-                    double v = 0.0;
-                    if (ok && nn < a.Q) v = self_w ? ws[rr * 33 + nn] : a.V.ptr[nn * a.V.cs + row];
-                    bv[nb] = v * bw;
-                }
-#pragma unroll
-                for (int mb = 0; mb < MBG; ++mb)
-#pragma unroll
-                    for (int nb = 0; nb < NBG; ++nb) dmma(g0[mb][nb], g1[mb][nb], av[mb], bv[nb]);
-            }
-        }
-        if (self_w) __syncwarp();
-    }
-    (void)rq;
-    if (!a.gram) return;
-    __syncthreads();
-    // red[warp][mb][nb][64]: fragment element (gid, 2tig+h)
-#pragma unroll
-    for (int mb = 0; mb < MBG; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NBG; ++nb) {
-            double* f = red + ((warp * MBG + mb) * NBG + nb) * 64;
-            f[gid * 8 + 2 * tig] = g0[mb][nb];
-            f[gid * 8 + 2 * tig + 1] = g1[mb][nb];
-        }
-    __syncthreads();
-    double* part = a.partial + static_cast<int64_t>(blockIdx.x) * a.P * a.Q;
-    for (int e = threadIdx.x; e < a.P * a.Q; e += blockDim.x) {
-        const int i = e % a.P, j = e / a.P;
-        const int off = ((i / 8) * NBG + (j / 8)) * 64 + (i % 8) * 8 + (j % 8);
-        double sum = 0.0;
-        for (int w = 0; w < kTsThreads / 32; ++w) sum += red[w * MBG * NBG * 64 + off];
-        part[i + j * a.P] = sum;
-    }
-}
-
-// One warp per Gram entry: lane l sums partial rows l, l+32, ... then a fixed
-// butterfly — deterministic for a fixed grid.
 __global__ void reduce_gram_kernel(const double* partial, int rows, int PQ, double* out) {
     const int e = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -932,11 +764,6 @@ int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s) {
     return grid;
 }
 
-bool ts_force_cuda_cores() {
-    static const bool v = std::getenv("SPB_TS_NO_MMA") != nullptr;
-    return v;
-}
-
 int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_elems, cudaStream_t st) {
     TsDev a{};
     a.n = s.n;
@@ -1005,16 +832,12 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     const bool colmajor_all = cm(s.U0, a.u0) && cm(s.U1, a.u1) && cm(s.V, a.kv) &&
                               (s.transform == TS_NONE || (cm(s.W, s.W.cols) && (!s.W2.ptr || cm(s.W2, s.W2.cols))));
     // bulk-copy kernel for aligned column-major operands (meshes' default)
-    static const bool no_bulk = [] {
-        const char* e = std::getenv("SPB_TS_BULK");
-        return e && e[0] == '0';
-    }();
     auto aligned = [](const View& v, int cols) {
         return cols == 0 || (reinterpret_cast<uintptr_t>(v.ptr) % 16 == 0 && (cols == 1 || v.cs % 2 == 0));
     };
     const int nblk_b = a.gram ? ((a.P + 7) / 8) * ((a.Q + 7) / 8) : 0;
     const int nw1 = s.transform == TS_NONE ? 0 : s.W.cols, nw2 = s.transform == TS_NONE ? 0 : a.kw - nw1;
-    if (!no_bulk && colmajor_all && !ts_force_cuda_cores() && aligned(s.U0, a.u0) && aligned(s.U1, a.u1) &&
+    if (colmajor_all && aligned(s.U0, a.u0) && aligned(s.U1, a.u1) &&
         aligned(s.V, a.kv) && aligned(s.W, nw1) && aligned(s.W2, nw2) &&
         (!s.b || reinterpret_cast<uintptr_t>(s.b) % 16 == 0) && nblk_b <= kBulkMaxBlk &&
         a.u0 + a.u1 + a.kv + 1 <= 64 && a.kw <= 64) {
@@ -1028,19 +851,10 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
         g.ncol = g.cb + g.has_b;
         size_t smb = 0;
         bool found = false;
-        static const int tr_env = [] {
-            const char* e = std::getenv("SPB_TS_TR");
-            return e ? std::atoi(e) : 0;
-        }();
-        static const int kb_env = [] {
-            const char* e = std::getenv("SPB_TS_STAGE_KB");
-            return e ? std::atoi(e) : 48;
-        }();
         const int KBp = (inner + 3) / 4 * 4, NWp = (a.kw + 7) / 8 * 8;
-        // tile rows: ~kb_env KB of loaded columns per stage, 64..2048 rows
+        // tile rows: ~48 KB of loaded columns per stage, 64..2048 rows
         int TR = 64;
-        while (TR < 2048 && static_cast<size_t>(g.nload) * (2 * TR) * 8 <= static_cast<size_t>(kb_env) * 1024) TR *= 2;
-        if (tr_env) TR = tr_env;
+        while (TR < 2048 && static_cast<size_t>(g.nload) * (2 * TR) * 8 <= static_cast<size_t>(48) * 1024) TR *= 2;
         for (; TR >= 64 && !found; TR /= 2) {
             for (int nst : {4, 3, 2}) {
                 const int SC = TR + 4;
@@ -1085,38 +899,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
             return a.P;
         }
     }
-    static const bool direct = std::getenv("SPB_TS_DIRECT") != nullptr;  // experimental, off by default
-    if (direct && colmajor_all && !ts_force_cuda_cores() && (s.transform == TS_NONE || (inner <= 32 && a.kw <= 32)) &&
-        (!a.gram || (a.P <= 40 && a.Q <= 32))) {
-        const int KB = (inner + 3) / 4, NBW = (a.kw + 7) / 8;
-        const int MBG = a.gram ? (a.P + 7) / 8 : 0, NBG = a.gram ? (a.Q + 7) / 8 : 0;
-        const bool small = KB <= 4 && NBW <= 2 && MBG <= 3 && NBG <= 1;
-        const bool mid = KB <= 8 && NBW <= 2 && MBG <= 4 && NBG <= 2;
-        const int mbg = small ? 3 : (mid ? 4 : 5), nbg = small ? 1 : (mid ? 2 : 4);
-        const size_t smc = sizeof(double) * std::max<size_t>(static_cast<size_t>(kTsThreads / 32) * 8 * 33,
-                                                            a.gram ? static_cast<size_t>(kTsThreads / 32) * mbg * nbg * 64 : 0);
-        const int64_t nblocks8 = (s.n + 7) / 8;
-        int gridc = grid_for(nblocks8, kTsThreads / 32, 4);
-        if (a.gram) {
-            while (static_cast<size_t>(gridc) * PQ > scratch_elems && gridc > 1) gridc = (gridc + 1) / 2;
-        }
-        auto go = [&](auto kern) {
-            if (smc > 48 * 1024)
-                SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smc)));
-            kern<<<gridc, kTsThreads, smc, st>>>(a);
-        };
-        if (small) go(ts_col_mma_kernel<4, 2, 3, 1>);
-        else if (mid) go(ts_col_mma_kernel<8, 2, 4, 2>);
-        else go(ts_col_mma_kernel<8, 4, 5, 4>);
-        SPB_LAUNCH_CHECK();
-        if (a.gram) {
-            reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 4), 128, 0, st>>>(scratch, gridc,
-                                                                                  static_cast<int>(PQ), gram_out);
-            SPB_LAUNCH_CHECK();
-        }
-        return a.P;
-    }
-    const bool mma_ok = !ts_force_cuda_cores() && (!a.gram || nblk <= kMaxItems * (kTsThreads / 32));
+    const bool mma_ok = (!a.gram || nblk <= kMaxItems * (kTsThreads / 32));
     if (mma_ok) {
         // reduction scratch: nitems x 64 doubles must fit in the staged smem
         const int kgroups = a.gram ? std::max(1, std::min(16, 8 / std::max(nblk, 1))) : 1;

@@ -65,6 +65,11 @@ struct DevOp {
     const int32_t* ell_pat_tab = nullptr;
     const double* ell_pat_deg = nullptr;
     int ell_npat = 0;
+    // band-staged SpMM (spmm_band.cu): the pattern offsets fall into band_n narrow
+    // bands [band_lo, band_hi] (band_plan); 0 = not planned
+    int band_n = 0;
+    int band_lo[4] = {0, 0, 0, 0};
+    int band_hi[4] = {0, 0, 0, 0};
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -110,6 +115,12 @@ struct EllPatStore {
     DBuf<double> deg;
 };
 bool build_ell_patterns(DevOp& op, EllPatStore& st, cudaStream_t s);
+// Band-staged SpMM on pattern-compressed meshes (spmm_band.cu): band_plan clusters
+// the pattern offsets into <= kMaxBands bands (false: no plan, op unchanged).
+constexpr int kMaxBands = 4;
+bool band_plan(DevOp& op, cudaStream_t s);
+bool spmm_band_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+int spmm_band_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
 // Row-length bins for the vector SpMM (spmm_vec.cu); also sets the long-row list.
 struct RowBins {
     DBuf<int32_t> rows;

@@ -96,17 +96,17 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     }
     colmajor_ = A.mode != OP_DIAGONAL && A.max_row <= 32 && A.n_long == 0;
     ld_ = colmajor_ ? ((rows_cap_ + 63) / 64) * 64 : max_cols;
-    static const bool no_ell = [] {
-        const char* e = std::getenv("SPB_NO_ELL");
-        return e && e[0] == '1';
-    }();
-    static const bool no_pat = [] {
-        const char* e = std::getenv("SPB_NO_ELL_PAT");
-        return e && e[0] == '1';
-    }();
-    if (colmajor_ && !no_ell && build_ell(A_, n_, ell_, s_) && !no_pat) {
+    // meshes: fixed-slot ELL, pattern-compressed when the rows share <= 256 slot
+    // patterns (any stencil with KL = KU in {2, 3, 13}: 5-, 7- and 27-point)
+    if (colmajor_ && build_ell(A_, n_, ell_, s_)) {
         const int kk = A_.ell_kl * 100 + A_.ell_ku;
-        if (kk == 202 || kk == 303 || kk == 1313) build_ell_patterns(A_, ellpat_, s_);
+        if ((kk == 202 || kk == 303 || kk == 1313) && build_ell_patterns(A_, ellpat_, s_) && !halo_) {
+            static const bool no_band = [] {  // A/B diagnostics only
+                const char* e = std::getenv("SPB_BAND");
+                return e && e[0] == '0';
+            }();
+            if (!no_band) band_plan(A_, s_);
+        }
     }
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
@@ -184,16 +184,6 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
         if (fused) {
             ctx_->timers.halo_launches += 1;
             ctx_->timers.halo_bytes += static_cast<double>(ctx_->comm.halo.total_send) * m * 8;
-            static const bool probe = [] {
-                const char* e = std::getenv("SPB_HALO_PROBE");
-                return e && e[0] == '1';
-            }();
-            if (probe) {
-                probe_.alloc(8);
-                const unsigned long long init[7] = {~0ull, 0ull, 0ull, 0ull, 0ull, ~0ull, 0ull};
-                SPB_CUDA(cudaMemcpyAsync(probe_.p, init, sizeof(init), cudaMemcpyHostToDevice, s_));
-                hf.probe = probe_.p;
-            }
         }
     }
     if (halo_ && !fused) {
@@ -212,48 +202,8 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
         ev = ctx_->next_event_pair(ea.mode == EPI_POLY ? 1 : 0);
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
-    static const bool fake_hf = [] {
-        const char* e = std::getenv("SPB_FAKE_HF");
-        return e && e[0] == '1';
-    }();
-    if (fake_hf && !halo_ && spmm_col_path(A_, Xlocal, m, ea)) {
-        // diagnostic: the fused-exchange kernel variant on one GPU (no peers)
-        hf = HaloFuse{};
-        hf.on = 1;
-        hf.nopush = 1;
-        hf.n_int = (A_.n + 31) / 32;
-        hf.bnd = hf.n_int;
-        fused = true;
-    }
-    static const bool ce_split = [] {
-        const char* e = std::getenv("SPB_HALO_CE_SPLIT");
-        return e && e[0] == '1';
-    }();
-    if (ce && ce_split) {
-        // diagnostic: wait for the halo first, then the plain kernel
-        halo_wait_flags(hf, s_);
-        fused = false;
-    }
     const int rows = spmm_launch(A_, Xg, m, ea, s_, fused ? &hf : nullptr);
     if (ce) halo_ce_finish(ctx_->comm, s_);
-    if (fused && hf.probe) {
-        unsigned long long h[7];
-        SPB_CUDA(cudaMemcpyAsync(h, hf.probe, sizeof(h), cudaMemcpyDeviceToHost, s_));
-        SPB_CUDA(cudaStreamSynchronize(s_));
-        probe_n_ += 1;
-        if (h[5] != ~0ull) {
-            probe_first_ += static_cast<double>(h[5] - h[0]);
-            probe_last_ += static_cast<double>(h[6] - h[0]);
-        }
-        probe_push_ += static_cast<double>(h[1] - h[0]);
-        probe_wait_ += h[3] ? static_cast<double>(h[2]) / static_cast<double>(h[3]) : 0.0;
-        probe_total_ += static_cast<double>(h[4] - h[0]);
-        if (probe_n_ % 400 == 0)
-            std::fprintf(stderr, "[spb-halo] rank %d: %lld fused SpMMs, push+fence %.2f us, mean warp wait %.2f us, "
-                                 "first halo tile at %.2f us, last wait released at %.2f us, kernel %.2f us\n",
-                         ctx_->comm.rank, probe_n_, probe_push_ / probe_n_ / 1e3, probe_wait_ / probe_n_ / 1e3,
-                         probe_first_ / probe_n_ / 1e3, probe_last_ / probe_n_ / 1e3, probe_total_ / probe_n_ / 1e3);
-    }
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     ctx_->timers.spmm_launches += 1;
     // algorithmic bytes of this launch: the operator's own

@@ -105,9 +105,6 @@ private:
 
     DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
     EllPatStore ellpat_; // its pattern-compressed form (ellpat.cu)
-    DBuf<unsigned long long> probe_;  // SPB_HALO_PROBE timestamps
-    long long probe_n_ = 0;
-    double probe_push_ = 0.0, probe_wait_ = 0.0, probe_total_ = 0.0, probe_first_ = 0.0, probe_last_ = 0.0;
     DBuf<double> gram_, scratch_, cmat_, cmat2_, partial_, norms_;
     DBuf<double> R_, H_, P_, S_, AS_, prodA_, prodB_, work_;
 };

@@ -27,6 +27,14 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// X loads of the SpMM kernels. With the halo exchange fused in (HF), peers write
+// the halo rows of X while the kernel runs, so X is not read-only for the
+// kernel's lifetime and ld.global.nc is not allowed: use L2-coherent loads.
+template <bool HF> __device__ __forceinline__ double ldx(const double* p) {
+    if constexpr (HF) return __ldcg(p);
+    else return __ldg(p);
+}
+
 struct RowAcc {
     // returns acc for (row, column c); xi = X(grow, c)
     template <int MODE, int G>
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
             for (int q = 0; q < CB; ++q) {
                 on[q] = c0 + q < m;
                 xcol[q] = xbase + static_cast<uint64_t>(on[q] ? c0 + q : c0) * ldx8;
-                xi[q] = *reinterpret_cast<const double*>(xcol[q] + grow8);
+                xi[q] = ldx<HF>(reinterpret_cast<const double*>(xcol[q] + grow8));
                 hv[q] = 0.0;
                 if (EPI == EPI_POLY && !ea.first && ea.h_terms && live && on[q])
                     hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
@@ -481,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_col_kernel(const DevOp op
                 const double w = kRegs ? rw[sidx < NSR ? sidx : 0] : sw[sidx * 32 + lane];
 #pragma unroll
                 for (int q = 0; q < CB; ++q) {
-                    const double g = __ldg(reinterpret_cast<const double*>(xcol[q] + o));
+                    const double g = ldx<HF>(reinterpret_cast<const double*>(xcol[q] + o));
                     acc[q] = __dadd_rn(acc[q], __dmul_rn(w, g));
                 }
             }
@@ -681,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
             for (int q = 0; q < CB; ++q) {
                 on[q] = c0 + q < m;
                 xc[q] = ta.X + static_cast<int64_t>(on[q] ? c0 + q : c0) * ta.ldx;
-                xi[q] = __ldg(xc[q] + own);
+                xi[q] = ldx<HF>(xc[q] + own);
                 hv[q] = 0.0;
                 if (EPI == EPI_POLY && !ea.first && ea.h_terms && live && on[q])
                     hv[q] = ta.H[static_cast<int64_t>(c0 + q) * ta.ldh + row];
@@ -696,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                 for (int u = 0; u < CH; ++u)
                     if (s0 + u < KL)
 #pragma unroll
-                        for (int q = 0; q < CB; ++q) gv[q][u] = __ldg(xc[q] + j[s0 + u]);
+                        for (int q = 0; q < CB; ++q) gv[q][u] = ldx<HF>(xc[q] + j[s0 + u]);
 #pragma unroll
                 for (int u = 0; u < CH; ++u)
                     if (s0 + u < KL)
@@ -712,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
                 for (int u = 0; u < CH; ++u)
                     if (s0 + u < W)
 #pragma unroll
-                        for (int q = 0; q < CB; ++q) gv[q][u] = __ldg(xc[q] + j[s0 + u]);
+                        for (int q = 0; q < CB; ++q) gv[q][u] = ldx<HF>(xc[q] + j[s0 + u]);
 #pragma unroll
                 for (int u = 0; u < CH; ++u)
                     if (s0 + u < W)
@@ -784,17 +792,14 @@ __global__ void __launch_bounds__(kThreads, MINB) spmm_ell_kernel(const DevOp op
     }
 }
 
-// PAT instantiations exist only for the pattern-compressed stencil classes
+// PAT instantiations exist only for the pattern-compressed stencil classes.
+// Launch shape (profiles/r01_cfg2_pat_variants.json): two columns per pass at
+// 4 CTAs/SM for 5/7-point stencils.
 template <int KL, int KU, int EPI>
-auto pat_ell_kernel(bool hf, int v = 0) -> decltype(&spmm_ell_kernel<KL, KU, EPI, 2, 4, false>) {
+auto pat_ell_kernel(bool hf) -> decltype(&spmm_ell_kernel<KL, KU, EPI, 2, 4, false>) {
     if constexpr (KL == KU && (KL == 2 || KL == 3)) {
         if (hf) return &spmm_ell_kernel<KL, KU, EPI, 2, 4, true, true>;
-        switch (v) {  // SPB_ELL_VARIANT: columns per pass / CTAs per SM
-        case 1: return &spmm_ell_kernel<KL, KU, EPI, 2, 5, false, true>;
-        case 2: return &spmm_ell_kernel<KL, KU, EPI, 1, 6, false, true>;
-        case 3: return &spmm_ell_kernel<KL, KU, EPI, 4, 3, false, true>;
-        default: return &spmm_ell_kernel<KL, KU, EPI, 2, 4, false, true>;
-        }
+        return &spmm_ell_kernel<KL, KU, EPI, 2, 4, false, true>;
     } else {
         return nullptr;
     }
@@ -835,38 +840,15 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             grid = grid_for(ntiles, kThreads / 32, per_sm);
             kern<<<grid, kThreads, smem, s>>>(op, ta, ea, hf ? *hf : HaloFuse{});
         };
-        static const int variant = [] {
-            const char* e = std::getenv("SPB_SPMM_VARIANT");
-            return e ? std::atoi(e) : 0;
-        }();
+        if (MODE == OP_LAPLACE_UNIT && !hf && spmm_band_ok(op, X, m, ea)) return spmm_band_launch(op, X, m, ea, s);
         if (MODE == OP_LAPLACE_UNIT && op.ell) {
-            // fixed-slot ELL (meshes): the slot pair is chosen by the solver
-            static const int evariant = [] {
-                const char* e = std::getenv("SPB_ELL_VARIANT");
-                return e ? std::atoi(e) : 0;
-            }();
-            // few tiles per warp (small row blocks, e.g. a mesh split over many GPUs):
-            // all columns in one pass (one gather latency per tile instead of m/2)
-            static const int wide_env = [] {
-                const char* e = std::getenv("SPB_ELL_WIDE");
-                return e ? std::atoi(e) : -1;
-            }();
-            const int64_t warps_total = static_cast<int64_t>(device_sm_count()) * 32;
-            // (measured slower than the 2-column passes at every size on cfg2: off unless asked for)
-            const bool wide = m > 2 && wide_env == 1 && ntiles < 4 * warps_total;
+            // fixed-slot ELL (meshes), pattern-compressed when the solver found the patterns
             const bool pat = op.ell_pat != nullptr;
 #define SPB_ELL(KL_, KU_)                                                                                   \
     do {                                                                                                    \
-        if (wide && m <= 4) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 4, 2, true>                               \
-                                  : spmm_ell_kernel<KL_, KU_, EPI, 4, 2, false>, 0);                         \
-        else if (wide) go(hf ? spmm_ell_kernel<KL_, KU_, EPI, 8, 1, true>                                   \
-                             : spmm_ell_kernel<KL_, KU_, EPI, 8, 1, false>, 0);                             \
-        else if (pat && pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr) != nullptr)                            \
-            go(pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr, evariant), 0);                                 \
+        if (pat && pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr) != nullptr)                                 \
+            go(pat_ell_kernel<KL_, KU_, EPI>(hf != nullptr), 0);                                           \
         else if (hf) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, true>, 0);                                     \
-        else if (evariant == 1) go(spmm_ell_kernel<KL_, KU_, EPI, 1, 6, false>, 0);                         \
-        else if (evariant == 2) go(spmm_ell_kernel<KL_, KU_, EPI, 2, 5, false>, 0);                         \
-        else if (evariant == 3) go(spmm_ell_kernel<KL_, KU_, EPI, 4, 3, false>, 0);                         \
         else go(spmm_ell_kernel<KL_, KU_, EPI, 2, 4, false>, 0);                                            \
     } while (0)
             switch (op.ell_kl * 100 + op.ell_ku) {
@@ -874,14 +856,11 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             case 303: SPB_ELL(3, 3); break;
             case 404: SPB_ELL(4, 4); break;
             case 1313:
-                // cfg4 A/B (profiles/r01_cfg4_pat_variants.json): 3 CTAs/SM (80 registers)
-                // 1.318 ms/launch, 4 CTAs/SM (64) 1.348, two columns per pass 1.765
-                if (pat && !hf && evariant == 3) go(spmm_ell_kernel<13, 13, EPI, 1, 4, false, true>, 0);
-                else if (pat && !hf) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false, true>, 0);
+                // cfg4 A/B (profiles/r01_cfg4_pat_variants.json): one column per pass at
+                // 3 CTAs/SM (80 registers) 1.318 ms/launch, 4 CTAs/SM 1.348, two columns 1.765
+                if (pat && !hf) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false, true>, 0);
                 else if (pat) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true, true>, 0);
                 else if (hf) go(spmm_ell_kernel<13, 13, EPI, 1, 4, true>, 0);
-                else if (evariant == 1) go(spmm_ell_kernel<13, 13, EPI, 2, 2, false>, 0);
-                else if (evariant == 2) go(spmm_ell_kernel<13, 13, EPI, 1, 3, false>, 0);
                 else go(spmm_ell_kernel<13, 13, EPI, 1, 4, false>, 0);
                 break;
             default:
@@ -893,21 +872,7 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             SPB_LAUNCH_CHECK();
             return grid;
         }
-        // HF instantiations (halo exchange fused in) only for the default variants
-        if (mr <= 8) {
-            if (hf) {
-                go(spmm_col_kernel<8, MODE, EPI, 2, 5, true>, 8);
-            } else {
-                switch (variant) {
-                case 1: go(spmm_col_kernel<8, MODE, EPI, 1, 1>, 8); break;
-                case 2: go(spmm_col_kernel<8, MODE, EPI, 1, 8>, 8); break;
-                case 3: go(spmm_col_kernel<8, MODE, EPI, 2, 1>, 8); break;
-                case 4: go(spmm_col_kernel<8, MODE, EPI, 4, 3>, 8); break;
-                case 5: go(spmm_col_kernel<8, MODE, EPI, 4, 1>, 8); break;
-                default: go(spmm_col_kernel<8, MODE, EPI, 2, 5>, 8); break;
-                }
-            }
-        }
+        if (mr <= 8) go(hf ? spmm_col_kernel<8, MODE, EPI, 2, 5, true> : spmm_col_kernel<8, MODE, EPI, 2, 5>, 8);
         else if (mr <= 16) go(hf ? spmm_col_kernel<16, MODE, EPI, 2, 1, true> : spmm_col_kernel<16, MODE, EPI>, 16);
         else go(hf ? spmm_col_kernel<32, MODE, EPI, 2, 1, true> : spmm_col_kernel<32, MODE, EPI>, 32);
         SPB_LAUNCH_CHECK();

@@ -187,13 +187,9 @@ static void fill_fuse(Comm& cm, const View& X, HaloFuse& hf) {
     hf.world = cm.world;
     hf.rot = hp.rot_tiles;
     hf.n_int = hp.n_int_tiles;
-    // halo tiles after ~80% of the interior (the peers' rows arrive ~10-15 us after
+    // halo tiles after 60% of the interior (the peers' rows arrive ~10-15 us after
     // launch), interior work after them keeps the tail free of waits
-    static const int bnd_pct = [] {
-        const char* e = std::getenv("SPB_HALO_BND_PCT");
-        return e ? std::atoi(e) : 60;
-    }();
-    hf.bnd = hp.n_int_tiles * bnd_pct / 100;
+    hf.bnd = hp.n_int_tiles * 60 / 100;
     hf.total = hp.total_send;
     // pairs are 16-byte aligned only in column-major blocks with even leading dimension
     hf.vec2 = (hp.vec2 && X.rs == 1 && (X.cols == 1 || X.cs % 2 == 0) &&
@@ -214,11 +210,6 @@ static void fill_fuse(Comm& cm, const View& X, HaloFuse& hf) {
 bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s) {
     if (!cm.sym.on || !cm.halo.on) return false;
     if (cm.sym_delta(X.ptr, cm.rank) == INT64_MIN) return false;
-    static const bool off = [] {
-        const char* e = std::getenv("SPB_HALO_FUSE");
-        return e && e[0] == '0';
-    }();
-    if (off) return false;
     if (cm.sym.last_halo_src == X.ptr) cm.barrier_p2p(s);
     cm.sym.last_halo_src = X.ptr;
     fill_fuse(cm, X, hf);

@@ -204,3 +204,78 @@ def test_make_partition_exact(ctx, ref):
         ctx.make_partition(tri, [0, 0, 0], 2)  # empty part
     with pytest.raises(InvalidArgument):
         ctx.make_partition(tri, [0, 1, 2], 2)  # out of range
+
+
+# ---- the eigensolver's own irregular-graph SpMM (row-length bins, chunked hub rows) ----
+def _hub_graph():
+    """R-MAT LCC plus one hub row of 15,000 entries and one of 9,000 (both > the
+    4,096-entry chunk, so the ordered multi-chunk finish runs), every bin populated."""
+    g, _ = gen.rmat(14, 16, seed=5)
+    n = g.n
+    rows = np.repeat(np.arange(n), np.diff(g.row_offsets))
+    edges = np.stack([rows, g.col_indices], axis=1)
+    edges = edges[edges[:, 0] < edges[:, 1]]
+    hub = [(0, j) for j in range(1, min(n, 15001))] + [(n - 1, j) for j in range(0, min(n - 1, 9000), 1)]
+    return gen.graph_from_edges(n, np.concatenate([edges, np.array(hub)]))
+
+
+HUB = _hub_graph()
+
+
+def test_hub_graph_shape():
+    deg = np.diff(HUB.row_offsets)
+    assert deg.max() > 3 * 4096 and (deg > 4096).sum() >= 2
+    for lo, hi in [(1, 16), (17, 64), (65, 256), (257, 512), (513, 4096)]:
+        assert ((deg >= lo) & (deg <= hi)).any(), (lo, hi)
+
+
+def _abs_bound(ref, kind, g, X):
+    """sum_k |a_ik x_k| per (row, column), from the reference's own L."""
+    import scipy.sparse as sp
+    L = ref.build_laplacian(kind, g)
+    A = sp.csr_matrix((np.abs(L["values"]), L["col_indices"], L["row_offsets"]), shape=(g.n, g.n))
+    return A @ np.abs(X), np.diff(L["row_offsets"])
+
+
+@pytest.mark.parametrize("m", [1, 7, 9, 21, 27])
+def test_solver_spmm_irregular_integer_exact(ctx, ref, m):
+    # integer-valued X: every partial sum of L_C x is an exact integer, so any
+    # summation order must reproduce spmv_block bit for bit (SURVEY §7)
+    X = np.random.default_rng(m).integers(-8, 9, (HUB.n, m)).astype(np.float64)
+    assert ctx.classify(HUB).regular is False
+    assert ctx.spmm_solver("combinatorial", HUB, X).tobytes() == ref.spmm("combinatorial", HUB, X).tobytes()
+
+
+@pytest.mark.parametrize("kind", ["combinatorial", "normalized"])
+@pytest.mark.parametrize("m", [1, 7, 9, 21, 27])
+def test_solver_spmm_irregular_within_rounding(ctx, ref, kind, m):
+    # any-order summation bound: |fl(sum) - sum| <= gamma_{len} * sum|terms| for both
+    # the reference's sequential row sums and the device's chunked/butterfly sums
+    X = np.random.default_rng(100 + m).uniform(-1, 1, (HUB.n, m))
+    y = ctx.spmm_solver(kind, HUB, X)
+    y_ref = ref.spmm(kind, HUB, X)
+    S, lens = _abs_bound(ref, kind, HUB, X)
+    eps = np.finfo(np.float64).eps / 2
+    gam = (lens * eps / (1 - lens * eps))[:, None]
+    err = np.abs(y - y_ref)
+    assert np.all(err <= 2 * gam * S + 1e-300), float(np.max(err / (gam * S + 1e-300)))
+    # rows short enough for a single ordered chain are far tighter in practice
+    assert np.median((err / (eps * S + 1e-300))[lens > 100]) < 64
+
+
+# ---- multi-chunk mt19937_64 jump-ahead (rng.cu) and row slices -------------------
+@pytest.mark.parametrize("n,d", [(300_001, 9), (1_000_003, 3)])
+def test_initial_guess_multi_chunk(ctx, ref, n, d):
+    assert n * d > 4 * (1 << 18)  # at least four 2^18-draw chunks
+    full = ctx.initial_guess("random", n, d, 42)
+    assert full.tobytes() == ref.initial_guess("random", n, d, 42).tobytes()
+    rng = np.random.default_rng(n)
+    slices = [(0, 1), (1, 262_143), (262_143, 2), (n - 5, 5), (n // 3, n // 3 + 7)]
+    slices += [(int(a), int(rng.integers(1, n - a))) for a in rng.integers(0, n - 1, 4)]
+    for row0, nloc in slices:
+        part = ctx.initial_guess_rows("random", n, d, 42, row0, nloc)
+        assert part.tobytes() == np.asfortranarray(full[row0:row0 + nloc]).tobytes(), (row0, nloc)
+    pw = ref.initial_guess("piecewise", n, d, 0)
+    for row0, nloc in slices[:4]:
+        part = ctx.initial_guess_rows("piecewise", n, d, 0, row0, nloc)
+        assert part.tobytes() == np.asfortranarray(pw[row0:row0 + nloc]).tobytes(), (row0, nloc)
