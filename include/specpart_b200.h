@@ -56,9 +56,11 @@ enum { SP_INIT_AUTO = 0, SP_INIT_RANDOM = 1, SP_INIT_PIECEWISE = 2 };
 enum { SP_LAP_COMBINATORIAL = 0, SP_LAP_NORMALIZED = 1, SP_LAP_DEGREE = 2 };
 
 /* report warnings bitmask (pipeline.cpp:140-148, 161-163) */
-enum { SP_WARN_BREAKDOWN_RECOVERED = 1, SP_WARN_UNCONVERGED = 2, SP_WARN_IMBALANCE = 4 };
+enum { SP_WARN_BREAKDOWN_RECOVERED = 1, SP_WARN_UNCONVERGED = 2, SP_WARN_IMBALANCE = 4,
+       SP_WARN_AMG_STAGNATED = 8 /* pipeline.cpp:116-117 */ };
 
 #define SP_MAX_EIG 64
+#define SP_MAX_AMG_LEVELS 20
 
 /* Graph (graph.hpp:17-32): symmetric CSR adjacency without stored self-loops,
  * column indices strictly increasing per row. values == NULL means unit edge
@@ -160,6 +162,12 @@ typedef struct sp_report {
      * eigensolver.hpp:28-35): n x d column-major, B-orthonormal; column 0 is the
      * one embed() drops (partitioner.cpp:19-25). NULL = not wanted. */
     double* eigenvectors_out;
+    /* RunReport::amg_levels (pipeline.hpp:48-51, 74): rows and stored entries per
+     * level of the AMG hierarchy, 0 levels when AMG did not run */
+    int32_t amg_levels;
+    int32_t pad1;
+    int64_t amg_n[SP_MAX_AMG_LEVELS];
+    int64_t amg_nnz[SP_MAX_AMG_LEVELS];
 } sp_report;
 
 typedef struct sp_context sp_context;
@@ -287,8 +295,9 @@ sp_status sp_initial_guess_rows(sp_context* ctx, int32_t init, int64_t n, int32_
                                 int64_t row0, int64_t nloc, double* X_out);
 
 /* LOBPCG (eigensolver.cpp:177-337) on the problem built from g. precond is
- * SP_PRECOND_JACOBI, SP_PRECOND_POLYNOMIAL (poly_seed feeds PolyConfig.seed) or
- * SP_PRECOND_NONE. X0 n x nev column-major. Outputs theta[nev], X n x nev,
+ * SP_PRECOND_JACOBI, SP_PRECOND_POLYNOMIAL (poly_seed feeds PolyConfig.seed),
+ * SP_PRECOND_AMG (poly_seed feeds AmgConfig.seed; regular/irregular preset by
+ * classify(g)) or SP_PRECOND_NONE. X0 n x nev column-major. Outputs theta[nev], X n x nev,
  * residual norms, converged flags, iteration count, retries. */
 sp_status sp_lobpcg(sp_context* ctx, const sp_graph* g, int32_t problem, int32_t precond,
                     uint64_t poly_seed, int32_t poly_degree, const double* X0, int32_t nev,
@@ -308,6 +317,11 @@ sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* g, uint64
 sp_status sp_mj_partition(sp_context* ctx, int64_t n, int32_t dims, const double* coords,
                           const double* weights, int64_t num_parts, int32_t* assignment_out,
                           double* part_weights_out, double* imbalance_out);
+
+/* cutsize (graph.cpp:184-196): cost of the edges whose endpoints have different
+ * ids, each undirected edge once (twice with doubled); ids are not validated. */
+sp_status sp_cutsize(sp_context* ctx, const sp_graph* g, const int32_t* assignment, int32_t doubled,
+                     double* cut_out);
 
 /* make_partition (graph.cpp:209-230): validates, tallies part weights, cut, imbalance. */
 sp_status sp_cut_imbalance(sp_context* ctx, const sp_graph* g, const int32_t* assignment,

@@ -159,6 +159,12 @@ sp_status ref_partition(const sp_graph* g, const sp_config* c, int32_t* assignme
             if (w.find("breakdown") != std::string::npos) rep->warnings |= SP_WARN_BREAKDOWN_RECOVERED;
             if (w.find("max_iters") != std::string::npos) rep->warnings |= SP_WARN_UNCONVERGED;
             if (w.find("imbalance") != std::string::npos) rep->warnings |= SP_WARN_IMBALANCE;
+            if (w.find("amg coarsening stagnated") != std::string::npos) rep->warnings |= SP_WARN_AMG_STAGNATED;
+        }
+        rep->amg_levels = static_cast<int32_t>(std::min<size_t>(R.amg_levels.size(), SP_MAX_AMG_LEVELS));
+        for (int32_t l = 0; l < rep->amg_levels; ++l) {
+            rep->amg_n[l] = R.amg_levels[l].n;
+            rep->amg_nnz[l] = R.amg_levels[l].nnz;
         }
         rep->laplacian_s = R.times.laplacian_s;
         rep->eigensolve_s = R.times.eigensolve_s;
@@ -264,6 +270,12 @@ sp_status ref_lobpcg(const sp_graph* g, int32_t problem, int32_t precond, uint64
             pc.seed = poly_seed;
             if (poly_degree > 0) pc.degree = poly_degree;
             M = polynomial_build(p.A, pc);
+        }
+        if (precond == SP_PRECOND_AMG) {  // presets by classify (pipeline.cpp:107-112), seed from poly_seed
+            AmgConfig ac = classify(G).kind == Regularity::Regular ? AmgConfig::regular_defaults()
+                                                                   : AmgConfig::irregular_defaults();
+            ac.seed = poly_seed;
+            M = amg_build(p.A, ac);
         }
         SolverConfig sc;
         sc.nev = nev;

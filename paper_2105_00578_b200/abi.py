@@ -14,7 +14,8 @@ PRECOND = {"auto": 0, "jacobi": 1, "polynomial": 2, "amg": 3, "none": 4}
 INIT = {"auto": 0, "random": 1, "piecewise": 2}
 LAP = {"combinatorial": 0, "normalized": 1, "degree": 2}
 SP_MAX_EIG = 64
-WARN_BREAKDOWN_RECOVERED, WARN_UNCONVERGED, WARN_IMBALANCE = 1, 2, 4
+SP_MAX_AMG_LEVELS = 20
+WARN_BREAKDOWN_RECOVERED, WARN_UNCONVERGED, WARN_IMBALANCE, WARN_AMG_STAGNATED = 1, 2, 4, 8
 
 
 # ---- the reference's exception types (include/specpart/errors.hpp) ----------
@@ -104,7 +105,9 @@ class SpReport(C.Structure):
                 ("spmm_eff_bytes", C.c_double), ("poly_eff_bytes", C.c_double),
                 ("part_weights", C.POINTER(C.c_double)), ("trace", C.POINTER(SpTraceRecord)),
                 ("trace_capacity", C.c_int32), ("trace_len", C.c_int32),
-                ("eigenvectors_out", C.POINTER(C.c_double))]
+                ("eigenvectors_out", C.POINTER(C.c_double)),
+                ("amg_levels", C.c_int32), ("pad1", C.c_int32),
+                ("amg_n", C.c_int64 * SP_MAX_AMG_LEVELS), ("amg_nnz", C.c_int64 * SP_MAX_AMG_LEVELS)]
 
 
 class SpGraphInfo(C.Structure):
@@ -141,6 +144,7 @@ SIGNATURES = {
                         C.POINTER(I32), C.POINTER(I32)]),
     "sp_poly_apply": (I32, [P, I32, C.POINTER(SpGraph), U64, I32, P, I32, P, P, C.POINTER(I32)]),
     "sp_mj_partition": (I32, [P, I64, I32, P, P, I64, P, P, C.POINTER(F64)]),
+    "sp_cutsize": (I32, [P, C.POINTER(SpGraph), P, I32, C.POINTER(F64)]),
     "sp_cut_imbalance": (I32, [P, C.POINTER(SpGraph), P, I64, I32, C.POINTER(F64), C.POINTER(F64), P]),
     "sp_ingest": (I32, [P, I64, P, P, I32, C.POINTER(P)]),
     "sp_device_graph_info": (I32, [P, P, C.POINTER(SpGraphInfo)]),

@@ -158,6 +158,7 @@ class RunReport:
     imbalance: float = 0.0
     part_weights: list = field(default_factory=list)
     trace: list = field(default_factory=list)
+    amg_levels: list = field(default_factory=list)  # [(n, nnz)] per level (pipeline.hpp:48-51)
     device: dict = field(default_factory=dict)
 
 
@@ -194,6 +195,8 @@ def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> 
     if r.warnings & abi.WARN_UNCONVERGED:
         warnings.append("eigensolver reached max_iters with unconverged columns; "
                         "partitioning on partially converged eigenvectors")
+    if r.warnings & abi.WARN_AMG_STAGNATED:
+        warnings.append("amg coarsening stagnated; hierarchy stopped early")
     if r.warnings & abi.WARN_IMBALANCE:
         warnings.append(f"imbalance {r.imbalance:.6f} exceeds 1+epsilon = {1.0 + r.epsilon:.6f}")
     trace = []
@@ -213,6 +216,7 @@ def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> 
         times={"laplacian_s": r.laplacian_s, "eigensolve_s": r.eigensolve_s,
                "partition_s": r.partition_s, "total_s": r.total_s},
         cutsize=r.cutsize, imbalance=r.imbalance, part_weights=list(part_weights), trace=trace,
+        amg_levels=[(int(r.amg_n[i]), int(r.amg_nnz[i])) for i in range(r.amg_levels)],
         device={"spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
                 "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus,
                 "poly_launches": r.poly_launches, "poly_bytes": r.poly_bytes, "poly_ms": r.poly_ms,

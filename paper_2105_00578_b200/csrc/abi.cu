@@ -5,6 +5,7 @@
 #include "context.hpp"
 #include "ingest.hpp"
 #include "metrics.hpp"
+#include "amg.hpp"
 #include "mj.hpp"
 #include "solver.hpp"
 
@@ -264,6 +265,24 @@ void validate_config(int64_t n, const sp_config* cfg) {
     if (cfg->epsilon < 0.0) throw_infeasible("partition_graph: epsilon < 0");
 }
 
+// amg_build on problem.A (the explicit CSR of the Laplacian, built here) into the solver
+void setup_amg(sp_context* ctx, DevGraph& g, int lap_kind, bool regular, uint64_t seed, Solver& solver) {
+    if (ctx->comm.active()) throw SpError(SP_ERROR, "amg_build: the AMG preconditioner runs on one GPU in this build");
+    cudaStream_t s = ctx->stream;
+    DevLaplacian Lx;
+    build_laplacian(lap_kind, g, true, Lx, s);
+    CsrDev A0;
+    A0.nrows = A0.ncols = g.n_local;
+    A0.nnz = g.nnz_local + g.n_local;
+    A0.max_row = static_cast<int>(std::min<int64_t>(g.max_degree_global + 1, 1 << 30));
+    A0.offs = std::move(Lx.offs_L);
+    A0.cols = std::move(Lx.cols_L);
+    A0.vals = std::move(Lx.vals_L);
+    AmgCfg ac = regular ? AmgCfg::regular_defaults() : AmgCfg::irregular_defaults();
+    ac.seed = seed;
+    solver.build_amg(std::move(A0), std::move(Lx.diag), ac);
+}
+
 // partition_graph (pipeline.cpp:47-167) on a graph whose arrays are on the
 // device. Writes all n part ids to asg (device) and fills the report.
 void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const double* x0, DBuf<int32_t>& asg,
@@ -301,9 +320,6 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     // resolution order: classify -> precond -> (problem, tol) -> init (pipeline.cpp:66-82)
     R.precond = cfg->precond == SP_PRECOND_AUTO ? (kind.regular ? SP_PRECOND_AMG : SP_PRECOND_POLYNOMIAL)
                                                 : cfg->precond;
-    if (R.precond == SP_PRECOND_AMG)
-        throw SpError(SP_ERROR, "AMG preconditioner is outside this build's hot path (SURVEY §8(f) rank 1); "
-                                "pass precond=jacobi or polynomial");
     const auto [auto_problem, auto_tol] = select_defaults(kind.regular, R.precond);
     R.problem = cfg->problem == SP_PROBLEM_AUTO ? auto_problem : cfg->problem;
     R.tol = cfg->tol > 0.0 ? cfg->tol : auto_tol;
@@ -340,6 +356,16 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     } else if (R.precond == SP_PRECOND_POLYNOMIAL) {
         solver.build_poly(cfg->seed ^ 0x706f6c79ULL, 25);
         R.poly_degree = static_cast<int32_t>(solver.roots().size());
+    } else if (R.precond == SP_PRECOND_AMG) {
+        // pipeline.cpp:107-118: regular / irregular presets, seed ^ "amg"
+        setup_amg(ctx, g, operator_kind(R.problem), kind.regular, cfg->seed ^ 0x616d67ULL, solver);
+        const Amg* amg = solver.amg();
+        R.amg_levels = std::min(amg->levels(), SP_MAX_AMG_LEVELS);
+        for (int l = 0; l < R.amg_levels; ++l) {
+            R.amg_n[l] = amg->level_n(l);
+            R.amg_nnz[l] = amg->level_nnz(l);
+        }
+        if (amg->stagnated()) R.warnings |= SP_WARN_AMG_STAGNATED;
     } else {
         solver.set_none();
     }
@@ -781,6 +807,7 @@ sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const
         sp.gram = true;
         sp.gram_left_u = true;
         sp.gram_left_self = false;
+        SPB_CUDA(cudaMemsetAsync(scratch.p + scratch.n - 1, 0, sizeof(double), s));
         if (n > 0) ts_run(sp, gd.p, scratch.p, scratch.n, s);
         else SPB_CUDA(cudaMemsetAsync(gd.p, 0, sizeof(double) * mu * mv, s));
         SPB_CUDA(cudaMemcpyAsync(G, gd.p, sizeof(double) * mu * mv, cudaMemcpyDeviceToHost, s));
@@ -815,6 +842,7 @@ sp_status sp_bench_blockop(sp_context* ctx, int64_t n, int32_t mu, int32_t mv, i
         sp.gram = gram != 0;
         sp.gram_left_u = gram == 1 || gram == 2;
         sp.gram_left_self = gram == 1 || gram == 3;
+        SPB_CUDA(cudaMemsetAsync(scratch.p + scratch.n - 1, 0, sizeof(double), s));
         ts_run(sp, gb.p, scratch.p, scratch.n, s);
         cudaEvent_t e0, e1;
         SPB_CUDA(cudaEventCreate(&e0));
@@ -883,6 +911,8 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
             solver.set_jacobi(inv.p);
         } else if (precond == SP_PRECOND_POLYNOMIAL) {
             solver.build_poly(poly_seed, poly_degree > 0 ? poly_degree : 25);
+        } else if (precond == SP_PRECOND_AMG) {
+            setup_amg(ctx, g, operator_kind(problem), classify(g).regular, poly_seed, solver);
         }
         const int64_t nloc = g.n_local;
         DBuf<double> Xb;
@@ -979,6 +1009,19 @@ sp_status sp_cut_imbalance(sp_context* ctx, const sp_graph* hg, const int32_t* a
         if (cut_out) *cut_out = pm.cut;
         if (imbalance_out) *imbalance_out = pm.imbalance;
         if (part_weights_out) std::memcpy(part_weights_out, pm.part_weights.data(), sizeof(double) * K);
+    });
+}
+
+sp_status sp_cutsize(sp_context* ctx, const sp_graph* hg, const int32_t* assignment, int32_t doubled,
+                     double* cut_out) {
+    return guarded(ctx, [&] {
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        DBuf<int32_t> a(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : hg->n, 1));
+        h2d(a.p, assignment, hg->n, s);
+        const double c = cutsize_dev(ctx, g, a.p, doubled != 0);
+        if (cut_out) *cut_out = c;
     });
 }
 

@@ -37,6 +37,10 @@ struct TsDev {
     int P, Q;
     int nb, slices;
     double* partial;
+    // fused final reduction (small Grams): the last CTA to finish sums every CTA's
+    // partial in CTA order into gram_out; counter is zero on entry and on exit
+    double* gram_out;
+    unsigned* counter;
 };
 
 constexpr int kStages = 3;
@@ -425,6 +429,7 @@ __global__ void __launch_bounds__(kTsThreads) ts_mma_kernel(const TsDev a) {
 // DMMA.8x8x4 per 8-row strip; the Gram splits the tile's k-steps over the
 // warps; per-warp fragments are summed in a fixed order (deterministic).
 constexpr int kBulkMaxBlk = 9;
+constexpr size_t kFusedGramMax = 64;  // P*Q up to which the bulk kernel reduces its own Gram
 constexpr int kBulkThreads = kTsThreads + 32;  // 8 consumer warps + 1 producer warp
 
 // Stage layout (columns of SC doubles): U [0, u) | V [cV, cV+kv) | 3 zero | b.
@@ -666,6 +671,26 @@ __global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a,
         for (int w = 0; w < kTsThreads / 32; ++w) sum += red[(w * nblk + blk) * 64 + off];
         part[i2 + j * a.P] = sum;
     }
+    if (!a.counter) return;
+    // last CTA: fixed-order (CTA 0, 1, ...) sum of the partials — the result does not
+    // depend on which CTA finishes last (deterministic, same order as reduce_gram_kernel)
+    __shared__ unsigned ticket;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) ticket = atomicAdd(a.counter, 1u);
+    __syncthreads();
+    if (ticket != gridDim.x - 1) return;
+    __threadfence();
+    const int PQ = a.P * a.Q;
+    const int lane2 = threadIdx.x & 31;
+    for (int e = warp; e < PQ; e += kBulkThreads / 32) {
+        double s = 0.0;
+        for (int r = lane2; r < static_cast<int>(gridDim.x); r += 32) s += __ldcg(a.partial + static_cast<int64_t>(r) * PQ + e);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane2 == 0) a.gram_out[e] = s;
+    }
+    if (threadIdx.x == 0) *a.counter = 0u;
 }
 
 __global__ void reduce_gram_kernel(const double* partial, int rows, int PQ, double* out) {
@@ -878,7 +903,8 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
             const int64_t nt2 = (s.n + g.TR - 1) / g.TR;
             int gridb = grid_for(nt2, 1, per_sm);
             if (a.gram) {
-                while (static_cast<size_t>(gridb) * PQ > scratch_elems && gridb > 1) gridb = (gridb + 1) / 2;
+                // the last scratch element is the fused reduction's counter
+                while (static_cast<size_t>(gridb) * PQ + 1 > scratch_elems && gridb > 1) gridb = (gridb + 1) / 2;
             }
             static void (*const kerns[kBulkMaxBlk + 1])(const TsDev, const BulkCfg) = {
                 ts_bulk_kernel<0>, ts_bulk_kernel<1>, ts_bulk_kernel<2>, ts_bulk_kernel<3>, ts_bulk_kernel<4>,
@@ -889,9 +915,14 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
                     SPB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
                 attr_set = true;
             }
+            // small Grams reduce inside the kernel (the last CTA); larger ones keep the
+            // separate wide reduction (one warp per element over every CTA)
+            const bool fused = a.gram && PQ <= kFusedGramMax && scratch_elems >= PQ * gridb + 1;
+            a.gram_out = fused ? gram_out : nullptr;
+            a.counter = fused ? reinterpret_cast<unsigned*>(scratch + scratch_elems - 1) : nullptr;
             kerns[nblk_b]<<<gridb, kBulkThreads, smb, st>>>(a, g);
             SPB_LAUNCH_CHECK();
-            if (a.gram) {
+            if (a.gram && !fused) {
                 reduce_gram_kernel<<<ceil_div(static_cast<int64_t>(PQ), 4), 128, 0, st>>>(scratch, gridb,
                                                                                       static_cast<int>(PQ), gram_out);
                 SPB_LAUNCH_CHECK();

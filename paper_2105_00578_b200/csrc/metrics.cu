@@ -166,7 +166,15 @@ PartitionMetrics make_partition_dev(sp_context* ctx, const DevGraph& g, const in
     for (double w : out.part_weights)
         if (w <= 0.0) throw_invalid("make_partition: empty part");
 
-    // cutsize (graph.cpp:184-196)
+    out.cut = cutsize_dev(ctx, g, a_global, doubled);
+    out.imbalance = imbalance_of(out.part_weights);
+    return out;
+}
+
+// cutsize (graph.cpp:184-196): no validation of the ids, as in the reference
+double cutsize_dev(sp_context* ctx, const DevGraph& g, const int32_t* a_global, bool doubled) {
+    cudaStream_t s = ctx->stream;
+    const int64_t n = g.n_local;
     const int grid = grid_for(std::max<int64_t>(n, 1), kT, 4);
     DBuf<double> part(grid), tot(1);
     cut_kernel<<<grid, kT, 0, s>>>(n, g.row0, g.offs.p, g.cols.p, g.unit_values ? nullptr : g.vals.p,
@@ -174,13 +182,11 @@ PartitionMetrics make_partition_dev(sp_context* ctx, const DevGraph& g, const in
     SPB_LAUNCH_CHECK();
     sum_kernel<<<1, 32, 0, s>>>(part.p, grid, tot.p);
     SPB_LAUNCH_CHECK();
-    cm.sum_small(tot.p, 1, s);
+    ctx->comm.sum_small(tot.p, 1, s);
     double cut = 0.0;
     SPB_CUDA(cudaMemcpyAsync(&cut, tot.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     SPB_CUDA(cudaStreamSynchronize(s));
-    out.cut = doubled ? 2.0 * cut : cut;
-    out.imbalance = imbalance_of(out.part_weights);
-    return out;
+    return doubled ? 2.0 * cut : cut;
 }
 
 // imbalance (graph.cpp:198-207)

@@ -18,5 +18,6 @@ struct PartitionMetrics {
 PartitionMetrics make_partition_dev(sp_context* ctx, const DevGraph& g, const int32_t* a_global,
                                     int64_t K, bool doubled);
 double imbalance_of(const std::vector<double>& part_weights);
+double cutsize_dev(sp_context* ctx, const DevGraph& g, const int32_t* a_global, bool doubled);
 
 } // namespace spb

@@ -65,11 +65,9 @@ struct DevOp {
     const int32_t* ell_pat_tab = nullptr;
     const double* ell_pat_deg = nullptr;
     int ell_npat = 0;
-    // band-staged SpMM (spmm_band.cu): the pattern offsets fall into band_n narrow
-    // bands [band_lo, band_hi] (band_plan); 0 = not planned
-    int band_n = 0;
-    int band_lo[4] = {0, 0, 0, 0};
-    int band_hi[4] = {0, 0, 0, 0};
+    // structured mesh (spmm_mesh.cu): row (z*ny + y)*nx + x has exactly the in-bounds
+    // points of its 5/7/27-point stencil (mesh_plan); 0 = not recognised
+    int mesh_nx = 0, mesh_ny = 0, mesh_nz = 0;
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -115,12 +113,11 @@ struct EllPatStore {
     DBuf<double> deg;
 };
 bool build_ell_patterns(DevOp& op, EllPatStore& st, cudaStream_t s);
-// Band-staged SpMM on pattern-compressed meshes (spmm_band.cu): band_plan clusters
-// the pattern offsets into <= kMaxBands bands (false: no plan, op unchanged).
-constexpr int kMaxBands = 4;
-bool band_plan(DevOp& op, cudaStream_t s);
-bool spmm_band_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
-int spmm_band_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
+// Structured-mesh SpMM (spmm_mesh.cu): mesh_plan recognises a naturally ordered
+// 5/7/27-point box mesh behind a pattern-compressed ELL (false: op unchanged).
+bool mesh_plan(DevOp& op, cudaStream_t s);
+bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
 // Row-length bins for the vector SpMM (spmm_vec.cu); also sets the long-row list.
 struct RowBins {
     DBuf<int32_t> rows;
@@ -155,7 +152,9 @@ struct TsSpec {
 enum { TS_NONE = 0, TS_UPDATE = 1, TS_COMBINE = 2 };
 
 // Runs the tile kernel; if spec.gram, writes the (P x Q) column-major Gram to
-// gram_out (device) and returns P. Deterministic for a fixed n.
+// gram_out (device) and returns P. Deterministic for a fixed n. The last element
+// of scratch is a reduction counter: it must hold 0 (as unsigned) on the first
+// call, and every call leaves it 0.
 int ts_run(const TsSpec& spec, double* gram_out, double* scratch, size_t scratch_elems,
            cudaStream_t s);
 

@@ -101,16 +101,17 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     if (colmajor_ && build_ell(A_, n_, ell_, s_)) {
         const int kk = A_.ell_kl * 100 + A_.ell_ku;
         if ((kk == 202 || kk == 303 || kk == 1313) && build_ell_patterns(A_, ellpat_, s_) && !halo_) {
-            static const bool no_band = [] {  // A/B diagnostics only
-                const char* e = std::getenv("SPB_BAND");
+            static const bool no_mesh = [] {  // A/B diagnostics only
+                const char* e = std::getenv("SPB_MESH");
                 return e && e[0] == '0';
             }();
-            if (!no_band) band_plan(A_, s_);
+            if (!no_mesh) mesh_plan(A_, s_);
         }
     }
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
+    SPB_CUDA(cudaMemsetAsync(scratch_.p, 0, sizeof(double) * scratch_.n, s_));  // ts_run's counter word
     cmat_.alloc(static_cast<size_t>(m3) * m3 + 64);
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
     partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 * 5 + A.n_long + 64) * 64);
@@ -479,6 +480,10 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         jacobi_apply(n_, inv_diag_, R.sub(0, k), H.sub(0, k), s_);
         return;
     }
+    if (prec_ == PREC_AMG) {
+        amg_->apply(R, k, H);
+        return;
+    }
     // GMRES polynomial, product form (preconditioners.cpp:171-193), one fused
     // SpMM per root: prod_{i+1} = prod_i - A prod_i / theta_i, H += prod_{i+1}/theta_{i+1}
     const int deg = static_cast<int>(roots_.size());
@@ -501,6 +506,15 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         spmm(cur, k, ea);
         cur = nxt;
     }
+}
+
+void Solver::build_amg(CsrDev&& A0, DBuf<double>&& diag0, const AmgCfg& cfg) {
+    if (halo_) throw SpError(1, "amg_build: the AMG preconditioner runs on one GPU in this build");
+    amg_ = std::make_unique<Amg>(
+        ctx_, std::move(A0), std::move(diag0), cfg, [this](const View& X, int m, const View& Y) { spmm_store(X, m, Y); },
+        [this](int cols, DBuf<double>& store) { return input_block(cols, store); },
+        [this](double* p, int cols) { return block(p, cols); }, max_cols_);
+    prec_ = PREC_AMG;
 }
 
 void Solver::build_poly(uint64_t seed, int degree) {

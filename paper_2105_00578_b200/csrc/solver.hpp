@@ -2,14 +2,17 @@
 #pragma once
 
 #include "context.hpp"
+#include "amg.hpp"
 #include "dense_host.hpp"
+
+#include <memory>
 
 #include <algorithm>
 #include <vector>
 
 namespace spb {
 
-enum PrecKind { PREC_NONE = 0, PREC_JACOBI = 1, PREC_POLY = 2 };
+enum PrecKind { PREC_NONE = 0, PREC_JACOBI = 1, PREC_POLY = 2, PREC_AMG = 3 };
 
 struct TraceRec {
     int iter = 0;
@@ -48,6 +51,9 @@ public:
 
     void set_jacobi(const double* inv_diag_dev) { prec_ = PREC_JACOBI; inv_diag_ = inv_diag_dev; }
     void set_none() { prec_ = PREC_NONE; }
+    // amg_build (preconditioners.cpp:722-728) on the explicit fine operator A0 (moved in)
+    void build_amg(CsrDev&& A0, DBuf<double>&& diag0, const AmgCfg& cfg);
+    const Amg* amg() const { return amg_.get(); }
     // polynomial_build (preconditioners.cpp:315-382): seeded Arnoldi -> harmonic
     // Ritz roots in Leja order. Throws on degree < 1.
     void build_poly(uint64_t seed, int degree);
@@ -102,6 +108,7 @@ private:
     PrecKind prec_ = PREC_NONE;
     const double* inv_diag_ = nullptr;
     std::vector<double> roots_;
+    std::unique_ptr<Amg> amg_;
 
     DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
     EllPatStore ellpat_; // its pattern-compressed form (ellpat.cu)

@@ -1,0 +1,418 @@
+// spmm_mesh.cu — SpMM on naturally ordered structured meshes: TMA 3-D tiles, z-marching.
+//
+// Same operator, slots, summation order and epilogues as spmm_ell_kernel (spmm.cu),
+// hence the same bit-exact result as kernels::spmv_block (src/kernels.cpp:36-62) on
+// L_C; only the data movement differs.
+//
+// The graphs of generators.cpp:126-162 (grid2d, stencil3d 7/27) number vertex
+// (x, y, z) as (z*ny + y)*nx + x, so every row's neighbours are the in-bounds
+// points of a 3x3x3 box around it. mesh_plan recognises that structure from the
+// pattern-compressed ELL (the offsets decompose as dz*nx*ny + dy*nx + dx and
+// every row's pattern is exactly its in-bounds stencil, verified on the device).
+//
+// A CTA owns a 32x32 (x, y) tile of one block column and marches a chunk of z
+// planes. A producer warp loads each plane of X as one 34x34 box (the tile plus
+// its x/y halo) with a 4-D tensor-map TMA copy (out-of-range halo is zero-filled
+// by the TMA unit), plus the 32x32 box of H the POLY epilogue reads, into a ring
+// of shared-memory stages tracked by mbarriers. Consumer warps compute plane z
+// from the stages of planes z-1, z, z+1 — each X element crosses L2 -> SM about
+// 1.13x (the halo) instead of the ~3x of per-plane gathers (z-1, z, z+1 reads of
+// the same element from three different tiles) — and write Y (and H) with
+// coalesced 256-byte warp stores.
+#include "bulk.cuh"
+#include "ops.cuh"
+#include "spmm_epilogue.cuh"
+
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+namespace spb {
+
+namespace {
+
+constexpr int kTile = 32;                 // x and y extent of a tile
+constexpr int kHaloW = kTile + 2;         // 34: tile + one halo point each side
+constexpr int kConsumers = 256;           // 8 consumer warps; warp w owns tile rows w, w+8, w+16, w+24
+constexpr int kMeshThreads = kConsumers + 32;
+constexpr int kXPlane = kHaloW * kHaloW;                       // doubles of an X box
+constexpr int kXPlanePad = ((kXPlane * 8 + 127) / 128) * 16;   // 128-byte aligned (in doubles)
+constexpr int kHPlane = kTile * kTile;
+constexpr int kMaxStages = 8;
+
+struct MeshGeo {
+    int nx, ny, nz;
+    int ntx, nty;       // tiles per plane
+    int zc, nzc;        // z planes per chunk, chunks
+    int nst;            // ring stages
+    int h_stage;        // stages carry the H box (POLY with an H read)
+    int stage;          // doubles per stage
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int KL, int KU, int EPI>
+__global__ void __launch_bounds__(kMeshThreads, 2)
+    spmm_mesh_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, const DevOp op,
+                     const EpiArgs ea, const int m, const MeshGeo geo) {
+    constexpr int W = KL + KU;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ int16_t s_code[256 * W];  // per (pattern, slot): (dz+1)*128 + (dy+1)*34 + (dx+1), -1 = padding
+    __shared__ double s_deg[256];
+    __shared__ double s_theta[kMaxCols];
+    __shared__ double s_sq[kConsumers / 32][kMaxCols];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int nxny = geo.nx * geo.ny;
+
+    if (tid == 0) {
+        for (int s = 0; s < geo.nst; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int e = tid; e < op.ell_npat * W; e += kMeshThreads) {
+        const int32_t d = op.ell_pat_tab[e];
+        int v = -1;
+        if (d != kEllPad) {
+            // d = dz*nxny + dy*nx + dx with dz, dy, dx in {-1, 0, 1} (mesh_plan checked it)
+            const int dz = d > nxny / 2 ? 1 : (d < -nxny / 2 ? -1 : 0);
+            const int r = d - dz * nxny;
+            const int dy = r > geo.nx / 2 ? 1 : (r < -geo.nx / 2 ? -1 : 0);
+            const int dx = r - dy * geo.nx;
+            v = (dz + 1) * 128 + (dy + 1) * kHaloW + (dx + 1);
+        }
+        s_code[e] = static_cast<int16_t>(v);
+    }
+    for (int e = tid; e < op.ell_npat; e += kMeshThreads) s_deg[e] = op.ell_pat_deg[e];
+    if (EPI == EPI_RESIDUAL) {
+        for (int c = tid; c < m; c += kMeshThreads) s_theta[c] = ea.theta[c];
+        for (int e = tid; e < (kConsumers / 32) * kMaxCols; e += kMeshThreads) (&s_sq[0][0])[e] = 0.0;
+    }
+    __syncthreads();
+
+    const int64_t items = static_cast<int64_t>(geo.ntx) * geo.nty * geo.nzc * m;
+    // item -> (column, z chunk, tile y, tile x); columns innermost so concurrent CTAs share planes in L2
+    auto decode = [&](int64_t it, int& c, int& tx, int& ty, int& z0, int& z1) {
+        c = static_cast<int>(it % m);
+        int64_t r = it / m;
+        tx = static_cast<int>(r % geo.ntx);
+        r /= geo.ntx;
+        ty = static_cast<int>(r % geo.nty);
+        const int zq = static_cast<int>(r / geo.nty);
+        z0 = zq * geo.zc;
+        z1 = min(geo.nz, z0 + geo.zc);
+    };
+    const unsigned xbytes = kXPlane * 8u, hbytes = geo.h_stage ? kHPlane * 8u : 0u;
+
+    if (warp == kConsumers / 32) {
+        if (lane == 0) {
+            int s = 0;
+            unsigned eph = 0;
+            int64_t g = 0;  // stage sequence number
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                int c, tx, ty, z0, z1;
+                decode(it, c, tx, ty, z0, z1);
+                // stage p carries X plane p and (POLY) the H box of output plane p - 1
+                for (int p = z0 - 1; p <= z1; ++p, ++g) {
+                    if (g >= geo.nst) mbar_wait(empty + s, eph);
+                    double* st = smem + static_cast<size_t>(s) * geo.stage;
+                    mbar_expect_tx(full + s, xbytes + hbytes);
+                    tma_load_4d(st, &xmap, tx * kTile - 1, ty * kTile - 1, p, c, full + s);
+                    if (geo.h_stage) tma_load_4d(st + kXPlanePad, &hmap, tx * kTile, ty * kTile, p - 1, c, full + s);
+                    if (++s == geo.nst) {
+                        s = 0;
+                        if (g >= geo.nst) eph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
+    int64_t g = 0;  // sequence number of the stage holding plane z0 - 1 of the current item
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int c, tx, ty, z0, z1;
+        decode(it, c, tx, ty, z0, z1);
+        const int x = tx * kTile + lane;
+        const bool xin = x < geo.nx;
+        // planes z0 - 1 and z0 first
+        mbar_wait(full + (g % geo.nst), static_cast<unsigned>((g / geo.nst) & 1));
+        mbar_wait(full + ((g + 1) % geo.nst), static_cast<unsigned>(((g + 1) / geo.nst) & 1));
+        for (int z = z0; z < z1; ++z) {
+            const int64_t gz = g + (z - z0) + 1;  // stage of plane z
+            // pattern ids of this plane's rows (issued before the wait for plane z + 1)
+            int pid[4];
+            bool live[4];
+            int64_t row[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int y = ty * kTile + warp + 8 * j;
+                live[j] = xin && y < geo.ny;
+                row[j] = (static_cast<int64_t>(z) * geo.ny + y) * geo.nx + x;
+                pid[j] = live[j] ? static_cast<int>(__ldg(op.ell_pat + row[j])) : 0;
+            }
+            double bd[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bd[j] = (EPI == EPI_RESIDUAL && ea.bdiag && live[j]) ? ea.bdiag[row[j]] : 1.0;
+            mbar_wait(full + ((gz + 1) % geo.nst), static_cast<unsigned>(((gz + 1) / geo.nst) & 1));
+            const double* pl[3] = {smem + static_cast<size_t>((gz - 1) % geo.nst) * geo.stage,
+                                   smem + static_cast<size_t>(gz % geo.nst) * geo.stage,
+                                   smem + static_cast<size_t>((gz + 1) % geo.nst) * geo.stage};
+            const double* hs = pl[2] + kXPlanePad;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ly = warp + 8 * j;
+                const int base = ly * kHaloW + lane;  // (dy+1)*34 + (dx+1) added per slot
+                const double xi = pl[1][base + kHaloW + 1];
+                double acc = 0.0;
+                // acc -= x_j over the lower slots, += deg * x_i, -= x_j over the upper slots:
+                // the storage order of build_combinatorial's row (bit-identical to spmv_block)
+#pragma unroll
+                for (int sl = 0; sl < KL; ++sl) {
+                    const int code = s_code[pid[j] * W + sl];
+                    if (code >= 0) acc = __dsub_rn(acc, pl[code >> 7][base + (code & 127)]);
+                }
+                acc = __dadd_rn(acc, __dmul_rn(s_deg[pid[j]], xi));
+#pragma unroll
+                for (int sl = KL; sl < W; ++sl) {
+                    const int code = s_code[pid[j] * W + sl];
+                    if (code >= 0) acc = __dsub_rn(acc, pl[code >> 7][base + (code & 127)]);
+                }
+                double sq = 0.0;
+                if (live[j]) {
+                    if (EPI == EPI_STORE) {
+                        ea.Y.at(row[j], c) = acc;
+                    } else if (EPI == EPI_RESIDUAL) {
+                        const double bx = ea.bdiag ? __dmul_rn(bd[j], xi) : xi;
+                        const double r = __dsub_rn(acc, __dmul_rn(s_theta[c], bx));
+                        ea.Y.at(row[j], c) = r;
+                        sq = r * r;
+                    } else {
+                        const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
+                        ea.Y.at(row[j], c) = pn;
+                        if (ea.h_terms) {
+                            const double hv = geo.h_stage ? hs[ly * kTile + lane] : 0.0;
+                            ea.H.at(row[j], c) = poly_h(ea, hv, xi, pn);
+                        }
+                    }
+                }
+                if (EPI == EPI_RESIDUAL) {
+                    double v = sq;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    if (lane == 0) s_sq[warp][c] += v;
+                }
+            }
+            // plane z - 1 is no longer needed by this item
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + ((gz - 1) % geo.nst)))
+                             : "memory");
+        }
+        // release planes z1 - 1 and z1
+        const int64_t gl = g + (z1 - z0);
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + (gl % geo.nst))) : "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + ((gl + 1) % geo.nst)))
+                         : "memory");
+        }
+        g += (z1 - z0) + 2;
+    }
+    if (EPI == EPI_RESIDUAL) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+        for (int c = tid; c < m; c += kConsumers) {
+            double v = 0.0;
+            for (int w = 0; w < kConsumers / 32; ++w) v += s_sq[w][c];
+            ea.partial[static_cast<int64_t>(blockIdx.x) * m + c] = v;
+        }
+    }
+}
+
+// ---- tensor maps (driver entry point: the library links only the runtime) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) {
+            cudaGetLastError();
+            return static_cast<EncodeTiledFn>(nullptr);
+        }
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// the block as a 4-D tensor (x, y, z, column) of doubles
+void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_xy) {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(op.mesh_nx), static_cast<cuuint64_t>(op.mesh_ny),
+                                static_cast<cuuint64_t>(op.mesh_nz), static_cast<cuuint64_t>(m)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(op.mesh_nx) * 8,
+                                   static_cast<cuuint64_t>(op.mesh_nx) * op.mesh_ny * 8,
+                                   static_cast<cuuint64_t>(m > 1 ? v.cs : (op.n + 1) & ~int64_t(1)) * 8};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_xy), static_cast<cuuint32_t>(box_xy), 1, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, v.ptr, dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw SpError(8, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+}
+
+template <int KL, int KU, int EPI>
+int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
+    MeshGeo geo{};
+    geo.nx = op.mesh_nx;
+    geo.ny = op.mesh_ny;
+    geo.nz = op.mesh_nz;
+    geo.ntx = (geo.nx + kTile - 1) / kTile;
+    geo.nty = (geo.ny + kTile - 1) / kTile;
+    geo.h_stage = (EPI == EPI_POLY && !ea.first && ea.h_terms) ? 1 : 0;
+    geo.stage = kXPlanePad + (geo.h_stage ? kHPlane : 0);
+    auto kern = spmm_mesh_kernel<KL, KU, EPI>;
+    static bool attr = false;
+    if (!attr) {
+        SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    // ring: up to 6 stages, sized so two CTAs share an SM
+    const size_t per_stage = sizeof(double) * geo.stage;
+    geo.nst = static_cast<int>(std::min<size_t>(6, (100 * 1024) / per_stage));
+    const size_t smem = per_stage * geo.nst;
+    int per_sm = 0;
+    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMeshThreads, smem));
+    const int ctas = device_sm_count() * std::max(per_sm, 1);
+    // z chunks: enough work items for ~4 per CTA, at least 8 planes per chunk (the two
+    // halo planes of a chunk are re-read from L2)
+    const int64_t per_chunk = static_cast<int64_t>(geo.ntx) * geo.nty * m;
+    int nzc = static_cast<int>(std::min<int64_t>(geo.nz, std::max<int64_t>(1, (4LL * ctas + per_chunk - 1) / per_chunk)));
+    nzc = std::min(nzc, std::max(1, geo.nz / 8));
+    geo.zc = (geo.nz + nzc - 1) / nzc;
+    geo.nzc = (geo.nz + geo.zc - 1) / geo.zc;
+    const int64_t items = per_chunk * geo.nzc;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, ctas)));
+    CUtensorMap xmap, hmap;
+    make_map(&xmap, X, m, op, kHaloW);
+    if (geo.h_stage) make_map(&hmap, ea.H, m, op, kTile);
+    else hmap = xmap;
+    kern<<<grid, kMeshThreads, smem, s>>>(xmap, hmap, op, ea, m, geo);
+    SPB_LAUNCH_CHECK();
+    return grid;
+}
+
+__global__ void mesh_verify_kernel(const DevOp op, int nx, int ny, int nz, int W, bool box27, int* bad) {
+    const int64_t nxny = static_cast<int64_t>(nx) * ny;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int x = static_cast<int>(i % nx), y = static_cast<int>((i / nx) % ny), z = static_cast<int>(i / nxny);
+        const int p = op.ell_pat[i];
+        int cnt = 0;
+        bool ok = true;
+        for (int s = 0; s < W && ok; ++s) {
+            const int32_t d = op.ell_pat_tab[p * W + s];
+            if (d == kEllPad) continue;
+            const int dz = d > nxny / 2 ? 1 : (d < -nxny / 2 ? -1 : 0);
+            const int64_t r = d - dz * nxny;
+            const int dy = r > nx / 2 ? 1 : (r < -nx / 2 ? -1 : 0);
+            const int dx = static_cast<int>(r - static_cast<int64_t>(dy) * nx);
+            ok = dx >= -1 && dx <= 1 && x + dx >= 0 && x + dx < nx && y + dy >= 0 && y + dy < ny && z + dz >= 0 &&
+                 z + dz < nz && (box27 || (dx != 0) + (dy != 0) + (dz != 0) == 1);
+            ++cnt;
+        }
+        // the row holds every in-bounds point of its stencil (offsets are sorted and distinct)
+        const int cx = 1 + (x > 0) + (x + 1 < nx), cy = 1 + (y > 0) + (y + 1 < ny), cz = 1 + (z > 0) + (z + 1 < nz);
+        const int want = box27 ? cx * cy * cz - 1 : (cx - 1) + (cy - 1) + (cz - 1);
+        if (!ok || cnt != want) atomicExch(bad, 1);
+    }
+}
+
+} // namespace
+
+bool mesh_plan(DevOp& op, cudaStream_t s) {
+    op.mesh_nx = op.mesh_ny = op.mesh_nz = 0;
+    if (!op.ell_pat || op.ell_npat <= 0 || op.row0 != 0 || op.dpos || !encode_fn()) return false;
+    const int W = op.ell_kl + op.ell_ku;
+    if (W != 4 && W != 6 && W != 26) return false;
+    std::vector<int32_t> tab(static_cast<size_t>(op.ell_npat) * W);
+    SPB_CUDA(cudaMemcpyAsync(tab.data(), op.ell_pat_tab, sizeof(int32_t) * tab.size(), cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    std::vector<int64_t> pos;
+    for (int32_t d : tab)
+        if (d != kEllPad && d > 0) pos.push_back(d);
+    std::sort(pos.begin(), pos.end());
+    pos.erase(std::unique(pos.begin(), pos.end()), pos.end());
+    // positive offsets: 5/7-point {1, nx[, nx*ny]}; 27-point {1, nx-1, nx, nx+1[, nx*ny-nx-1 .. nx*ny+nx+1]}
+    int64_t nx = 0, nxny = 0;
+    const bool box27 = W == 26;
+    if (!box27 && (pos.size() == 2 || pos.size() == 3) && pos[0] == 1) {
+        nx = pos[1];
+        nxny = pos.size() == 3 ? pos[2] : op.n;
+    } else if (box27 && (pos.size() == 4 || pos.size() == 13) && pos[0] == 1) {
+        nx = pos[2];
+        nxny = pos.size() == 13 ? pos[8] : op.n;
+    } else {
+        return false;
+    }
+    if (nx < 4 || nxny % nx || op.n % nxny) return false;
+    const int64_t ny = nxny / nx, nz = op.n / nxny;
+    if (nx % 2 || nx > (1 << 30) || ny > (1 << 30) || nz > (1 << 30)) return false;  // TMA: 16-byte strides
+    DBuf<int> bad(1);
+    SPB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    mesh_verify_kernel<<<grid_for(op.n, 256, 8), 256, 0, s>>>(op, static_cast<int>(nx), static_cast<int>(ny),
+                                                              static_cast<int>(nz), W, box27, bad.p);
+    SPB_LAUNCH_CHECK();
+    int hb = 1;
+    SPB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    if (hb) return false;
+    op.mesh_nx = static_cast<int>(nx);
+    op.mesh_ny = static_cast<int>(ny);
+    op.mesh_nz = static_cast<int>(nz);
+    return true;
+}
+
+bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
+    if (op.mesh_nx <= 0 || !op.ell_pat || op.mode != OP_LAPLACE_UNIT || op.row0 != 0 || op.dpos || m > kMaxCols)
+        return false;
+    // column-major blocks, 16-byte aligned bases and column strides (TMA global address rules)
+    auto ok = [&](const View& v) {
+        return v.rs == 1 && reinterpret_cast<uintptr_t>(v.ptr) % 16 == 0 && (m == 1 || (v.cs % 2 == 0 && v.cs >= op.n));
+    };
+    if (!ok(X) || ea.Y.rs != 1) return false;
+    if (ea.mode == EPI_POLY && ea.h_terms && !ea.first && !ok(ea.H)) return false;
+    return true;
+}
+
+int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
+    const int kk = op.ell_kl * 100 + op.ell_ku;
+    switch (ea.mode) {
+#define SPB_MESH(EPI_)                                                                  \
+    switch (kk) {                                                                     \
+    case 202: return launch_mesh<2, 2, EPI_>(op, X, m, ea, s);                        \
+    case 303: return launch_mesh<3, 3, EPI_>(op, X, m, ea, s);                        \
+    default: return launch_mesh<13, 13, EPI_>(op, X, m, ea, s);                       \
+    }
+    case EPI_STORE: SPB_MESH(EPI_STORE)
+    case EPI_RESIDUAL: SPB_MESH(EPI_RESIDUAL)
+    default: SPB_MESH(EPI_POLY)
+#undef SPB_MESH
+    }
+}
+
+} // namespace spb

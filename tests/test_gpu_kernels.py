@@ -279,3 +279,16 @@ def test_initial_guess_multi_chunk(ctx, ref, n, d):
     for row0, nloc in slices[:4]:
         part = ctx.initial_guess_rows("piecewise", n, d, 0, row0, nloc)
         assert part.tobytes() == np.asfortranarray(pw[row0:row0 + nloc]).tobytes(), (row0, nloc)
+
+
+# ---- structured-mesh SpMM (spmm_mesh.cu: TMA 3-D tiles, z-marching): bit-exact -------
+MESHES = [("st7_40x12x10", gen.stencil3d(40, 12, 10, 7)), ("st27_34x8x6", gen.stencil3d(34, 8, 6, 27)),
+          ("grid_66x40", gen.grid2d(66, 40)), ("st7_64x64x64", gen.stencil3d(64, 64, 64, 7)),
+          ("st27_32x32x40", gen.stencil3d(32, 32, 40, 27))]
+
+
+@pytest.mark.parametrize("m", [1, 3, 7, 9, 21])
+@pytest.mark.parametrize("name,g", MESHES, ids=[n for n, _ in MESHES])
+def test_spmm_bit_exact_structured_mesh(ctx, ref, name, g, m):
+    X = np.random.default_rng(m).uniform(-1, 1, (g.n, m))
+    assert ctx.spmm("combinatorial", g, X).tobytes() == ref.spmm("combinatorial", g, X).tobytes()
