@@ -312,6 +312,22 @@ sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* g, uint64
                         int32_t degree, const double* R, int32_t m, double* H_out,
                         double* roots_out, int32_t* achieved_out);
 
+/* Jacobi (jacobi_build), the GMRES polynomial (polynomial_build: seed, degree;
+ * roots_out/achieved_out as sp_poly_apply) or none, built on an explicit n x n
+ * CSR operator (make_operator, laplacian.cpp:40-51, Gershgorin bound included)
+ * and applied to R: the diagonal-operator KATs of preconditioner_test.cpp:38-118
+ * and acceptance c12 (acceptance.cpp:361-403). */
+sp_status sp_precond_apply_csr(sp_context* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
+                               const double* vals, int32_t precond, uint64_t seed, int32_t degree, const double* R,
+                               int32_t m, double* H_out, double* roots_out, int32_t* achieved_out);
+
+/* H = M R for any preconditioner of the pipeline (Preconditioner::apply,
+ * preconditioners.hpp:16-27) built on the operator of kind 0 (L_C) or 1 (L_N)
+ * from g: SP_PRECOND_JACOBI, _POLYNOMIAL (seed, degree as PolyConfig), _AMG
+ * (seed as AmgConfig.seed, preset by classify(g)), _NONE (H = R). */
+sp_status sp_precond_apply(sp_context* ctx, int32_t kind, const sp_graph* g, int32_t precond, uint64_t seed,
+                           int32_t degree, const double* R, int32_t m, double* H_out);
+
 /* Multi-jagged partitioning (partitioner.cpp:140-170) of n points with `dims`
  * coordinates (n x dims column-major), positive weights (NULL = unit). */
 sp_status sp_mj_partition(sp_context* ctx, int64_t n, int32_t dims, const double* coords,

@@ -84,6 +84,7 @@ int main(int argc, char** argv) {
     if (precond == "jacobi") cfg.precond = PrecondChoice::Jacobi;
     else if (precond == "polynomial") cfg.precond = PrecondChoice::Polynomial;
     else if (precond == "none") cfg.precond = PrecondChoice::None;
+    else if (precond == "amg") cfg.precond = PrecondChoice::Amg;
     SparseMatrix raw = parse_matrix_market_file(argv[2]);
     Graph whole = symmetrize(raw);
     auto [g, original_ids] = largest_connected_component(whole);

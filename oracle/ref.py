@@ -36,6 +36,7 @@ _SIG = {
                          C.POINTER(I32), C.POINTER(I32)]),
     "ref_poly_apply": (I32, [I32, C.POINTER(abi.SpGraph), U64, I32, P, I32, P, P, C.POINTER(I32)]),
     "ref_poly_apply_csr": (I32, [I64, P, P, P, U64, I32, P, I32, P, C.POINTER(I32)]),
+    "ref_precond_apply": (I32, [I32, C.POINTER(abi.SpGraph), I32, U64, I32, P, I32, P]),
     "ref_mj_partition": (I32, [I64, I32, P, P, I64, P, P, C.POINTER(F64)]),
     "ref_cut_imbalance": (I32, [C.POINTER(abi.SpGraph), P, I64, I32, C.POINTER(F64), C.POINTER(F64), P]),
     "ref_sym_eig": (I32, [I32, P, P, P]),
@@ -166,6 +167,15 @@ class RefLib:
                                                 vals.ctypes.data, seed, degree, Rc.ctypes.data, Rc.shape[1],
                                                 H.ctypes.data, C.byref(ach)))
         return H, ach.value
+
+    def precond_apply(self, kind: str, g: Graph, precond: str, R, seed: int = 0, degree: int = 25):
+        Rc = _colmajor(R)
+        n, m = Rc.shape
+        H = np.empty((n, m), order="F")
+        gc = g.as_c()
+        self._check(self.lib.ref_precond_apply(abi.LAP[kind], C.byref(gc), abi.PRECOND[precond], seed, degree,
+                                               Rc.ctypes.data, m, H.ctypes.data))
+        return H
 
     def mj_partition(self, coords, weights, num_parts: int) -> Partition:
         Cc = _colmajor(coords)

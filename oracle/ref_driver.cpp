@@ -336,6 +336,30 @@ sp_status ref_poly_apply_csr(int64_t n, const int64_t* offsets, const int32_t* c
     });
 }
 
+sp_status ref_precond_apply(int32_t kind, const sp_graph* g, int32_t precond, uint64_t seed, int32_t degree,
+                            const double* R, int32_t m, double* H_out) {
+    return guarded([&] {
+        Graph G = to_graph(g);
+        LinearOperator A = build_kind(kind, G);
+        std::unique_ptr<Preconditioner> M;
+        if (precond == SP_PRECOND_JACOBI) M = jacobi_build(A);
+        else if (precond == SP_PRECOND_POLYNOMIAL) {
+            PolyConfig pc;
+            pc.seed = seed;
+            if (degree > 0) pc.degree = degree;
+            M = polynomial_build(A, pc);
+        } else if (precond == SP_PRECOND_AMG) {
+            AmgConfig ac = classify(G).kind == Regularity::Regular ? AmgConfig::regular_defaults()
+                                                                   : AmgConfig::irregular_defaults();
+            ac.seed = seed;
+            M = amg_build(A, ac);
+        }
+        Dense r = to_dense(R, G.n(), m);
+        Dense h = M ? M->apply(r) : r;
+        std::memcpy(H_out, h.data.data(), sizeof(double) * G.n() * m);
+    });
+}
+
 sp_status ref_mj_partition(int64_t n, int32_t dims, const double* coords, const double* weights,
                            int64_t num_parts, int32_t* assignment_out, double* part_weights_out,
                            double* imbalance_out) {

@@ -143,6 +143,8 @@ SIGNATURES = {
     "sp_lobpcg": (I32, [P, C.POINTER(SpGraph), I32, I32, U64, I32, P, I32, F64, I32, I32, P, P, P, P,
                         C.POINTER(I32), C.POINTER(I32)]),
     "sp_poly_apply": (I32, [P, I32, C.POINTER(SpGraph), U64, I32, P, I32, P, P, C.POINTER(I32)]),
+    "sp_precond_apply_csr": (I32, [P, I64, P, P, P, I32, U64, I32, P, I32, P, P, C.POINTER(I32)]),
+    "sp_precond_apply": (I32, [P, I32, C.POINTER(SpGraph), I32, U64, I32, P, I32, P]),
     "sp_mj_partition": (I32, [P, I64, I32, P, P, I64, P, P, C.POINTER(F64)]),
     "sp_cutsize": (I32, [P, C.POINTER(SpGraph), P, I32, C.POINTER(F64)]),
     "sp_cut_imbalance": (I32, [P, C.POINTER(SpGraph), P, I64, I32, C.POINTER(F64), C.POINTER(F64), P]),

@@ -448,6 +448,32 @@ class Context:
                                            m, H.ctypes.data, roots.ctypes.data, C.byref(ach)))
         return H, roots[: ach.value]
 
+    def precond_apply_csr(self, row_offsets, col_indices, values, precond: str, R, seed: int = 0, degree: int = 25):
+        """jacobi / polynomial / none built on an explicit CSR operator and applied to R
+        (sp_precond_apply_csr). Returns (H, Leja-ordered roots) — roots empty unless polynomial."""
+        offs = np.ascontiguousarray(row_offsets, dtype=np.int64)
+        cols = np.ascontiguousarray(col_indices, dtype=np.int32)
+        vals = _f64(values)
+        Rc = _colmajor(R)
+        n, m = Rc.shape
+        H = np.empty((n, m), dtype=np.float64, order="F")
+        roots = np.empty(max(degree, 25))
+        ach = C.c_int32()
+        self._check(self.lib.sp_precond_apply_csr(self._h, n, offs.ctypes.data, cols.ctypes.data, vals.ctypes.data,
+                                                  abi.PRECOND[precond], seed, degree, Rc.ctypes.data, m,
+                                                  H.ctypes.data, roots.ctypes.data, C.byref(ach)))
+        return H, roots[: ach.value]
+
+    def precond_apply(self, kind: str, g: Graph, precond: str, R, seed: int = 0, degree: int = 25):
+        """H = M R (Preconditioner::apply) for precond in jacobi / polynomial / amg / none."""
+        Rc = _colmajor(R)
+        n, m = Rc.shape
+        H = np.empty((n, m), dtype=np.float64, order="F")
+        gc = g.as_c()
+        self._check(self.lib.sp_precond_apply(self._h, abi.LAP[kind], C.byref(gc), abi.PRECOND[precond], seed, degree,
+                                              Rc.ctypes.data, m, H.ctypes.data))
+        return H
+
     def mj_partition(self, coords, weights, num_parts: int) -> Partition:
         Cc = _colmajor(coords)
         n, dims = Cc.shape

@@ -106,20 +106,22 @@ def _build_cli(verbose: bool) -> None:
 
 
 def _build_shim_test(verbose: bool) -> None:
-    """tests/cpp/shim_test.cpp against include/specpart_b200.hpp + the library (a reference-style
-    C++ caller that compiles unchanged against the shim)."""
-    src = ROOT / "tests" / "cpp" / "shim_test.cpp"
-    exe = ROOT / "build" / "shim_test"
-    if not src.exists():
-        return
-    if exe.exists() and exe.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime,
-                                                   (ROOT / "include" / "specpart_b200.hpp").stat().st_mtime):
-        return
-    cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), str(src), "-L", str(PKG), "-lspecpart_b200",
-           "-Wl,-rpath,$ORIGIN/../paper_2105_00578_b200", "-o", str(exe)]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    """tests/cpp/{shim,caller}_test.cpp against include/specpart_b200.hpp + the library (reference-style
+    C++ callers that compile unchanged against the shim; nlohmann/json for RunReport::to_json)."""
+    for name in ("shim_test", "caller_test"):
+        src = ROOT / "tests" / "cpp" / f"{name}.cpp"
+        exe = ROOT / "build" / name
+        if not src.exists():
+            continue
+        if exe.exists() and exe.stat().st_mtime >= max(src.stat().st_mtime, LIB.stat().st_mtime,
+                                                       (ROOT / "include" / "specpart_b200.hpp").stat().st_mtime):
+            continue
+        exe.parent.mkdir(parents=True, exist_ok=True)
+        cmd = ["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), "-I", str(NLOHMANN), str(src), "-L", str(PKG),
+               "-lspecpart_b200", "-Wl,-rpath,$ORIGIN/../paper_2105_00578_b200", "-o", str(exe)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
 
 
 if __name__ == "__main__":

@@ -265,6 +265,44 @@ void validate_config(int64_t n, const sp_config* cfg) {
     if (cfg->epsilon < 0.0) throw_infeasible("partition_graph: epsilon < 0");
 }
 
+// Gershgorin bound of an explicit CSR operator (laplacian.cpp:14-28): max_i (a_ii + sum_j!=i |a_ij|)
+__global__ void explicit_bound_kernel(const DevOp op, unsigned long long* out) {
+    double b = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double d = 0.0, off = 0.0;
+        for (int64_t k = op.offs[i]; k < op.offs[i + 1]; ++k) {
+            if (op.cols[k] == i) d += op.vals[k];
+            else off += fabs(op.vals[k]);
+        }
+        b = fmax(b, d + off);
+    }
+    // the bound is >= 0 (it starts at 0.0): doubles >= 0 order like their bit patterns
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(b)));
+}
+// inverse_diagonal (preconditioners.cpp:44-49) of an explicit CSR operator
+__global__ void explicit_inv_diag_kernel(const DevOp op, double* inv) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double d = 0.0;
+        for (int64_t k = op.offs[i]; k < op.offs[i + 1]; ++k)
+            if (op.cols[k] == i) d = op.vals[k];
+        inv[i] = fabs(d) < 1e-300 ? 1.0 : 1.0 / d;
+    }
+}
+double explicit_bound(const DevOp& op, cudaStream_t s) {
+    DBuf<unsigned long long> d(1);
+    SPB_CUDA(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), s));
+    explicit_bound_kernel<<<grid_for(op.n, 256, 4), 256, 0, s>>>(op, d.p);
+    SPB_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    SPB_CUDA(cudaMemcpyAsync(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SPB_CUDA(cudaStreamSynchronize(s));
+    double b;
+    std::memcpy(&b, &h, sizeof(b));
+    return b;
+}
+
 // amg_build on problem.A (the explicit CSR of the Laplacian, built here) into the solver
 void setup_amg(sp_context* ctx, DevGraph& g, int lap_kind, bool regular, uint64_t seed, Solver& solver) {
     if (ctx->comm.active()) throw SpError(SP_ERROR, "amg_build: the AMG preconditioner runs on one GPU in this build");
@@ -960,6 +998,94 @@ sp_status sp_poly_apply(sp_context* ctx, int32_t kind, const sp_graph* hg, uint6
         const std::vector<double>& rt = solver.roots();
         if (roots_out) std::memcpy(roots_out, rt.data(), sizeof(double) * rt.size());
         if (achieved_out) *achieved_out = static_cast<int32_t>(rt.size());
+    });
+}
+
+sp_status sp_precond_apply_csr(sp_context* ctx, int64_t n, const int64_t* offsets, const int32_t* cols,
+                               const double* vals, int32_t precond, uint64_t seed, int32_t degree, const double* Rh,
+                               int32_t m, double* H_out, double* roots_out, int32_t* achieved_out) {
+    return guarded(ctx, [&] {
+        if (ctx->comm.active()) throw_invalid("sp_precond_apply_csr: single-GPU entry point");
+        if (m < 1 || m > 32) throw_dimension("sp_precond_apply_csr: 1 <= m <= 32");
+        if (n < 1 || !offsets || !cols || !vals) throw_invalid("sp_precond_apply_csr: empty operator");
+        cudaStream_t s = ctx->stream;
+        const int64_t nnz = offsets[n];
+        DBuf<int64_t> o(n + 1);
+        DBuf<int32_t> c(std::max<int64_t>(nnz, 1));
+        DBuf<double> v(std::max<int64_t>(nnz, 1));
+        h2d(o.p, offsets, n + 1, s);
+        h2d(c.p, cols, nnz, s);
+        h2d(v.p, vals, nnz, s);
+        DevOp op;
+        op.mode = OP_EXPLICIT;
+        op.n = n;
+        op.nnz = nnz;
+        op.offs = o.p;
+        op.cols = c.p;
+        op.vals = v.p;
+        op.x_rows = n;
+        op.long_threshold = int64_t(1) << 40;
+        int64_t mr = 0;
+        for (int64_t i = 0; i < n; ++i) mr = std::max(mr, offsets[i + 1] - offsets[i]);
+        op.max_row = static_cast<int>(std::min<int64_t>(mr, 1 << 30));
+        op.bound = explicit_bound(op, s);  // make_operator's Gershgorin bound (laplacian.cpp:14-28)
+        Solver solver(ctx, op, nullptr, m);
+        DBuf<double> inv(n);
+        if (precond == SP_PRECOND_JACOBI) {
+            explicit_inv_diag_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(op, inv.p);
+            SPB_LAUNCH_CHECK();
+            solver.set_jacobi(inv.p);
+        } else if (precond == SP_PRECOND_POLYNOMIAL) {
+            solver.build_poly(seed, degree > 0 ? degree : 25);
+        } else if (precond == SP_PRECOND_NONE) {
+            solver.set_none();
+        } else {
+            throw_invalid("sp_precond_apply_csr: jacobi, polynomial or none");
+        }
+        DBuf<double> rd, hd(solver.block_elems(m));
+        const View Rv = solver.block(solver.input_block(m, rd), m);
+        upload_block(Rh, n, 0, n, m, Rv, s);
+        solver.apply_precond(Rv, m, solver.block(hd.p, m));
+        download_block(solver.block(hd.p, m), n, m, H_out, s);
+        const std::vector<double>& rt = solver.roots();
+        if (roots_out) std::memcpy(roots_out, rt.data(), sizeof(double) * rt.size());
+        if (achieved_out) *achieved_out = static_cast<int32_t>(rt.size());
+    });
+}
+
+sp_status sp_precond_apply(sp_context* ctx, int32_t kind, const sp_graph* hg, int32_t precond, uint64_t seed,
+                           int32_t degree, const double* Rh, int32_t m, double* H_out) {
+    return guarded(ctx, [&] {
+        if (ctx->comm.active()) throw_invalid("sp_precond_apply: single-GPU entry point");
+        if (m < 1 || m > 32) throw_dimension("sp_precond_apply: 1 <= m <= 32");
+        if (kind != 0 && kind != 1) throw_invalid("sp_precond_apply: kind must be combinatorial or normalized");
+        cudaStream_t s = ctx->stream;
+        DevGraph g;
+        upload_graph(ctx, hg, g);
+        const GraphKindInfo k = classify(g);
+        DevLaplacian A;
+        build_laplacian(kind, g, false, A, s);
+        if (!k.regular) build_row_bins(A.op, kLongRow, A.bins, s);
+        Solver solver(ctx, A.op, nullptr, m);
+        DBuf<double> inv;
+        if (precond == SP_PRECOND_JACOBI) {
+            inverse_diagonal(A, inv, s);
+            solver.set_jacobi(inv.p);
+        } else if (precond == SP_PRECOND_POLYNOMIAL) {
+            solver.build_poly(seed, degree > 0 ? degree : 25);
+        } else if (precond == SP_PRECOND_AMG) {
+            setup_amg(ctx, g, kind, k.regular, seed, solver);
+        } else if (precond == SP_PRECOND_NONE) {
+            solver.set_none();
+        } else {
+            throw_invalid("sp_precond_apply: unknown preconditioner");
+        }
+        const int64_t n = g.n_local;
+        DBuf<double> rd, hd(solver.block_elems(m));
+        const View Rv = solver.block(solver.input_block(m, rd), m);
+        upload_block(Rh, n, 0, n, m, Rv, s);
+        solver.apply_precond(Rv, m, solver.block(hd.p, m));
+        download_block(solver.block(hd.p, m), n, m, H_out, s);
     });
 }
 

@@ -11,12 +11,13 @@
 // every row's pattern is exactly its in-bounds stencil, verified on the device).
 //
 // A CTA owns a 32x32 (x, y) tile of one block column and marches a chunk of z
-// planes. A producer warp loads each plane of X as one 34x34 box (the tile plus
-// its x/y halo) with a 4-D tensor-map TMA copy (out-of-range halo is zero-filled
-// by the TMA unit), plus the 32x32 box of H the POLY epilogue reads, into a ring
+// planes. A producer warp loads each plane of X as one 36x34 box (the tile plus
+// its x/y halo; the x start is moved to x0 - 2 because a box must start on a
+// 16-byte boundary of the innermost dimension) with a 4-D tensor-map TMA copy
+// (out-of-range halo is zero-filled by the TMA unit), plus the 32x32 box of H the POLY epilogue reads, into a ring
 // of shared-memory stages tracked by mbarriers. Consumer warps compute plane z
 // from the stages of planes z-1, z, z+1 — each X element crosses L2 -> SM about
-// 1.13x (the halo) instead of the ~3x of per-plane gathers (z-1, z, z+1 reads of
+// 1.2x (the halo) instead of the ~3x of per-plane gathers (z-1, z, z+1 reads of
 // the same element from three different tiles) — and write Y (and H) with
 // coalesced 256-byte warp stores.
 #include "bulk.cuh"
@@ -34,10 +35,11 @@ namespace spb {
 namespace {
 
 constexpr int kTile = 32;                 // x and y extent of a tile
-constexpr int kHaloW = kTile + 2;         // 34: tile + one halo point each side
+constexpr int kHaloW = kTile + 4;         // 36: x extent of an X box (its start must be 16-byte aligned: x0 - 2)
+constexpr int kHaloH = kTile + 2;         // 34: y extent (one halo row each side)
 constexpr int kConsumers = 256;           // 8 consumer warps; warp w owns tile rows w, w+8, w+16, w+24
 constexpr int kMeshThreads = kConsumers + 32;
-constexpr int kXPlane = kHaloW * kHaloW;                       // doubles of an X box
+constexpr int kXPlane = kHaloW * kHaloH;                       // doubles of an X box
 constexpr int kXPlanePad = ((kXPlane * 8 + 127) / 128) * 16;   // 128-byte aligned (in doubles)
 constexpr int kHPlane = kTile * kTile;
 constexpr int kMaxStages = 8;
@@ -60,20 +62,16 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <int KL, int KU, int EPI>
+template <bool BOX27, int EPI>
 __global__ void __launch_bounds__(kMeshThreads, 2)
     spmm_mesh_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, const DevOp op,
                      const EpiArgs ea, const int m, const MeshGeo geo) {
-    constexpr int W = KL + KU;
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-    __shared__ int16_t s_code[256 * W];  // per (pattern, slot): (dz+1)*128 + (dy+1)*34 + (dx+1), -1 = padding
-    __shared__ double s_deg[256];
     __shared__ double s_theta[kMaxCols];
     __shared__ double s_sq[kConsumers / 32][kMaxCols];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int nxny = geo.nx * geo.ny;
 
     if (tid == 0) {
         for (int s = 0; s < geo.nst; ++s) {
@@ -82,20 +80,6 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int e = tid; e < op.ell_npat * W; e += kMeshThreads) {
-        const int32_t d = op.ell_pat_tab[e];
-        int v = -1;
-        if (d != kEllPad) {
-            // d = dz*nxny + dy*nx + dx with dz, dy, dx in {-1, 0, 1} (mesh_plan checked it)
-            const int dz = d > nxny / 2 ? 1 : (d < -nxny / 2 ? -1 : 0);
-            const int r = d - dz * nxny;
-            const int dy = r > geo.nx / 2 ? 1 : (r < -geo.nx / 2 ? -1 : 0);
-            const int dx = r - dy * geo.nx;
-            v = (dz + 1) * 128 + (dy + 1) * kHaloW + (dx + 1);
-        }
-        s_code[e] = static_cast<int16_t>(v);
-    }
-    for (int e = tid; e < op.ell_npat; e += kMeshThreads) s_deg[e] = op.ell_pat_deg[e];
     if (EPI == EPI_RESIDUAL) {
         for (int c = tid; c < m; c += kMeshThreads) s_theta[c] = ea.theta[c];
         for (int e = tid; e < (kConsumers / 32) * kMaxCols; e += kMeshThreads) (&s_sq[0][0])[e] = 0.0;
@@ -129,7 +113,7 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                     if (g >= geo.nst) mbar_wait(empty + s, eph);
                     double* st = smem + static_cast<size_t>(s) * geo.stage;
                     mbar_expect_tx(full + s, xbytes + hbytes);
-                    tma_load_4d(st, &xmap, tx * kTile - 1, ty * kTile - 1, p, c, full + s);
+                    tma_load_4d(st, &xmap, tx * kTile - 2, ty * kTile - 1, p, c, full + s);
                     if (geo.h_stage) tma_load_4d(st + kXPlanePad, &hmap, tx * kTile, ty * kTile, p - 1, c, full + s);
                     if (++s == geo.nst) {
                         s = 0;
@@ -153,43 +137,65 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         mbar_wait(full + ((g + 1) % geo.nst), static_cast<unsigned>(((g + 1) / geo.nst) & 1));
         for (int z = z0; z < z1; ++z) {
             const int64_t gz = g + (z - z0) + 1;  // stage of plane z
-            // pattern ids of this plane's rows (issued before the wait for plane z + 1)
-            int pid[4];
             bool live[4];
             int64_t row[4];
+            double bd[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int y = ty * kTile + warp + 8 * j;
                 live[j] = xin && y < geo.ny;
                 row[j] = (static_cast<int64_t>(z) * geo.ny + y) * geo.nx + x;
-                pid[j] = live[j] ? static_cast<int>(__ldg(op.ell_pat + row[j])) : 0;
+                bd[j] = (EPI == EPI_RESIDUAL && ea.bdiag && live[j]) ? ea.bdiag[row[j]] : 1.0;
             }
-            double bd[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bd[j] = (EPI == EPI_RESIDUAL && ea.bdiag && live[j]) ? ea.bdiag[row[j]] : 1.0;
             mbar_wait(full + ((gz + 1) % geo.nst), static_cast<unsigned>(((gz + 1) / geo.nst) & 1));
-            const double* pl[3] = {smem + static_cast<size_t>((gz - 1) % geo.nst) * geo.stage,
-                                   smem + static_cast<size_t>(gz % geo.nst) * geo.stage,
-                                   smem + static_cast<size_t>((gz + 1) % geo.nst) * geo.stage};
-            const double* hs = pl[2] + kXPlanePad;
+            const double* p0 = smem + static_cast<size_t>((gz - 1) % geo.nst) * geo.stage;  // plane z - 1
+            const double* p1 = smem + static_cast<size_t>(gz % geo.nst) * geo.stage;        // plane z
+            const double* p2 = smem + static_cast<size_t>((gz + 1) % geo.nst) * geo.stage;  // plane z + 1
+            const double* hs = p2 + kXPlanePad;
+            // x / z neighbours present (mesh_plan verified every row is its full in-bounds stencil)
+            const bool xm = xin && x > 0, xp = x + 1 < geo.nx, zm = z > 0, zp = z + 1 < geo.nz;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int ly = warp + 8 * j;
-                const int base = ly * kHaloW + lane;  // (dy+1)*34 + (dx+1) added per slot
-                const double xi = pl[1][base + kHaloW + 1];
+                const int y = ty * kTile + ly;
+                const bool ym = y > 0, yp = y + 1 < geo.ny;
+                const int ctr = (ly + 1) * kHaloW + lane + 2;  // this row's element in its plane box
+                const double xi = p1[ctr];
                 double acc = 0.0;
-                // acc -= x_j over the lower slots, += deg * x_i, -= x_j over the upper slots:
-                // the storage order of build_combinatorial's row (bit-identical to spmv_block)
+                // the row's entries in storage (= ascending column = lexicographic (dz, dy, dx))
+                // order: acc -= x_j before the diagonal, += deg * x_i, -= x_j after it —
+                // build_combinatorial's order, so the sum is bit-identical to spmv_block
+                int deg = 0;
+                if constexpr (BOX27) {
 #pragma unroll
-                for (int sl = 0; sl < KL; ++sl) {
-                    const int code = s_code[pid[j] * W + sl];
-                    if (code >= 0) acc = __dsub_rn(acc, pl[code >> 7][base + (code & 127)]);
-                }
-                acc = __dadd_rn(acc, __dmul_rn(s_deg[pid[j]], xi));
+                    for (int t = 0; t < 27; ++t) {
+                        const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
+                        if (t == 13) continue;
+                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym : dy > 0 ? yp : true) &&
+                                        (dx < 0 ? xm : dx > 0 ? xp : true);
+                        deg += on ? 1 : 0;
+                    }
 #pragma unroll
-                for (int sl = KL; sl < W; ++sl) {
-                    const int code = s_code[pid[j] * W + sl];
-                    if (code >= 0) acc = __dsub_rn(acc, pl[code >> 7][base + (code & 127)]);
+                    for (int t = 0; t < 27; ++t) {
+                        const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
+                        const double* pl = dz < 0 ? p0 : dz > 0 ? p2 : p1;
+                        if (t == 13) {
+                            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
+                            continue;
+                        }
+                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym : dy > 0 ? yp : true) &&
+                                        (dx < 0 ? xm : dx > 0 ? xp : true);
+                        if (on) acc = __dsub_rn(acc, pl[ctr + dy * kHaloW + dx]);
+                    }
+                } else {
+                    deg = zm + ym + xm + xp + yp + zp;
+                    if (zm) acc = __dsub_rn(acc, p0[ctr]);
+                    if (ym) acc = __dsub_rn(acc, p1[ctr - kHaloW]);
+                    if (xm) acc = __dsub_rn(acc, p1[ctr - 1]);
+                    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
+                    if (xp) acc = __dsub_rn(acc, p1[ctr + 1]);
+                    if (yp) acc = __dsub_rn(acc, p1[ctr + kHaloW]);
+                    if (zp) acc = __dsub_rn(acc, p2[ctr]);
                 }
                 double sq = 0.0;
                 if (live[j]) {
@@ -261,13 +267,13 @@ EncodeTiledFn encode_fn() {
 }
 
 // the block as a 4-D tensor (x, y, z, column) of doubles
-void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_xy) {
+void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_x, int box_y) {
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(op.mesh_nx), static_cast<cuuint64_t>(op.mesh_ny),
                                 static_cast<cuuint64_t>(op.mesh_nz), static_cast<cuuint64_t>(m)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(op.mesh_nx) * 8,
                                    static_cast<cuuint64_t>(op.mesh_nx) * op.mesh_ny * 8,
                                    static_cast<cuuint64_t>(m > 1 ? v.cs : (op.n + 1) & ~int64_t(1)) * 8};
-    const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_xy), static_cast<cuuint32_t>(box_xy), 1, 1};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_x), static_cast<cuuint32_t>(box_y), 1, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, v.ptr, dims, strides, box, es,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -275,7 +281,7 @@ void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_x
     if (r != CUDA_SUCCESS) throw SpError(8, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
 }
 
-template <int KL, int KU, int EPI>
+template <bool BOX27, int EPI>
 int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
     MeshGeo geo{};
     geo.nx = op.mesh_nx;
@@ -285,7 +291,7 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
     geo.nty = (geo.ny + kTile - 1) / kTile;
     geo.h_stage = (EPI == EPI_POLY && !ea.first && ea.h_terms) ? 1 : 0;
     geo.stage = kXPlanePad + (geo.h_stage ? kHPlane : 0);
-    auto kern = spmm_mesh_kernel<KL, KU, EPI>;
+    auto kern = spmm_mesh_kernel<BOX27, EPI>;
     static bool attr = false;
     if (!attr) {
         SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -308,8 +314,8 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
     const int64_t items = per_chunk * geo.nzc;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, ctas)));
     CUtensorMap xmap, hmap;
-    make_map(&xmap, X, m, op, kHaloW);
-    if (geo.h_stage) make_map(&hmap, ea.H, m, op, kTile);
+    make_map(&xmap, X, m, op, kHaloW, kHaloH);
+    if (geo.h_stage) make_map(&hmap, ea.H, m, op, kTile, kTile);
     else hmap = xmap;
     kern<<<grid, kMeshThreads, smem, s>>>(xmap, hmap, op, ea, m, geo);
     SPB_LAUNCH_CHECK();
@@ -400,14 +406,10 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
 }
 
 int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
-    const int kk = op.ell_kl * 100 + op.ell_ku;
+    const bool box27 = op.ell_kl == 13;
     switch (ea.mode) {
 #define SPB_MESH(EPI_)                                                                  \
-    switch (kk) {                                                                     \
-    case 202: return launch_mesh<2, 2, EPI_>(op, X, m, ea, s);                        \
-    case 303: return launch_mesh<3, 3, EPI_>(op, X, m, ea, s);                        \
-    default: return launch_mesh<13, 13, EPI_>(op, X, m, ea, s);                       \
-    }
+    return box27 ? launch_mesh<true, EPI_>(op, X, m, ea, s) : launch_mesh<false, EPI_>(op, X, m, ea, s);
     case EPI_STORE: SPB_MESH(EPI_STORE)
     case EPI_RESIDUAL: SPB_MESH(EPI_RESIDUAL)
     default: SPB_MESH(EPI_POLY)

@@ -199,6 +199,11 @@ std::string report_json(const sp_report& r, const std::vector<double>& part_weig
                    {"theta", vec(r.theta, r.eigenvectors)},
                    {"residual_norms", vec(r.residual_norms, r.eigenvectors)},
                    {"converged", conv}};
+    if (r.amg_levels > 0) {
+        json lv = json::array();
+        for (int l = 0; l < r.amg_levels; ++l) lv.push_back({{"n", r.amg_n[l]}, {"nnz", r.amg_nnz[l]}});
+        j["solver"]["amg_levels"] = lv;
+    }
     if (with_trace && r.trace_len > 0) {
         json tr = json::array();
         for (int t = 0; t < r.trace_len; ++t) {
@@ -649,6 +654,7 @@ int run_partition(const Args& a) {
         rep.init = SP_INIT_RANDOM;
         warnings.push_back("initial vectors loaded from " + a.init_file);
     } else {
+        if (rep.warnings & SP_WARN_AMG_STAGNATED) warnings.emplace_back("amg coarsening stagnated; hierarchy stopped early");
         if (rep.warnings & SP_WARN_BREAKDOWN_RECOVERED)
             warnings.emplace_back("eigensolver recovered from a basis breakdown by clearing the search directions");
         if (rep.warnings & SP_WARN_UNCONVERGED)

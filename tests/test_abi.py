@@ -74,8 +74,9 @@ def test_context_creation_fails_loudly_without_gpu():
         Context(0)
 
 
-def test_shim_test_binary_links():
-    exe = ROOT / "build" / "shim_test"
-    assert exe.exists(), "build() compiles tests/cpp/shim_test.cpp against include/specpart_b200.hpp"
+@pytest.mark.parametrize("name", ["shim_test", "caller_test"])
+def test_shim_test_binary_links(name):
+    exe = ROOT / "build" / name
+    assert exe.exists(), f"build() compiles tests/cpp/{name}.cpp against include/specpart_b200.hpp"
     out = subprocess.run(["ldd", str(exe)], capture_output=True, text=True).stdout
     assert "libspecpart_b200.so" in out and "not found" not in out.split("libspecpart_b200.so")[1].split("\n")[0]

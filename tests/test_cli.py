@@ -101,8 +101,8 @@ def _sections(text):
 def test_partition_matches_reference(tmp_path, case):
     name = case["name"]
     out, rep = tmp_path / "p.txt", tmp_path / "r.json"
-    r = run("--input", GOLD / f"{name}.mtx", "--parts", case["K"], "--problem", case["problem"], "--precond",
-            case["precond"], "--seed", case["seed"], "--output", out, "--report", rep)
+    r = run("--input", GOLD / f"{case.get('input', name)}.mtx", "--parts", case["K"], "--problem", case["problem"],
+            "--precond", case["precond"], "--seed", case["seed"], "--output", out, "--report", rep)
     assert r.returncode == 0, r.stderr
     mine, ref = json.loads(rep.read_text()), json.loads((GOLD / f"{name}.json").read_text())
     # same keys everywhere, graph and resolved config exact (ingestion/LCC/classify are bit-exact)

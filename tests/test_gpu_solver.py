@@ -211,3 +211,17 @@ def test_cpp_shim_caller():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_cpp_reference_caller_run_partition():
+    # tools/specpart.cpp:63-184's call sequence (parse -> symmetrize -> LCC -> partition_graph,
+    # and the --init-file stage-by-stage path) compiled against the shim (tests/cpp/caller_test.cpp)
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    exe = root / "build" / "caller_test"
+    for mtx in ("grid32.mtx", "messy.mtx"):
+        r = subprocess.run([str(exe), str(root / "tests" / "golden" / "cli" / mtx)], capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "0 failures" in r.stdout
