@@ -290,6 +290,10 @@ def main():
     clk.start()
     clk.wait_first()
     ctx.set_timing(True)
+    if os.environ.get("SPB_RECURRENCE") == "1":  # A/B of the AX/AH/AP recurrence
+        ctx.set_recurrence(True)
+    if os.environ.get("SPB_RELABEL") == "0":  # A/B of the irregular-graph relabel
+        ctx.set_relabel(False)
     dg = ctx.upload(gp)
     for _ in range(args.warmup):
         ctx.partition_resident(dg, cfg, copy_assignment=False)

@@ -186,6 +186,17 @@ const char* sp_last_error(const sp_context* ctx);
 int sp_version(void);
 /* Record CUDA events around every SpMM launch (report.spmm_ms); off by default. */
 sp_status sp_context_set_timing(sp_context* ctx, int on);
+/* LOBPCG with the AX/AH/AP recurrence: one SpMM per iteration
+ * on the new preconditioned block instead of the reference's A*S and A*X
+ * (eigensolver.cpp:138-155, 210-222), with A*X recomputed exactly whenever the
+ * recurrence reports convergence and every 10 iterations. Off by default (the
+ * reference's algorithm); applies to sp_partition* and sp_lobpcg on this context. */
+sp_status sp_context_set_recurrence(sp_context* ctx, int on);
+/* Irregular graphs (classify) on one GPU: run the eigensolver on a degree-descending
+ * relabel of the vertices (hub rows of every block stay L2-resident for the SpMM
+ * gathers); the initial block and the eigenvectors are permuted in and out, so the
+ * multi-jagged stage and the metrics see the caller's numbering. On by default. */
+sp_status sp_context_set_relabel(sp_context* ctx, int on);
 
 /* ---- end to end (pipeline.cpp:47-167) --------------------------------------
  * assignment_out: n int32 part ids in [0, K). x0_colmajor: optional n x d

@@ -128,6 +128,8 @@ SIGNATURES = {
     "sp_context_destroy": (None, [P]),
     "sp_last_error": (C.c_char_p, [P]),
     "sp_context_set_timing": (I32, [P, C.c_int]),
+    "sp_context_set_recurrence": (I32, [P, C.c_int]),
+    "sp_context_set_relabel": (I32, [P, C.c_int]),
     "sp_partition": (I32, [P, C.POINTER(SpGraph), C.POINTER(SpConfig), P, C.POINTER(SpReport), P]),
     "sp_graph_upload": (I32, [P, C.POINTER(SpGraph), C.POINTER(P)]),
     "sp_graph_free": (None, [P]),

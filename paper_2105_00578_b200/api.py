@@ -302,6 +302,14 @@ class Context:
     def set_timing(self, on: bool):
         self._check(self.lib.sp_context_set_timing(self._h, int(on)))
 
+    def set_relabel(self, on: bool):
+        """Irregular graphs: degree-descending relabel inside the solver (on by default)."""
+        self._check(self.lib.sp_context_set_relabel(self._h, int(on)))
+
+    def set_recurrence(self, on: bool):
+        """LOBPCG AX/AH/AP recurrence (one SpMM per iteration); off = the reference's algorithm."""
+        self._check(self.lib.sp_context_set_recurrence(self._h, int(on)))
+
     # pipeline.cpp:47-167
     def partition_graph(self, g: Graph, cfg: RunConfig, x0=None, out=None,
                         return_eigenvectors: bool = False) -> RunResult:

@@ -369,16 +369,25 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
                          std::to_string(n));
     if (d > 32) throw_dimension("partition_graph: d > 32 eigenvectors is not supported");
 
+    // irregular graphs on one GPU: the solver runs on a degree-descending relabel of the
+    // graph (relabel.cu; hub rows of every block stay L2-resident for the SpMM gathers)
+    Relabel rl;
+    DevGraph gr;
+    if (!kind.regular && !ctx->comm.active() && ctx->relabel) {
+        relabel_by_degree(g, gr, rl, s);
+        prepare_graph(ctx, gr);
+    }
+    DevGraph& go = rl.on ? gr : g;  // the graph the operators are built on
     DevLaplacian A;
-    build_laplacian(operator_kind(R.problem), g, false, A, s);
+    build_laplacian(operator_kind(R.problem), go, false, A, s);
     A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
     if (!kind.regular) build_row_bins(A.op, kLongRow, A.bins, s);  // length bins + long-row list
-    localize_operator(ctx->comm, g, A, s);  // multi-GPU: halo numbering + exchange plan
+    localize_operator(ctx->comm, go, A, s);  // multi-GPU: halo numbering + exchange plan
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {
         // B = D must be positive (laplacian.cpp:169-173)
         if (!g.positive_degrees) throw_degenerate("generalized problem requires positive degrees");
-        bdiag = g.deg.p;
+        bdiag = go.deg.p;
     }
     SPB_CUDA(cudaStreamSynchronize(s));
     R.laplacian_s = since(t_lap);
@@ -387,6 +396,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     // Stage 2: preconditioner + eigensolve
     const auto t_eig = Clock::now();
     Solver solver(ctx, A.op, bdiag, d);
+    solver.set_recurrence(ctx->recurrence);
     DBuf<double> inv;
     if (R.precond == SP_PRECOND_JACOBI) {
         inverse_diagonal(A, inv, s);
@@ -396,7 +406,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
         R.poly_degree = static_cast<int32_t>(solver.roots().size());
     } else if (R.precond == SP_PRECOND_AMG) {
         // pipeline.cpp:107-118: regular / irregular presets, seed ^ "amg"
-        setup_amg(ctx, g, operator_kind(R.problem), kind.regular, cfg->seed ^ 0x616d67ULL, solver);
+        setup_amg(ctx, go, operator_kind(R.problem), kind.regular, cfg->seed ^ 0x616d67ULL, solver);
         const Amg* amg = solver.amg();
         R.amg_levels = std::min(amg->levels(), SP_MAX_AMG_LEVELS);
         for (int l = 0; l < R.amg_levels; ++l) {
@@ -409,11 +419,15 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     }
     ctx->prof.mark(s, "precond_build");
     const int64_t nloc = g.n_local;
-    DBuf<double> Xb;
+    DBuf<double> Xb, X0b;
     const View X = solver.block(solver.input_block(d, Xb), d);
-    if (x0) upload_block(x0, n, g.row0, nloc, d, X, s);
-    else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X, s);
-    else initial_block_piecewise(n, d, g.row0, nloc, X, s);
+    // the initial block in the reference's vertex order (then permuted into the relabel)
+    if (rl.on) X0b.alloc(solver.block_elems(d));
+    const View X0 = rl.on ? solver.block(X0b.p, d) : X;
+    if (x0) upload_block(x0, n, g.row0, nloc, d, X0, s);
+    else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X0, s);
+    else initial_block_piecewise(n, d, g.row0, nloc, X0, s);
+    if (rl.on) permute_rows_in(rl, nloc, d, X0, X, s);
     ctx->prof.mark(s, "initial_block");
     SolveOpts so;
     so.nev = d;
@@ -436,7 +450,12 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     // Stage 3: embed (drop column 0) + multi-jagged on the whole embedding
     const auto t_mj = Clock::now();
     DBuf<double> Xall;
-    const View Xg = gather_block(ctx, X, d, Xall);
+    View Xsrc = X;
+    if (rl.on) {  // back to the reference's vertex order (MJ ties break by vertex id)
+        permute_rows_out(rl, nloc, d, X, X0, s);
+        Xsrc = X0;
+    }
+    const View Xg = gather_block(ctx, Xsrc, d, Xall);
     asg.alloc(static_cast<size_t>(std::max<int64_t>(ctx->comm.active() ? ctx->comm.n_pad * ctx->comm.world : n, 1)));
     if (!g.positive_weights) throw_infeasible("mj_partition: weights must be positive");
     mj_partition_dev(n, d - 1, Xg.sub(1, d - 1), g.vw_all.p, g.unit_weights, K, asg.p, s);
@@ -653,6 +672,18 @@ const char* sp_last_error(const sp_context* c) { return c ? c->err.c_str() : "nu
 sp_status sp_context_set_timing(sp_context* c, int on) {
     if (!c) return SP_INVALID;
     c->time_spmm = on != 0;
+    return SP_OK;
+}
+
+sp_status sp_context_set_recurrence(sp_context* ctx, int on) {
+    if (!ctx) return SP_INVALID;
+    ctx->recurrence = on != 0;
+    return SP_OK;
+}
+
+sp_status sp_context_set_relabel(sp_context* ctx, int on) {
+    if (!ctx) return SP_INVALID;
+    ctx->relabel = on != 0;
     return SP_OK;
 }
 
@@ -943,6 +974,7 @@ sp_status sp_lobpcg(sp_context* ctx, const sp_graph* hg, int32_t problem, int32_
             bdiag = g.deg.p;
         }
         Solver solver(ctx, A.op, bdiag, nev);
+        solver.set_recurrence(ctx->recurrence);
         DBuf<double> inv;
         if (precond == SP_PRECOND_JACOBI) {
             inverse_diagonal(A, inv, s);

@@ -780,7 +780,45 @@ __global__ void colsum_kernel(int64_t n, View v, double* partial) {
     }
 }
 
+struct Theta {
+    double t[kMaxCols];
+};
+__global__ void residual_ax_kernel(int64_t n, int m, View X, View AX, const double* bdiag, const Theta th, View R,
+                                   double* partial) {
+    __shared__ double red[256];
+    for (int c = 0; c < m; ++c) {
+        double s = 0.0;
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const double x = X.at(i, c);
+            const double bx = bdiag ? __dmul_rn(bdiag[i], x) : x;
+            const double r = __dsub_rn(AX.at(i, c), __dmul_rn(th.t[c], bx));
+            R.at(i, c) = r;
+            s += r * r;
+        }
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) partial[static_cast<int64_t>(blockIdx.x) * m + c] = red[0];
+        __syncthreads();
+    }
+}
+
 } // namespace
+
+int residual_from_ax(int64_t n, const View& X, const View& AX, const double* bdiag, const double* theta_host,
+                     int m, const View& R, double* partial, cudaStream_t s) {
+    if (m > kMaxCols) throw_dimension("residual_from_ax: too many columns");
+    Theta th{};
+    for (int c = 0; c < m; ++c) th.t[c] = theta_host[c];
+    const int grid = grid_for(std::max<int64_t>(n, 1), 256, 2);
+    residual_ax_kernel<<<grid, 256, 0, s>>>(n, m, X, AX, bdiag, th, R, partial);
+    SPB_LAUNCH_CHECK();
+    return grid;
+}
 
 int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s) {
     const int grid = grid_for(n, 256, 2);

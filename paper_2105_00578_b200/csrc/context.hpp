@@ -189,6 +189,8 @@ struct sp_context {
     std::string err;
     spb::Timers timers;
     bool time_spmm = false;   // record CUDA events around every SpMM (bench/diagnostics)
+    bool recurrence = false;  // LOBPCG AX/AH/AP recurrence (Solver::set_recurrence)
+    bool relabel = true;      // irregular graphs: degree-descending relabel (relabel.cu)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // event pairs recorded around SpMM launches; resolved without extra syncs
     // once the pipeline has synchronized (collect_spmm_times)

@@ -61,4 +61,15 @@ void build_laplacian(int kind, const DevGraph& g, bool materialize, DevLaplacian
 void collect_long_rows(const DevGraph& g, DevLaplacian& L, int64_t threshold, cudaStream_t s);
 void inverse_diagonal(const DevLaplacian& L, DBuf<double>& inv, cudaStream_t s);
 
+// Degree-descending vertex order of a one-GPU graph (relabel.cu): new vertex r is old
+// vertex perm[r] (ties by ascending id); out holds the relabelled CSR.
+struct Relabel {
+    DBuf<int32_t> perm, inv;  // new -> old, old -> new
+    bool on = false;
+};
+void relabel_by_degree(const DevGraph& g, DevGraph& out, Relabel& rl, cudaStream_t s);
+// dst_new(r, :) = src_old(perm[r], :)  /  dst_old(perm[r], :) = src_new(r, :)
+void permute_rows_in(const Relabel& rl, int64_t n, int m, const View& src_old, const View& dst_new, cudaStream_t s);
+void permute_rows_out(const Relabel& rl, int64_t n, int m, const View& src_new, const View& dst_old, cudaStream_t s);
+
 } // namespace spb

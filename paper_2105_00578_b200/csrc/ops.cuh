@@ -158,6 +158,12 @@ enum { TS_NONE = 0, TS_UPDATE = 1, TS_COMBINE = 2 };
 int ts_run(const TsSpec& spec, double* gram_out, double* scratch, size_t scratch_elems,
            cudaStream_t s);
 
+// R = AX - theta .* (B X) (the SpMM RESIDUAL epilogue's arithmetic, eigensolver.cpp:212-218)
+// from a tracked A X, with per-CTA partial sums of R^2 per column (fixed order); returns
+// the number of partial rows (reduce with reduce_partials).
+int residual_from_ax(int64_t n, const View& X, const View& AX, const double* bdiag, const double* theta_host,
+                     int m, const View& R, double* partial, cudaStream_t s);
+
 // Deterministic per-CTA column sums; returns the number of partial rows.
 int colsum_partials(int64_t n, const View& v, double* scratch, cudaStream_t s);
 

@@ -27,6 +27,7 @@ namespace spb {
 namespace {
 
 constexpr double kRankDropTol = 1e-10;  // eigensolver.cpp:55
+constexpr int kTrueResidualEvery = 10;   // recurrence: exact A X at least this often
 
 double max_abs_dev_identity(const std::vector<double>& G, int k) {
     double e = 0.0;
@@ -116,7 +117,7 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
     partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 * 5 + A.n_long + 64) * 64);
     norms_.alloc(64);
-    H_.alloc(block_elems(max_cols));
+    pH_ = input_block(max_cols, H_);
     P_.alloc(block_elems(max_cols));
     AS_.alloc(block_elems(m3));
     pR_ = input_block(max_cols, R_);
@@ -264,13 +265,38 @@ void Solver::residuals(const View& X, const std::vector<double>& theta, SolveRes
     }
 }
 
+void Solver::residuals_from(const View& X, const View& AX, const std::vector<double>& theta, SolveResult& r,
+                            double thr) {
+    const int nev = static_cast<int>(theta.size());
+    const int rows = residual_from_ax(n_, X.sub(0, nev), AX.sub(0, nev), bdiag_, theta.data(), nev,
+                                      block(pR_, nev), partial_.p, s_);
+    reduce_partials(partial_.p, rows, nev, norms_.p, s_);
+    ctx_->comm.sum_small(norms_.p, nev, s_);
+    std::vector<double> sq(nev);
+    SPB_CUDA(cudaMemcpyAsync(sq.data(), norms_.p, sizeof(double) * nev, cudaMemcpyDeviceToHost, s_));
+    SPB_CUDA(cudaStreamSynchronize(s_));
+    for (int j = 0; j < nev; ++j) {
+        r.residual_norms[j] = std::sqrt(sq[j]);
+        r.converged[j] = r.residual_norms[j] <= thr ? 1 : 0;
+    }
+}
+
+void Solver::ts_mirror(const TsSpec& spec) {
+    TsSpec t = spec;
+    t.gram = false;
+    t.b = nullptr;
+    t.n = n_;
+    ts_run(t, nullptr, scratch_.p, scratch_.n, s_);
+}
+
 // ---------------------------------------------------------------------------
 // Block B-orthonormalization (b_orthonormalize, eigensolver.cpp:88-129)
 
 Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, const View& dst,
-                            SolveResult& st) {
+                            SolveResult& st, const View* AV, const View* Aagainst, const View* Adst) {
     Orth out;
     if (k == 0) return out;
+    const bool mirror = AV != nullptr;
     const View Vin = V.sub(0, k);
     const View D = dst.sub(0, k);
     int P, Q;
@@ -301,6 +327,13 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
         p1.transform = TS_UPDATE;
         p1.gram_left_u = true;
         p1.gram_left_self = false;
+        if (mirror) {
+            TsSpec m1 = p1;  // A W1 = A V - (A against) C0
+            m1.U0 = Aagainst->sub(0, a);
+            m1.V = AV->sub(0, k);
+            m1.W = Adst->sub(0, k);
+            ts_mirror(m1);
+        }
         int P1, Q1;
         gram_dev(p1, P1, Q1);  // a x k
         SPB_CUDA(cudaMemcpyAsync(cmat2_.p, gram_.p, sizeof(double) * P1 * Q1, cudaMemcpyDeviceToDevice, s_));
@@ -315,6 +348,13 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
         p2.transform = TS_UPDATE;
         p2.gram_left_u = false;
         p2.gram_left_self = true;
+        if (mirror) {
+            TsSpec m2 = p2;  // A W2 = A W1 - (A against) C1
+            m2.U0 = Aagainst->sub(0, a);
+            m2.V = Adst->sub(0, k);
+            m2.W = Adst->sub(0, k);
+            ts_mirror(m2);
+        }
         int P2, Q2;
         G2 = gram_to_host(p2, P2, Q2);
         src = D;
@@ -370,9 +410,15 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
             uncertain = true;
         }
     }
+    // the column-wise path's coefficients are not tracked: A dst is recomputed exactly
+    auto slow = [&] {
+        Orth o = b_orth_slow(src, k, against, a, dst, orig, st);
+        if (mirror && o.kept > 0) spmm_store(dst.sub(0, o.kept), o.kept, Adst->sub(0, o.kept));
+        return o;
+    };
     if (uncertain) {
         ++st.slow_orth;
-        return b_orth_slow(src, k, against, a, dst, orig, st);
+        return slow();
     }
     out.kept = static_cast<int>(T.size());
     if (out.kept == 0) return out;
@@ -389,6 +435,12 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
     cb.b = bdiag_;
     cb.transform = TS_COMBINE;
     cb.gram_left_self = true;
+    if (mirror) {
+        TsSpec mc = cb;  // A dst = (A src) T
+        mc.V = a > 0 ? Adst->sub(0, k) : AV->sub(0, k);
+        mc.W = Adst->sub(0, out.kept);
+        ts_mirror(mc);
+    }
     int P3, Q3;
     std::vector<double> G3 = gram_to_host(cb, P3, Q3);
     if (max_abs_dev_identity(G3, out.kept) > 1e-12) {
@@ -397,8 +449,7 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
         L.a = G3;
         if (!cholesky_lower(L)) {
             ++st.slow_orth;
-            std::vector<double> o2(k);
-            return b_orth_slow(src, k, against, a, dst, orig, st);
+            return slow();
         }
         const int kk = out.kept;
         std::vector<double> Tinv(static_cast<size_t>(kk) * kk, 0.0);  // (L^{-1})^T, column-major
@@ -416,6 +467,12 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
         cq.transform = TS_COMBINE;
         cq.n = n_;
         ts_run(cq, nullptr, scratch_.p, scratch_.n, s_);
+        if (mirror) {
+            TsSpec mq = cq;
+            mq.V = Adst->sub(0, kk);
+            mq.W = Adst->sub(0, kk);
+            ts_mirror(mq);
+        }
         ++st.cholqr_fixups;
     }
     return out;
@@ -650,8 +707,15 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     const View AS = colmajor_ ? colmajor(AS_.p, ld_, m3) : rowmajor(AS_.p, m3, m3);
     const View Xv = X.sub(0, nev);
     const View Rv = block(pR_, nev);
-    const View Hv = block(H_.p, nev);
+    const View Hv = block(pH_, nev);
     const View Pv = block(P_.p, nev);
+    // recurrence: A X, A H, A P tracked next to X, H, P (A S lives in AS either way)
+    if (recur_) {
+        AX_.alloc(block_elems(nev));
+        AP_.alloc(block_elems(nev));
+        AH_.alloc(block_elems(nev));
+    }
+    const View AXv = recur_ ? block(AX_.p, nev) : View{};
     int p_cols = 0;
     std::vector<double> theta;
     int iter = 0;
@@ -661,11 +725,13 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
 
     // Rayleigh-Ritz on an orthonormal basis Q (m columns of S): theta, Y (m x nev)
     auto projected_eig = [&](int m, std::vector<double>& th, std::vector<double>& Y) {
-        EpiArgs ea;
-        ea.mode = EPI_STORE;
-        ea.Y = AS.sub(0, m);
-        spmm(S.sub(0, m), m, ea);
-        ctx_->prof.mark(s_, "rr_spmm");
+        if (!recur_) {  // the recurrence carried A S through the orthonormalization
+            EpiArgs ea;
+            ea.mode = EPI_STORE;
+            ea.Y = AS.sub(0, m);
+            spmm(S.sub(0, m), m, ea);
+            ctx_->prof.mark(s_, "rr_spmm");
+        }
         TsSpec g;
         g.U0 = S.sub(0, m);
         g.V = AS.sub(0, m);
@@ -696,6 +762,25 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         cb.n = n_;
         ts_run(cb, nullptr, scratch_.p, scratch_.n, s_);
     };
+    // residuals: the SpMM epilogue (reference), or R = AX - BX theta from the tracked AX,
+    // with A X recomputed exactly when the recurrence reports convergence and every
+    // kTrueResidualEvery iterations (bounds the drift of the recurrence)
+    auto residual_step = [&](int it) {
+        if (!recur_) {
+            residuals(Xv, theta, res, thr);
+            return;
+        }
+        residuals_from(Xv, AXv, theta, res, thr);
+        if (res.all_converged() || it % kTrueResidualEvery == 0) {
+            spmm_store(Xv, nev, AXv);
+            residuals_from(Xv, AXv, theta, res, thr);
+        }
+    };
+    auto orth = [&](const View& V, int k, const View& against, int a, const View& dst, const View& AV) {
+        if (!recur_) return b_orth(V, k, against, a, dst, res);
+        const View Ad = AS.sub(a, m3 - a);
+        return b_orth(V, k, against, a, dst, res, &AV, &AS, &Ad);
+    };
     auto record = [&](int it) {
         if (!o.record_trace) return;
         TraceRec t;
@@ -708,8 +793,9 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     };
 
     // initial Rayleigh-Ritz (eigensolver.cpp:239-252)
+    if (recur_) spmm_store(Xv, nev, AXv);
     for (;;) {
-        Orth ox = b_orth(Xv, nev, View{}, 0, S, res);
+        Orth ox = orth(Xv, nev, View{}, 0, S, AXv);
         if (ox.kept < nev) {
             if (retried) throw BreakdownErr(iter, true);
             retried = true;
@@ -719,9 +805,10 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         std::vector<double> Y;
         projected_eig(nev, theta, Y);
         combine_into(S, nev, Y, nev, Xv);
+        if (recur_) combine_into(AS, nev, Y, nev, AXv);
         break;
     }
-    residuals(Xv, theta, res, thr);
+    residual_step(0);
     record(0);
 
     while (iter < o.max_iters && !res.all_converged()) {
@@ -737,25 +824,27 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
             gather_cols(n_, Rv, active.data(), na, block(pW_, na), s_);
             RI = block(pW_, na);
         }
-        const View HI = block(H_.p, na);
+        const View HI = block(pH_, na);
         ctx_->prof.mark(s_, "lobpcg_misc");
         apply_precond(RI, na, HI);
+        const View AHI = recur_ ? block(AH_.p, na) : View{};
+        if (recur_) spmm_store(HI, na, AHI);  // the recurrence's one SpMM per iteration
         ctx_->prof.mark(s_, "precond_apply");
 
         int nx = 0, nh = 0, np = 0;
         for (;;) {
-            Orth ox = b_orth(Xv, nev, View{}, 0, S, res);
+            Orth ox = orth(Xv, nev, View{}, 0, S, AXv);
             bool breakdown = false;
             if (ox.kept < nev) {
                 breakdown = true;
             } else {
                 nx = ox.kept;
-                Orth oh = b_orth(HI, na, S, nx, S.sub(nx, m3 - nx), res);
+                Orth oh = orth(HI, na, S, nx, S.sub(nx, m3 - nx), AHI);
                 nh = oh.kept;
                 np = 0;
                 if (p_cols > 0) {
-                    Orth op = b_orth(block(P_.p, p_cols), p_cols, S, nx + nh,
-                                     S.sub(nx + nh, m3 - nx - nh), res);
+                    Orth op = orth(block(P_.p, p_cols), p_cols, S, nx + nh, S.sub(nx + nh, m3 - nx - nh),
+                                   recur_ ? block(AP_.p, p_cols) : View{});
                     np = op.kept;
                 }
             }
@@ -772,8 +861,9 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         projected_eig(m, theta, Y);
         ctx_->prof.mark(s_, "rayleigh_ritz");
         combine_into(S, m, Y, nev, Xv);
+        if (recur_) combine_into(AS, m, Y, nev, AXv);
         ctx_->prof.mark(s_, "combine");
-        residuals(Xv, theta, res, thr);
+        residual_step(iter);
         ctx_->prof.mark(s_, "residual");
 
         std::vector<int> next;
@@ -787,6 +877,7 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
                 for (int r = 0; r < hpc; ++r)
                     Yhp[static_cast<size_t>(c) * hpc + r] = Y[static_cast<size_t>(next[c]) * m + hp + r];
             combine_into(S.sub(hp, hpc), hpc, Yhp, nn, block(P_.p, nn));
+            if (recur_) combine_into(AS.sub(hp, hpc), hpc, Yhp, nn, block(AP_.p, nn));
             p_cols = nn;
         } else {
             p_cols = 0;

@@ -51,6 +51,13 @@ public:
 
     void set_jacobi(const double* inv_diag_dev) { prec_ = PREC_JACOBI; inv_diag_ = inv_diag_dev; }
     void set_none() { prec_ = PREC_NONE; }
+    // AX/AH/AP recurrence: A is applied to the new H block only;
+    // A*S, A*X and A*P follow the same small-matrix transforms as S, X and P, the
+    // residual R = AX - BX diag(theta) needs no SpMM, and A*X is recomputed exactly
+    // every kTrueResidualEvery iterations and whenever the recurrence says converged.
+    // Off by default (the reference recomputes A*S and A*X every iteration,
+    // eigensolver.cpp:138-155, 210-222).
+    void set_recurrence(bool on) { recur_ = on; }
     // amg_build (preconditioners.cpp:722-728) on the explicit fine operator A0 (moved in)
     void build_amg(CsrDev&& A0, DBuf<double>&& diag0, const AmgCfg& cfg);
     const Amg* amg() const { return amg_.get(); }
@@ -83,7 +90,13 @@ private:
         int kept = 0;
         std::vector<int> kept_idx;
     };
-    Orth b_orth(const View& V, int k, const View& against, int a, const View& dst, SolveResult& st);
+    // With AV (= A V), Aagainst and Adst (recurrence), every transform of V into dst is
+    // applied to AV into Adst as well, so Adst = A dst on return.
+    Orth b_orth(const View& V, int k, const View& against, int a, const View& dst, SolveResult& st,
+                const View* AV = nullptr, const View* Aagainst = nullptr, const View* Adst = nullptr);
+    void ts_mirror(const TsSpec& spec);  // a transform of a TsSpec without its Gram (recurrence side)
+    void residuals_from(const View& X, const View& AX, const std::vector<double>& theta, SolveResult& r,
+                        double thr);
     Orth b_orth_slow(const View& src, int k, const View& against, int a, const View& dst,
                      const std::vector<double>& orig, SolveResult& st);
     // gram helpers: run ts, all-reduce over ranks, copy to host (col-major)
@@ -109,6 +122,9 @@ private:
     const double* inv_diag_ = nullptr;
     std::vector<double> roots_;
     std::unique_ptr<Amg> amg_;
+    bool recur_ = false;
+    double* pH_ = nullptr;      // H is an SpMM input (recurrence: A*H)
+    DBuf<double> AX_, AP_, AH_;
 
     DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
     EllPatStore ellpat_; // its pattern-compressed form (ellpat.cu)

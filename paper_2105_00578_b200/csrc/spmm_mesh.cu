@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
     __shared__ double s_theta[kMaxCols];
-    __shared__ double s_sq[kConsumers / 32][kMaxCols];
+    __shared__ double s_sq[EPI == EPI_RESIDUAL ? kConsumers / 32 : 1][kMaxCols];
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
@@ -125,55 +125,79 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         return;
     }
 
-    // ---- consumers
-    int64_t g = 0;  // sequence number of the stage holding plane z0 - 1 of the current item
+    // ---- consumers: (slot, phase) of the next stage in sequence, advanced without divisions
+    int qs = 0;
+    unsigned qph = 0;
+    auto advance = [&](int& sl, unsigned& ph) {
+        if (++sl == geo.nst) {
+            sl = 0;
+            ph ^= 1u;
+        }
+    };
+    auto release = [&](int sl) {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + sl)) : "memory");
+    };
+    const int64_t nxny = static_cast<int64_t>(geo.nx) * geo.ny;
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         int c, tx, ty, z0, z1;
         decode(it, c, tx, ty, z0, z1);
         const int x = tx * kTile + lane;
         const bool xin = x < geo.nx;
+        // per item: this thread's rows of one plane (offsets within a plane), y neighbours
+        int64_t roff[4];
+        bool live[4], ym[4], yp[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int y = ty * kTile + warp + 8 * j;
+            live[j] = xin && y < geo.ny;
+            ym[j] = y > 0;
+            yp[j] = y + 1 < geo.ny;
+            roff[j] = static_cast<int64_t>(y) * geo.nx + x;
+        }
+        const bool xm = xin && x > 0, xp = x + 1 < geo.nx;
+        double* ycol = ea.Y.ptr + static_cast<int64_t>(c) * ea.Y.cs;  // column-major (rs == 1)
+        double* hcol = EPI == EPI_POLY ? ea.H.ptr + static_cast<int64_t>(c) * ea.H.cs : nullptr;
         // planes z0 - 1 and z0 first
-        mbar_wait(full + (g % geo.nst), static_cast<unsigned>((g / geo.nst) & 1));
-        mbar_wait(full + ((g + 1) % geo.nst), static_cast<unsigned>(((g + 1) / geo.nst) & 1));
+        int sp = qs;
+        unsigned pp = qph;
+        int sc = sp;
+        unsigned pc = pp;
+        advance(sc, pc);
+        mbar_wait(full + sp, pp);
+        mbar_wait(full + sc, pc);
         for (int z = z0; z < z1; ++z) {
-            const int64_t gz = g + (z - z0) + 1;  // stage of plane z
-            bool live[4];
-            int64_t row[4];
+            int sn = sc;
+            unsigned pn2 = pc;
+            advance(sn, pn2);
+            const int64_t zoff = static_cast<int64_t>(z) * nxny;
             double bd[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int y = ty * kTile + warp + 8 * j;
-                live[j] = xin && y < geo.ny;
-                row[j] = (static_cast<int64_t>(z) * geo.ny + y) * geo.nx + x;
-                bd[j] = (EPI == EPI_RESIDUAL && ea.bdiag && live[j]) ? ea.bdiag[row[j]] : 1.0;
-            }
-            mbar_wait(full + ((gz + 1) % geo.nst), static_cast<unsigned>(((gz + 1) / geo.nst) & 1));
-            const double* p0 = smem + static_cast<size_t>((gz - 1) % geo.nst) * geo.stage;  // plane z - 1
-            const double* p1 = smem + static_cast<size_t>(gz % geo.nst) * geo.stage;        // plane z
-            const double* p2 = smem + static_cast<size_t>((gz + 1) % geo.nst) * geo.stage;  // plane z + 1
+            for (int j = 0; j < 4; ++j)
+                bd[j] = (EPI == EPI_RESIDUAL && ea.bdiag && live[j]) ? ea.bdiag[zoff + roff[j]] : 1.0;
+            mbar_wait(full + sn, pn2);
+            const double* p0 = smem + static_cast<size_t>(sp) * geo.stage;  // plane z - 1
+            const double* p1 = smem + static_cast<size_t>(sc) * geo.stage;  // plane z
+            const double* p2 = smem + static_cast<size_t>(sn) * geo.stage;  // plane z + 1
             const double* hs = p2 + kXPlanePad;
-            // x / z neighbours present (mesh_plan verified every row is its full in-bounds stencil)
-            const bool xm = xin && x > 0, xp = x + 1 < geo.nx, zm = z > 0, zp = z + 1 < geo.nz;
+            const bool zm = z > 0, zp = z + 1 < geo.nz;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int ly = warp + 8 * j;
-                const int y = ty * kTile + ly;
-                const bool ym = y > 0, yp = y + 1 < geo.ny;
                 const int ctr = (ly + 1) * kHaloW + lane + 2;  // this row's element in its plane box
                 const double xi = p1[ctr];
                 double acc = 0.0;
                 // the row's entries in storage (= ascending column = lexicographic (dz, dy, dx))
                 // order: acc -= x_j before the diagonal, += deg * x_i, -= x_j after it —
                 // build_combinatorial's order, so the sum is bit-identical to spmv_block
-                int deg = 0;
                 if constexpr (BOX27) {
+                    int deg = 0;
 #pragma unroll
                     for (int t = 0; t < 27; ++t) {
                         const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
                         if (t == 13) continue;
-                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym : dy > 0 ? yp : true) &&
-                                        (dx < 0 ? xm : dx > 0 ? xp : true);
-                        deg += on ? 1 : 0;
+                        deg += ((dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym[j] : dy > 0 ? yp[j] : true) &&
+                                (dx < 0 ? xm : dx > 0 ? xp : true)) ? 1 : 0;
                     }
 #pragma unroll
                     for (int t = 0; t < 27; ++t) {
@@ -183,36 +207,34 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                             acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
                             continue;
                         }
-                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym : dy > 0 ? yp : true) &&
-                                        (dx < 0 ? xm : dx > 0 ? xp : true);
+                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) &&
+                                        (dy < 0 ? ym[j] : dy > 0 ? yp[j] : true) && (dx < 0 ? xm : dx > 0 ? xp : true);
                         if (on) acc = __dsub_rn(acc, pl[ctr + dy * kHaloW + dx]);
                     }
                 } else {
-                    deg = zm + ym + xm + xp + yp + zp;
+                    const int deg = zm + ym[j] + xm + xp + yp[j] + zp;
                     if (zm) acc = __dsub_rn(acc, p0[ctr]);
-                    if (ym) acc = __dsub_rn(acc, p1[ctr - kHaloW]);
+                    if (ym[j]) acc = __dsub_rn(acc, p1[ctr - kHaloW]);
                     if (xm) acc = __dsub_rn(acc, p1[ctr - 1]);
                     acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
                     if (xp) acc = __dsub_rn(acc, p1[ctr + 1]);
-                    if (yp) acc = __dsub_rn(acc, p1[ctr + kHaloW]);
+                    if (yp[j]) acc = __dsub_rn(acc, p1[ctr + kHaloW]);
                     if (zp) acc = __dsub_rn(acc, p2[ctr]);
                 }
                 double sq = 0.0;
                 if (live[j]) {
+                    const int64_t r = zoff + roff[j];
                     if (EPI == EPI_STORE) {
-                        ea.Y.at(row[j], c) = acc;
+                        ycol[r] = acc;
                     } else if (EPI == EPI_RESIDUAL) {
                         const double bx = ea.bdiag ? __dmul_rn(bd[j], xi) : xi;
-                        const double r = __dsub_rn(acc, __dmul_rn(s_theta[c], bx));
-                        ea.Y.at(row[j], c) = r;
-                        sq = r * r;
+                        const double rr = __dsub_rn(acc, __dmul_rn(s_theta[c], bx));
+                        ycol[r] = rr;
+                        sq = rr * rr;
                     } else {
                         const double pn = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
-                        ea.Y.at(row[j], c) = pn;
-                        if (ea.h_terms) {
-                            const double hv = geo.h_stage ? hs[ly * kTile + lane] : 0.0;
-                            ea.H.at(row[j], c) = poly_h(ea, hv, xi, pn);
-                        }
+                        ycol[r] = pn;
+                        if (ea.h_terms) hcol[r] = poly_h(ea, geo.h_stage ? hs[ly * kTile + lane] : 0.0, xi, pn);
                     }
                 }
                 if (EPI == EPI_RESIDUAL) {
@@ -222,21 +244,17 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                     if (lane == 0) s_sq[warp][c] += v;
                 }
             }
-            // plane z - 1 is no longer needed by this item
-            __syncwarp();
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + ((gz - 1) % geo.nst)))
-                             : "memory");
+            release(sp);  // plane z - 1 is no longer needed by this item
+            sp = sc;
+            pp = pc;
+            sc = sn;
+            pc = pn2;
         }
-        // release planes z1 - 1 and z1
-        const int64_t gl = g + (z1 - z0);
-        __syncwarp();
-        if (lane == 0) {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + (gl % geo.nst))) : "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + ((gl + 1) % geo.nst)))
-                         : "memory");
-        }
-        g += (z1 - z0) + 2;
+        release(sp);  // planes z1 - 1 and z1
+        release(sc);
+        qs = sc;
+        qph = pc;
+        advance(qs, qph);
     }
     if (EPI == EPI_RESIDUAL) {
         asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -297,9 +315,14 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
         SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    // ring: up to 6 stages, sized so two CTAs share an SM
+    // ring: up to 6 stages, sized so `ctas` CTAs share an SM
+    static const int ring_ctas = [] {  // A/B diagnostics only
+        const char* e = std::getenv("SPB_MESH_CTAS");
+        return e ? std::max(2, std::atoi(e)) : 2;
+    }();
     const size_t per_stage = sizeof(double) * geo.stage;
-    geo.nst = static_cast<int>(std::min<size_t>(6, (100 * 1024) / per_stage));
+    const size_t budget = ring_ctas >= 3 ? 72 * 1024 : 100 * 1024;
+    geo.nst = static_cast<int>(std::min<size_t>(6, budget / per_stage));
     const size_t smem = per_stage * geo.nst;
     int per_sm = 0;
     SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMeshThreads, smem));
@@ -400,7 +423,7 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
     auto ok = [&](const View& v) {
         return v.rs == 1 && reinterpret_cast<uintptr_t>(v.ptr) % 16 == 0 && (m == 1 || (v.cs % 2 == 0 && v.cs >= op.n));
     };
-    if (!ok(X) || ea.Y.rs != 1) return false;
+    if (!ok(X) || ea.Y.rs != 1 || (ea.mode == EPI_POLY && ea.h_terms && ea.H.rs != 1)) return false;
     if (ea.mode == EPI_POLY && ea.h_terms && !ea.first && !ok(ea.H)) return false;
     return true;
 }
