@@ -217,7 +217,9 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     const double nrows = static_cast<double>(A_.n);
     const double csr_b = idx_b * static_cast<double>(A_.nnz) + 8.0 * (nrows + 1);
     double op_b = csr_b;
-    if (A_.ell_pat)
+    if (!fused && !halo_ && spmm_mesh_ok(A_, Xg, m, ea))
+        op_b = 0.0;  // structured mesh: the stencil is implicit, no index bytes (spmm_mesh.cu)
+    else if (A_.ell_pat)
         op_b = nrows + 4.0 * A_.ell_npat * (A_.ell_kl + A_.ell_ku) + 8.0 * A_.ell_npat;
     else if (A_.ell)
         op_b = 4.0 * (A_.ell_kl + A_.ell_ku) * nrows + 8.0 * nrows;

@@ -139,6 +139,10 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + sl)) : "memory");
     };
     const int64_t nxny = static_cast<int64_t>(geo.nx) * geo.ny;
+    // tile rows of this thread: 27-point: four consecutive rows (the (dy, dx) neighbours of
+    // the four outputs share registers: 18 shared-memory loads per plane instead of 36);
+    // 7-point: rows warp, warp + 8, ...
+    auto row_of = [&](int j) { return BOX27 ? 4 * warp + j : warp + 8 * j; };
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         int c, tx, ty, z0, z1;
         decode(it, c, tx, ty, z0, z1);
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         bool live[4], ym[4], yp[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int y = ty * kTile + warp + 8 * j;
+            const int y = ty * kTile + row_of(j);
             live[j] = xin && y < geo.ny;
             ym[j] = y > 0;
             yp[j] = y + 1 < geo.ny;
@@ -181,37 +185,50 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
             const double* p2 = smem + static_cast<size_t>(sn) * geo.stage;  // plane z + 1
             const double* hs = p2 + kXPlanePad;
             const bool zm = z > 0, zp = z + 1 < geo.nz;
+            // the rows' entries in storage (= ascending column = lexicographic (dz, dy, dx))
+            // order: acc -= x_j before the diagonal, += deg * x_i, -= x_j after it —
+            // build_combinatorial's order, so each sum is bit-identical to spmv_block
+            double accv[4], xiv[4];
+            if constexpr (BOX27) {
+                int deg[4];
+                const int cx = 1 + xm + xp, cz = 1 + zm + zp;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int ly = warp + 8 * j;
-                const int ctr = (ly + 1) * kHaloW + lane + 2;  // this row's element in its plane box
-                const double xi = p1[ctr];
-                double acc = 0.0;
-                // the row's entries in storage (= ascending column = lexicographic (dz, dy, dx))
-                // order: acc -= x_j before the diagonal, += deg * x_i, -= x_j after it —
-                // build_combinatorial's order, so the sum is bit-identical to spmv_block
-                if constexpr (BOX27) {
-                    int deg = 0;
+                for (int j = 0; j < 4; ++j) {
+                    deg[j] = cx * (1 + ym[j] + yp[j]) * cz - 1;
+                    accv[j] = 0.0;
+                    xiv[j] = p1[(row_of(j) + 1) * kHaloW + lane + 2];
+                }
+                const int r0 = 4 * warp;  // box row of tile row r0 - 1
 #pragma unroll
-                    for (int t = 0; t < 27; ++t) {
-                        const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
-                        if (t == 13) continue;
-                        deg += ((dz < 0 ? zm : dz > 0 ? zp : true) && (dy < 0 ? ym[j] : dy > 0 ? yp[j] : true) &&
-                                (dx < 0 ? xm : dx > 0 ? xp : true)) ? 1 : 0;
-                    }
+                for (int dzi = 0; dzi < 3; ++dzi) {
+                    const double* pl = dzi == 0 ? p0 : dzi == 1 ? p1 : p2;
+                    const bool zon = dzi == 0 ? zm : dzi == 2 ? zp : true;
+                    double v[6][3];  // box rows r0 .. r0 + 5 (tile rows r0 - 1 .. r0 + 4), x - 1 .. x + 1
 #pragma unroll
-                    for (int t = 0; t < 27; ++t) {
-                        const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
-                        const double* pl = dz < 0 ? p0 : dz > 0 ? p2 : p1;
-                        if (t == 13) {
-                            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
-                            continue;
-                        }
-                        const bool on = (dz < 0 ? zm : dz > 0 ? zp : true) &&
-                                        (dy < 0 ? ym[j] : dy > 0 ? yp[j] : true) && (dx < 0 ? xm : dx > 0 ? xp : true);
-                        if (on) acc = __dsub_rn(acc, pl[ctr + dy * kHaloW + dx]);
-                    }
-                } else {
+                    for (int r = 0; r < 6; ++r)
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) v[r][d] = pl[(r0 + r) * kHaloW + lane + 1 + d];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int dyi = 0; dyi < 3; ++dyi)
+#pragma unroll
+                            for (int dxi = 0; dxi < 3; ++dxi) {
+                                if (dzi == 1 && dyi == 1 && dxi == 1) {
+                                    accv[j] = __dadd_rn(accv[j], __dmul_rn(static_cast<double>(deg[j]), xiv[j]));
+                                    continue;
+                                }
+                                const bool on = zon && (dyi == 0 ? ym[j] : dyi == 2 ? yp[j] : true) &&
+                                                (dxi == 0 ? xm : dxi == 2 ? xp : true);
+                                if (on) accv[j] = __dsub_rn(accv[j], v[j + dyi][dxi]);
+                            }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int ctr = (row_of(j) + 1) * kHaloW + lane + 2;  // this row's element in its plane box
+                    const double xi = p1[ctr];
+                    double acc = 0.0;
                     const int deg = zm + ym[j] + xm + xp + yp[j] + zp;
                     if (zm) acc = __dsub_rn(acc, p0[ctr]);
                     if (ym[j]) acc = __dsub_rn(acc, p1[ctr - kHaloW]);
@@ -220,7 +237,14 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                     if (xp) acc = __dsub_rn(acc, p1[ctr + 1]);
                     if (yp[j]) acc = __dsub_rn(acc, p1[ctr + kHaloW]);
                     if (zp) acc = __dsub_rn(acc, p2[ctr]);
+                    accv[j] = acc;
+                    xiv[j] = xi;
                 }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int ly = row_of(j);
+                const double acc = accv[j], xi = xiv[j];
                 double sq = 0.0;
                 if (live[j]) {
                     const int64_t r = zoff + roff[j];

@@ -59,3 +59,93 @@ def test_row_partition_covers_rows_once(n, world):
     else:
         assert sum(nl for _, nl in parts) == n
         assert all(parts[k][0] == k * ((n + world - 1) // world) for k in range(world))
+
+
+# ---- the halo plan of csrc/halo.cu, restated on the host and run over gloo -------------
+def _halo_plan(offs, cols, n, world, rank):
+    """localize_operator (halo.cu:1-17): own rows [row0, row0+nloc); the foreign columns in
+    ascending id (hence grouped by owner); columns rewritten to local ids (own j -> j-row0,
+    halo j -> base + slot, base = nloc rounded up to 32 rows after the zero row); dpos[i] =
+    stored columns with global id < global i (where build_combinatorial splices the diagonal)."""
+    import numpy as np
+    r0, nl = row_partition(n, world)[rank]
+    k0, k1 = offs[r0], offs[r0 + nl]
+    lc = cols[k0:k1].astype(np.int64)
+    foreign = (lc < r0) | (lc >= r0 + nl)
+    halo = np.unique(lc[foreign])
+    base = ((nl + 1 + 31) // 32) * 32
+    loc = np.where(foreign, base + np.searchsorted(halo, lc), lc - r0)
+    rows = np.repeat(np.arange(nl), np.diff(offs[r0:r0 + nl + 1]))
+    dpos = np.bincount(rows, weights=(lc < (r0 + rows)), minlength=nl).astype(np.int64)
+    return r0, nl, offs[r0:r0 + nl + 1] - k0, loc, halo, base, dpos
+
+
+def _spmv_worker(rank, world, port, q):
+    import numpy as np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2105_00578_b200 import generators as gen
+        g = gen.rmat(10, 8, seed=11)[0]
+        n, offs, cols = g.n, g.row_offsets, g.col_indices
+        deg = np.diff(offs).astype(np.float64)
+        X = np.random.default_rng(5).integers(-9, 10, (n, 3)).astype(np.float64)
+        r0, nl, loffs, loc, halo, base, dpos = _halo_plan(offs, cols, n, world, rank)
+        # halo id lists go to their owners (all-gathered here), which become the send lists
+        lists = [None] * world
+        dist.all_gather_object(lists, halo.tolist())
+        n_pad = (n + world - 1) // world
+        send = {p: [j - r0 for j in lists[p] if r0 <= j < r0 + nl] for p in range(world) if p != rank}
+        # one exchange round: pack the rows each peer needs, receive the halo rows in list order
+        packs = [None] * world
+        dist.all_gather_object(packs, {p: X[r0 + np.asarray(s, dtype=np.int64)].tolist() for p, s in send.items()})
+        Xl = np.zeros((base + halo.size, 3))
+        Xl[:nl] = X[r0:r0 + nl]
+        got = []
+        for p in range(world):
+            if p != rank and packs[p].get(rank):
+                got.extend(packs[p][rank])
+        Xl[base:] = np.asarray(got).reshape(-1, 3)
+        assert np.all(halo // n_pad != rank)
+        # L_C rows in storage order: -x_j, the diagonal at slot dpos (laplacian.cpp:53-79)
+        Y = np.zeros((nl, 3))
+        for i in range(nl):
+            acc = np.zeros(3)
+            ks = range(loffs[i], loffs[i + 1])
+            for t, k in enumerate(ks):
+                if t == dpos[i]:
+                    acc = acc + deg[r0 + i] * Xl[i]
+                acc = acc - Xl[loc[k]]
+            if dpos[i] == len(ks):
+                acc = acc + deg[r0 + i] * Xl[i]
+            Y[i] = acc
+        ys = [None] * world
+        dist.all_gather_object(ys, Y.tolist())
+        q.put((rank, np.concatenate([np.asarray(y).reshape(-1, 3) for y in ys]).tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_plan_row_partitioned_spmv_is_exact(world):
+    import numpy as np
+    from paper_2105_00578_b200 import generators as gen
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spmv_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = gen.rmat(10, 8, seed=11)[0]
+    X = np.random.default_rng(5).integers(-9, 10, (g.n, 3)).astype(np.float64)
+    deg = np.diff(g.row_offsets).astype(np.float64)
+    rows = np.repeat(np.arange(g.n), np.diff(g.row_offsets))
+    Y = deg[:, None] * X
+    np.subtract.at(Y, rows, X[g.col_indices])
+    for r in range(world):
+        assert got[r] == got[0]
+    assert np.frombuffer(got[0]).reshape(-1, 3).tobytes() == Y.tobytes()
