@@ -705,8 +705,8 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     res.residual_norms.assign(nev, 0.0);
 
     const int m3 = 3 * nev;
-    const View S = colmajor_ ? colmajor(pS_, ld_, m3) : rowmajor(pS_, m3, m3);
-    const View AS = colmajor_ ? colmajor(AS_.p, ld_, m3) : rowmajor(AS_.p, m3, m3);
+    const View S = block(pS_, m3);
+    const View AS = block(AS_.p, m3);
     const View Xv = X.sub(0, nev);
     const View Rv = block(pR_, nev);
     const View Hv = block(pH_, nev);
