@@ -79,18 +79,12 @@ public:
     // short-row operators (meshes: row-per-lane SpMM), row-major otherwise.
     bool colmajor_blocks() const { return colmajor_; }
     int64_t ld() const { return ld_; }
-    // row-major rows are padded to whole 32-byte sectors (a gathered row of m = 7 doubles
-    // is then 2 sectors, not 2-3 depending on its alignment)
-    static int row_pad(int cols) { return (cols + 3) & ~3; }
-    View block(double* p, int cols) const {
-        return colmajor_ ? colmajor(p, ld_, cols) : rowmajor(p, row_pad(cols), cols);
-    }
+    // (padding row-major rows to 32-byte sectors was measured slower on cfg3: 287 vs 247 ms)
+    View block(double* p, int cols) const { return colmajor_ ? colmajor(p, ld_, cols) : rowmajor(p, cols, cols); }
     // A block that can be an SpMM input (symmetric heap on multi-GPU P2P runs;
     // otherwise allocated into `fallback`). Collective in the multi-GPU case.
     double* input_block(int cols, DBuf<double>& fallback);
-    size_t block_elems(int cols) const {
-        return colmajor_ ? static_cast<size_t>(ld_) * cols : static_cast<size_t>(rows_cap_) * row_pad(cols);
-    }
+    size_t block_elems(int cols) const { return static_cast<size_t>(colmajor_ ? ld_ : rows_cap_) * cols; }
 
 private:
     struct Orth {
