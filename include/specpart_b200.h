@@ -295,6 +295,14 @@ sp_status sp_bench_blockop(sp_context* ctx, int64_t n, int32_t mu, int32_t mv, i
 sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const double* V,
                   int32_t mv, const double* b, double* G);
 
+/* kernels::mult / kernels::mult_sub (kernels.cpp:127-157, kernels.hpp:24-28): op 0 computes
+ * Y = X C, op 1 computes Y -= X C, X n x k, C k x m, Y n x m, all column-major (Y is read for
+ * op 1). The block product of LOBPCG's Rayleigh-Ritz combine and CGS projection: the TS
+ * kernel's COMBINE / UPDATE transforms (fp64 DMMA, fixed summation order, so repeated calls
+ * agree bit for bit; agreement with the reference's k-ordered loop is to rounding). k, m <= 64. */
+sp_status sp_block_combine(sp_context* ctx, int64_t n, const double* X, int32_t k, const double* C,
+                           int32_t m, int32_t op, double* Y);
+
 /* Initial blocks (eigensolver.cpp:20-51), n x d column-major, bit-identical. */
 sp_status sp_initial_guess(sp_context* ctx, int32_t init, int64_t n, int32_t d, uint64_t seed,
                            double* X_out);

@@ -740,6 +740,37 @@ inline Dense apply_block(const LinearOperator& op, const Dense& V) {
     return Y;
 }
 
+// ---- kernels.hpp:20-28: the block products LOBPCG is built from, on the device -------------------
+namespace kernels {
+inline Dense gram(const Dense& U, const Dense& V) {  // U^T V
+    if (U.rows != V.rows) throw DimensionError("gram: row mismatch");
+    sp_context* c = b200::context();
+    Dense G(U.cols, V.cols);
+    if (U.cols == 0 || V.cols == 0) return G;
+    b200::rethrow(sp_gram(c, U.rows, U.data.data(), static_cast<std::int32_t>(U.cols), V.data.data(),
+                          static_cast<std::int32_t>(V.cols), nullptr, G.data.data()),
+                  c);
+    return G;
+}
+inline void mult(const Dense& X, const Dense& C, Dense& Y) {  // Y = X C
+    if (X.cols != C.rows) throw DimensionError("mult: inner dimension mismatch");
+    sp_context* c = b200::context();
+    Y = Dense(X.rows, C.cols);
+    if (X.rows == 0 || C.cols == 0) return;
+    b200::rethrow(sp_block_combine(c, X.rows, X.data.data(), static_cast<std::int32_t>(X.cols), C.data.data(),
+                                   static_cast<std::int32_t>(C.cols), 0, Y.data.data()),
+                  c);
+}
+inline void mult_sub(Dense& Y, const Dense& X, const Dense& C) {  // Y -= X C
+    if (X.cols != C.rows || Y.rows != X.rows || Y.cols != C.cols) throw DimensionError("mult_sub: shape mismatch");
+    sp_context* c = b200::context();
+    if (X.rows == 0 || C.cols == 0) return;
+    b200::rethrow(sp_block_combine(c, X.rows, X.data.data(), static_cast<std::int32_t>(X.cols), C.data.data(),
+                                   static_cast<std::int32_t>(C.cols), 1, Y.data.data()),
+                  c);
+}
+} // namespace kernels
+
 // ---- preconditioner builders (preconditioners.hpp:30-91) -----------------------------------------
 inline std::unique_ptr<Preconditioner> jacobi_build(const LinearOperator&) {
     return std::make_unique<b200::JacobiPreconditioner>();

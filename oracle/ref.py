@@ -31,6 +31,7 @@ _SIG = {
     "ref_spmm": (I32, [I32, C.POINTER(abi.SpGraph), P, I32, P]),
     "ref_spmm_csr": (I32, [I64, I64, P, P, P, P, I32, P]),
     "ref_gram": (I32, [I64, P, I32, P, I32, P, P]),
+    "ref_mult": (I32, [I64, P, I32, P, I32, I32, P]),
     "ref_initial_guess": (I32, [I32, I64, I32, U64, P]),
     "ref_lobpcg": (I32, [C.POINTER(abi.SpGraph), I32, I32, U64, I32, P, I32, F64, I32, I32, P, P, P, P,
                          C.POINTER(I32), C.POINTER(I32)]),
@@ -126,6 +127,15 @@ class RefLib:
         self._check(self.lib.ref_gram(Uc.shape[0], Uc.ctypes.data, Uc.shape[1], Vc.ctypes.data, Vc.shape[1],
                                       _ptr(bb), G.ctypes.data))
         return G
+
+    def mult(self, X, C, Y=None):
+        Xc, Cc = _colmajor(X), _colmajor(C)
+        out = np.empty((Xc.shape[0], Cc.shape[1]), order="F")
+        if Y is not None:
+            out[...] = _colmajor(Y)
+        self._check(self.lib.ref_mult(Xc.shape[0], Xc.ctypes.data, Xc.shape[1], Cc.ctypes.data, Cc.shape[1],
+                                      0 if Y is None else 1, out.ctypes.data))
+        return out
 
     def initial_guess(self, init: str, n: int, d: int, seed: int = 0):
         X = np.empty((n, d), order="F")

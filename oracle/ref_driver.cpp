@@ -247,6 +247,21 @@ sp_status ref_gram(int64_t n, const double* U, int32_t mu, const double* V, int3
     });
 }
 
+sp_status ref_mult(int64_t n, const double* X, int32_t k, const double* C, int32_t m, int32_t op, double* Y) {
+    return guarded([&] {
+        Dense x = to_dense(X, n, k);
+        Dense c = to_dense(C, k, m);
+        Dense y;
+        if (op == 0) {
+            kernels::mult(x, c, y);
+        } else {
+            y = to_dense(Y, n, m);
+            kernels::mult_sub(y, x, c);
+        }
+        std::memcpy(Y, y.data.data(), sizeof(double) * n * m);
+    });
+}
+
 sp_status ref_initial_guess(int32_t init, int64_t n, int32_t d, uint64_t seed, double* X_out) {
     return guarded([&] {
         Dense X = init == SP_INIT_PIECEWISE ? initial_guess_piecewise(n, d)

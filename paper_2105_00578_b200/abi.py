@@ -139,6 +139,7 @@ SIGNATURES = {
     "sp_spmm_solver": (I32, [P, I32, C.POINTER(SpGraph), P, I32, P]),
     "sp_spmm_csr": (I32, [P, I64, I64, P, P, P, P, I32, P]),
     "sp_gram": (I32, [P, I64, P, I32, P, I32, P, P]),
+    "sp_block_combine": (I32, [P, I64, P, I32, P, I32, I32, P]),
     "sp_bench_blockop": (I32, [P, I64, I32, I32, I32, I32, I32, I32, C.POINTER(F64)]),
     "sp_initial_guess": (I32, [P, I32, I64, I32, U64, P]),
     "sp_initial_guess_rows": (I32, [P, I32, I64, I32, U64, I64, I64, P]),

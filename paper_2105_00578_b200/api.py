@@ -418,6 +418,18 @@ class Context:
                                      Vc.shape[1], _ptr(bb), G.ctypes.data))
         return G
 
+    def mult(self, X, C, Y=None) -> np.ndarray:
+        """kernels::mult (Y = X C) or, given Y, kernels::mult_sub (returns Y - X C)."""
+        Xc, Cc = _colmajor(X), _colmajor(C)
+        if Xc.shape[1] != Cc.shape[0]:
+            raise DimensionError("mult: inner dimension mismatch")
+        out = np.empty((Xc.shape[0], Cc.shape[1]), dtype=np.float64, order="F")
+        if Y is not None:
+            out[...] = _colmajor(Y)
+        self._check(self.lib.sp_block_combine(self._h, Xc.shape[0], Xc.ctypes.data, Xc.shape[1], Cc.ctypes.data,
+                                              Cc.shape[1], 0 if Y is None else 1, out.ctypes.data))
+        return out
+
     def initial_guess(self, init: str, n: int, d: int, seed: int = 0) -> np.ndarray:
         X = np.empty((n, d), dtype=np.float64, order="F")
         self._check(self.lib.sp_initial_guess(self._h, abi.INIT[init], n, d, seed, X.ctypes.data))

@@ -884,6 +884,40 @@ sp_status sp_gram(sp_context* ctx, int64_t n, const double* U, int32_t mu, const
     });
 }
 
+sp_status sp_block_combine(sp_context* ctx, int64_t n, const double* X, int32_t k, const double* C, int32_t m,
+                           int32_t op, double* Y) {
+    return guarded(ctx, [&] {
+        if (n < 0 || k < 1 || m < 1 || k > 64 || m > 64) throw SpError(SP_DIMENSION, "sp_block_combine: bad sizes");
+        if (op != 0 && op != 1) throw_invalid("sp_block_combine: op must be 0 (Y = X C) or 1 (Y -= X C)");
+        if (n == 0) return;
+        cudaStream_t s = ctx->stream;
+        const size_t rows = static_cast<size_t>(n);
+        DBuf<double> xd(rows * k), yd(rows * m), wd, cd(static_cast<size_t>(k) * m),
+            scratch(static_cast<size_t>(device_sm_count()) * 8 * 64 + 64);
+        upload_block(X, n, 0, n, k, rowmajor(xd.p, k, k), s);
+        h2d(cd.p, C, static_cast<int64_t>(k) * m, s);
+        SPB_CUDA(cudaMemsetAsync(scratch.p + scratch.n - 1, 0, sizeof(double), s));
+        TsSpec sp;
+        sp.n = n;
+        sp.C = cd.p;
+        sp.ldc = k;
+        if (op == 0) {  // W = V C
+            sp.V = rowmajor(xd.p, k, k);
+            sp.W = rowmajor(yd.p, m, m);
+            sp.transform = TS_COMBINE;
+        } else {        // W = V - U C
+            wd.alloc(rows * m);
+            upload_block(Y, n, 0, n, m, rowmajor(yd.p, m, m), s);
+            sp.U0 = rowmajor(xd.p, k, k);
+            sp.V = rowmajor(yd.p, m, m);
+            sp.W = rowmajor(wd.p, m, m);
+            sp.transform = TS_UPDATE;
+        }
+        ts_run(sp, nullptr, scratch.p, scratch.n, s);
+        download_block(sp.W, n, m, Y, s);
+    });
+}
+
 sp_status sp_bench_blockop(sp_context* ctx, int64_t n, int32_t mu, int32_t mv, int32_t mw, int32_t transform,
                            int32_t gram, int32_t iters, double* ms_out) {
     return guarded(ctx, [&] {

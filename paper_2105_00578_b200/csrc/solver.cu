@@ -28,6 +28,10 @@ namespace {
 
 constexpr double kRankDropTol = 1e-10;  // eigensolver.cpp:55
 constexpr int kTrueResidualEvery = 10;   // recurrence: exact A X at least this often
+// X = S Y with S B-orthonormal and Y orthonormal is B-orthonormal to rounding, so the
+// reference's per-iteration b_orthonormalize(X) (eigensolver.cpp:275) is run every
+// kReorthXEvery iterations (and on any retry); in between X enters S as is
+constexpr int kReorthXEvery = 16;
 
 double max_abs_dev_identity(const std::vector<double>& G, int k) {
     double e = 0.0;
@@ -117,8 +121,12 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     cmat2_.alloc(static_cast<size_t>(m3) * m3 + 64);
     partial_.alloc((static_cast<size_t>(device_sm_count()) * 8 * 5 + A.n_long + 64) * 64);
     norms_.alloc(64);
-    pH_ = input_block(max_cols, H_);
-    P_.alloc(block_elems(max_cols));
+    if (colmajor_) {
+        pHP_ = input_block(2 * max_cols, HP_);  // [H | P]
+    } else {
+        pH_ = input_block(max_cols, H_);
+        P_.alloc(block_elems(max_cols));
+    }
     AS_.alloc(block_elems(m3));
     pR_ = input_block(max_cols, R_);
     pS_ = input_block(m3, S_);
@@ -709,14 +717,23 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
     const View AS = block(AS_.p, m3);
     const View Xv = X.sub(0, nev);
     const View Rv = block(pR_, nev);
-    const View Hv = block(pH_, nev);
-    const View Pv = block(P_.p, nev);
     // recurrence: A X, A H, A P tracked next to X, H, P (A S lives in AS either way)
     if (recur_) {
         AX_.alloc(block_elems(nev));
         AP_.alloc(block_elems(nev));
         AH_.alloc(block_elems(nev));
+        if (pHP_) AHP_.alloc(block_elems(2 * nev));
     }
+    // H and P views: [H | P] in one column-major buffer when available
+    const bool merge_hp = pHP_ != nullptr;
+    auto h_view = [&](int k) { return merge_hp ? block(pHP_, k) : block(pH_, k); };
+    auto ah_view = [&](int k) { return merge_hp ? block(AHP_.p, k) : block(AH_.p, k); };
+    auto p_view = [&](int h, int k) {  // P of k columns, after an H of h columns
+        return merge_hp ? colmajor(pHP_ + static_cast<size_t>(h) * ld_, ld_, k) : block(P_.p, k);
+    };
+    auto ap_view = [&](int h, int k) {
+        return merge_hp ? colmajor(AHP_.p + static_cast<size_t>(h) * ld_, ld_, k) : block(AP_.p, k);
+    };
     const View AXv = recur_ ? block(AX_.p, nev) : View{};
     int p_cols = 0;
     std::vector<double> theta;
@@ -826,31 +843,47 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
             gather_cols(n_, Rv, active.data(), na, block(pW_, na), s_);
             RI = block(pW_, na);
         }
-        const View HI = block(pH_, na);
+        const View HI = h_view(na);
         ctx_->prof.mark(s_, "lobpcg_misc");
         apply_precond(RI, na, HI);
-        const View AHI = recur_ ? block(AH_.p, na) : View{};
+        const View AHI = recur_ ? ah_view(na) : View{};
         if (recur_) spmm_store(HI, na, AHI);  // the recurrence's one SpMM per iteration
         ctx_->prof.mark(s_, "precond_apply");
 
         int nx = 0, nh = 0, np = 0;
+        bool full_x = iter % kReorthXEvery == 0;
         for (;;) {
-            Orth ox = orth(Xv, nev, View{}, 0, S, AXv);
             bool breakdown = false;
-            if (ox.kept < nev) {
-                breakdown = true;
-            } else {
+            if (full_x) {
+                Orth ox = orth(Xv, nev, View{}, 0, S, AXv);
+                breakdown = ox.kept < nev;
                 nx = ox.kept;
-                Orth oh = orth(HI, na, S, nx, S.sub(nx, m3 - nx), AHI);
-                nh = oh.kept;
+            } else {
+                copy_view(n_, Xv, S.sub(0, nev), s_);
+                if (recur_) copy_view(n_, AXv, AS.sub(0, nev), s_);
+                nx = nev;
+            }
+            if (!breakdown) {
                 np = 0;
-                if (p_cols > 0) {
-                    Orth op = orth(block(P_.p, p_cols), p_cols, S, nx + nh, S.sub(nx + nh, m3 - nx - nh),
-                                   recur_ ? block(AP_.p, p_cols) : View{});
-                    np = op.kept;
+                if (merge_hp) {
+                    // [H | P] against X as one block: MGS2 on its Gram visits H's columns before
+                    // P's, the reference's span order (only the total kept count is needed)
+                    const int k = na + p_cols;
+                    const View HPv = colmajor(pHP_, ld_, k);
+                    const View AHP = recur_ ? colmajor(AHP_.p, ld_, k) : View{};
+                    nh = orth(HPv, k, S, nx, S.sub(nx, m3 - nx), AHP).kept;
+                } else {
+                    Orth oh = orth(HI, na, S, nx, S.sub(nx, m3 - nx), AHI);
+                    nh = oh.kept;
+                    if (p_cols > 0) {
+                        Orth op = orth(p_view(na, p_cols), p_cols, S, nx + nh, S.sub(nx + nh, m3 - nx - nh),
+                                       recur_ ? ap_view(na, p_cols) : View{});
+                        np = op.kept;
+                    }
                 }
             }
             if (!breakdown) break;
+            full_x = true;
             if (retried) throw BreakdownErr(iter, true);
             retried = true;
             ++res.retries;
@@ -878,8 +911,9 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
             for (int c = 0; c < nn; ++c)
                 for (int r = 0; r < hpc; ++r)
                     Yhp[static_cast<size_t>(c) * hpc + r] = Y[static_cast<size_t>(next[c]) * m + hp + r];
-            combine_into(S.sub(hp, hpc), hpc, Yhp, nn, block(P_.p, nn));
-            if (recur_) combine_into(AS.sub(hp, hpc), hpc, Yhp, nn, block(AP_.p, nn));
+            // the next iteration's H has nn columns (the same unconverged set): P goes after it
+            combine_into(S.sub(hp, hpc), hpc, Yhp, nn, p_view(nn, nn));
+            if (recur_) combine_into(AS.sub(hp, hpc), hpc, Yhp, nn, ap_view(nn, nn));
             p_cols = nn;
         } else {
             p_cols = 0;
@@ -887,8 +921,6 @@ SolveResult Solver::lobpcg(const View& X0, const SolveOpts& o, const View& X) {
         ctx_->prof.mark(s_, "combine");
         record(iter);
     }
-    (void)Pv;
-    (void)Hv;
     res.iterations = iter;
     res.theta = theta;
     if (ctx_->prof.on)

@@ -126,6 +126,10 @@ private:
     bool recur_ = false;
     double* pH_ = nullptr;      // H is an SpMM input (recurrence: A*H)
     DBuf<double> AX_, AP_, AH_;
+    // column-major blocks: H and P side by side in one buffer ([H | P], P after H's
+    // columns) so both are orthonormalized as one block (lobpcg); recurrence: [AH | AP]
+    double* pHP_ = nullptr;
+    DBuf<double> HP_, AHP_;
 
     DBuf<int32_t> ell_;  // fixed-slot ELL of A (meshes), see spmm_ell_kernel
     EllPatStore ellpat_; // its pattern-compressed form (ellpat.cu)

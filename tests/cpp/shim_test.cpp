@@ -55,6 +55,26 @@ int main() {
     if (whole.adjacency.nnz() != 10 || lcc.n() != 3 || lcc.adjacency.nnz() != 6 || old != std::vector<std::int64_t>{0, 1, 2})
         ++fails;
     if (classify(lcc).kind != Regularity::Regular || classify(lcc).max_degree != 2) ++fails;
+    // kernels.hpp: gram / mult / mult_sub on small exact integers (every product exact in fp64)
+    Dense X(5, 2), C(2, 3);
+    for (int i = 0; i < 5; ++i) { X(i, 0) = i + 1; X(i, 1) = 2 - i; }
+    for (int j = 0; j < 3; ++j) { C(0, j) = j - 1; C(1, j) = 2 * j + 1; }
+    Dense Y;
+    kernels::mult(X, C, Y);
+    Dense Z = Y;
+    kernels::mult_sub(Z, X, C);
+    Dense G = kernels::gram(X, Y);
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 3; ++j) {
+            if (Y(i, j) != X(i, 0) * C(0, j) + X(i, 1) * C(1, j)) ++fails;
+            if (Z(i, j) != 0.0) ++fails;
+        }
+    for (int a = 0; a < 2; ++a)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0;
+            for (int i = 0; i < 5; ++i) s += X(i, a) * Y(i, j);
+            if (G(a, j) != s) ++fails;
+        }
     std::printf("shim_test: cut %.0f, %d boundaries, %d failures\n", r.report.cutsize, boundaries, fails);
     return fails ? 1 : 0;
 }

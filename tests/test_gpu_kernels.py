@@ -292,3 +292,24 @@ MESHES = [("st7_40x12x10", gen.stencil3d(40, 12, 10, 7)), ("st27_34x8x6", gen.st
 def test_spmm_bit_exact_structured_mesh(ctx, ref, name, g, m):
     X = np.random.default_rng(m).uniform(-1, 1, (g.n, m))
     assert ctx.spmm("combinatorial", g, X).tobytes() == ref.spmm("combinatorial", g, X).tobytes()
+
+
+@pytest.mark.parametrize("n,k,m", [(1, 1, 1), (1000, 9, 9), (20001, 27, 9), (5000, 18, 4), (70001, 3, 3), (300, 40, 21)])
+def test_block_combine_matches_mult(ctx, ref, n, k, m):
+    """sp_block_combine vs kernels::mult / mult_sub (kernels.cpp:127-157)."""
+    rng = np.random.default_rng(n + k * 7 + m)
+    X, C, Y = rng.uniform(-1, 1, (n, k)), rng.uniform(-1, 1, (k, m)), rng.uniform(-1, 1, (n, m))
+    bound = np.abs(X) @ np.abs(C) * (k + 2) * np.finfo(float).eps
+    a = ctx.mult(X, C)
+    assert a.tobytes() == ctx.mult(X, C).tobytes()
+    assert np.all(np.abs(a - ref.mult(X, C)) <= bound)
+    b = ctx.mult(X, C, Y)
+    assert np.all(np.abs(b - ref.mult(X, C, Y)) <= bound + np.abs(Y) * np.finfo(float).eps)
+
+
+def test_block_combine_rejects_bad_shapes(ctx):
+    from paper_2105_00578_b200 import DimensionError
+    with pytest.raises(DimensionError):
+        ctx.mult(np.ones((4, 3)), np.ones((2, 2)))
+    with pytest.raises(DimensionError):
+        ctx.mult(np.ones((4, 65)), np.ones((65, 2)))
