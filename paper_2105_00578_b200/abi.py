@@ -6,6 +6,7 @@ The structs below are the C-ABI layout; keep them in lockstep with the header
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 SP_OK, SP_ERROR, SP_PARSE, SP_BREAKDOWN, SP_INFEASIBLE, SP_DEGENERATE, SP_DIMENSION, SP_INVALID, SP_CUDA, SP_NCCL = range(10)
@@ -157,7 +158,8 @@ SIGNATURES = {
     "sp_classify": (I32, [P, C.POINTER(SpGraph), C.POINTER(SpGraphInfo)]),
 }
 
-LIB_PATH = Path(__file__).resolve().parent / "libspecpart_b200.so"
+# SPECPART_B200_LIB: load another build of the library (A/B of two builds on one box)
+LIB_PATH = Path(os.environ.get("SPECPART_B200_LIB") or Path(__file__).resolve().parent / "libspecpart_b200.so")
 _lib = None
 
 
