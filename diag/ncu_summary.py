@@ -10,7 +10,9 @@ hdr, units = rows[0], rows[1]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "launch__registers_per_thread", "launch__grid_size", "lts__t_sector_hit_rate.pct"]
+        "launch__registers_per_thread", "launch__grid_size", "lts__t_sector_hit_rate.pct",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
 idx = {w: hdr.index(w) for w in want if w in hdr}
 stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warp_latency_issue_stalled") and h.endswith(".ratio")]
 if not stall:

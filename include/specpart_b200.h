@@ -184,6 +184,12 @@ sp_status sp_context_create_dist(int device, int rank, int world, const void* nc
 void sp_context_destroy(sp_context* ctx);
 const char* sp_last_error(const sp_context* ctx);
 int sp_version(void);
+/* Memory-safety check (debug): with SPECPART_B200_GUARD=1 in the environment of the
+ * process, every device buffer carries guard bands that are verified when it is
+ * released; this also verifies every live buffer now. *violations = bytes found
+ * overwritten so far (0 = clean), *buffers = buffers checked so far; both -1 when the
+ * process does not run in guard mode. */
+sp_status sp_debug_guard_check(int64_t* violations, int64_t* buffers);
 /* Record CUDA events around every SpMM launch (report.spmm_ms); off by default. */
 sp_status sp_context_set_timing(sp_context* ctx, int on);
 /* LOBPCG with the AX/AH/AP recurrence: one SpMM per iteration

@@ -422,7 +422,7 @@ class Context:
         """kernels::mult (Y = X C) or, given Y, kernels::mult_sub (returns Y - X C)."""
         Xc, Cc = _colmajor(X), _colmajor(C)
         if Xc.shape[1] != Cc.shape[0]:
-            raise DimensionError("mult: inner dimension mismatch")
+            raise abi.DimensionError("mult: inner dimension mismatch")
         out = np.empty((Xc.shape[0], Cc.shape[1]), dtype=np.float64, order="F")
         if Y is not None:
             out[...] = _colmajor(Y)

@@ -424,11 +424,13 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     // the initial block in the reference's vertex order (then permuted into the relabel)
     if (rl.on) X0b.alloc(solver.block_elems(d));
     const View X0 = rl.on ? solver.block(X0b.p, d) : X;
+    ctx->prof.mark(s, "initial_alloc");
     if (x0) upload_block(x0, n, g.row0, nloc, d, X0, s);
     else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X0, s);
     else initial_block_piecewise(n, d, g.row0, nloc, X0, s);
-    if (rl.on) permute_rows_in(rl, nloc, d, X0, X, s);
     ctx->prof.mark(s, "initial_block");
+    if (rl.on) permute_rows_in(rl, nloc, d, X0, X, s);
+    ctx->prof.mark(s, "initial_permute");
     SolveOpts so;
     so.nev = d;
     so.tol = R.tol;
@@ -668,6 +670,22 @@ void sp_context_destroy(sp_context* c) {
 }
 
 const char* sp_last_error(const sp_context* c) { return c ? c->err.c_str() : "null context"; }
+
+sp_status sp_debug_guard_check(int64_t* violations, int64_t* buffers) {
+    if (!violations || !buffers) return SP_INVALID;
+    if (!spb::guard_on()) {
+        *violations = *buffers = -1;
+        return SP_OK;
+    }
+    try {
+        long long checked = 0;
+        *violations = spb::guard_check_all(&checked);
+        *buffers = checked;
+        return SP_OK;
+    } catch (...) {
+        return SP_CUDA;
+    }
+}
 
 sp_status sp_context_set_timing(sp_context* c, int on) {
     if (!c) return SP_INVALID;

@@ -62,6 +62,16 @@ struct AllocStreamScope {
     ~AllocStreamScope() { alloc_stream() = prev; }
 };
 
+// Guard mode (SPECPART_B200_GUARD=1 in the environment, read once): every DBuf carries
+// 64 KiB guard bands before and after it, filled with a byte pattern and checked when
+// the buffer is released (and by sp_debug_guard_check), so an out-of-bounds store
+// into a neighbouring pool allocation — which raises no fault — is reported. The
+// memory-safety check this library uses on the B200 pool (guard.cu).
+bool guard_on();
+void* guard_alloc(size_t bytes, cudaStream_t s);
+void guard_free(void* p, cudaStream_t s);
+long long guard_check_all(long long* checked);  // bytes overwritten so far
+
 template <class T> struct DBuf {
     T* p = nullptr;
     size_t n = 0;
@@ -78,11 +88,15 @@ template <class T> struct DBuf {
     void alloc(size_t count) {
         if (count <= n && p) return;
         release();
-        if (count) SPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
+        if (count) {
+            if (guard_on()) p = static_cast<T*>(guard_alloc(count * sizeof(T), alloc_stream()));
+            else SPB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
+        }
         n = count;
     }
     void release() {
-        if (p) cudaFreeAsync(p, alloc_stream());
+        if (p && guard_on()) guard_free(p, alloc_stream());
+        else if (p) cudaFreeAsync(p, alloc_stream());
         p = nullptr;
         n = 0;
     }

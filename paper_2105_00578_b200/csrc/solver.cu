@@ -939,24 +939,31 @@ void initial_block_random(int64_t n, int d, uint64_t seed, int64_t row0, int64_t
     mt_uniform_block(seed, n, d, row0, nloc, X.sub(0, d), s);
 }
 
+// initial_guess_piecewise (eigensolver.cpp:35-51): column 0 all ones, column b+1 the
+// indicator of the b-th of d-1 consecutive row ranges (n/d rows, the first n%d one longer)
+__global__ void piecewise_kernel(int64_t n, int d, int64_t row0, int64_t nloc, View X) {
+    const int64_t base = n / d, rem = n % d;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < nloc * d;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(t % d);
+        const int64_t r = t / d, i = row0 + r;
+        double v = 1.0;
+        if (c > 0) {
+            const int64_t b = c - 1;
+            const int64_t start = b * base + (b < rem ? b : rem);
+            const int64_t len = base + (b < rem ? 1 : 0);
+            v = (i >= start && i < start + len) ? 1.0 : 0.0;
+        }
+        X.at(r, c) = v;
+    }
+}
+
 void initial_block_piecewise(int64_t n, int d, int64_t row0, int64_t nloc, const View& X, cudaStream_t s) {
     if (d > n) throw_infeasible("initial_guess_piecewise: d > n");
     if (d < 1) throw_infeasible("initial_guess_piecewise: d < 1");
-    std::vector<double> h(static_cast<size_t>(std::max<int64_t>(nloc, 1)) * d, 0.0);
-    const int64_t base = n / d, rem = n % d;
-    for (int64_t i = 0; i < nloc; ++i) h[i] = 1.0;
-    int64_t start = 0;
-    for (int b = 0; b + 1 < d; ++b) {
-        const int64_t len = base + (b < rem ? 1 : 0);
-        for (int64_t i = std::max(start, row0); i < std::min(start + len, row0 + nloc); ++i)
-            h[static_cast<size_t>(b + 1) * nloc + (i - row0)] = 1.0;
-        start += len;
-    }
     if (nloc <= 0) return;
-    DBuf<double> tmp(h.size());
-    SPB_CUDA(cudaMemcpyAsync(tmp.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, s));
-    copy_view(nloc, colmajor(tmp.p, nloc, d), X.sub(0, d), s);
-    SPB_CUDA(cudaStreamSynchronize(s));
+    piecewise_kernel<<<grid_for(nloc * d, 256, 8), 256, 0, s>>>(n, d, row0, nloc, X.sub(0, d));
+    SPB_LAUNCH_CHECK();
 }
 
 } // namespace spb
