@@ -30,7 +30,7 @@ def launches(path, out):
     tot = sum(a[1] for a in agg.values())
     with open(out, "w") as f:
         f.write(f"# ncu launch list — {path}\n\n")
-        f.write("Cold-cache, serialised device times of every kernel in one cfg2 partition "
+        f.write("Cold-cache, serialised device times of every kernel in one partition "
                 "(`ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                 "--clock-control none`). Compare shares, not absolutes.\n\n")
         f.write(f"Total kernel time {tot / 1e6:.2f} ms over {sum(a[0] for a in agg.values())} launches.\n\n")

@@ -13,7 +13,6 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
-#include <cstdlib>
 #include <vector>
 
 namespace spb {
@@ -22,82 +21,11 @@ namespace {
 
 constexpr int kVThreads = 256;
 
-template <int S, int MB, int MODE, int EPI>
-__global__ void __launch_bounds__(kVThreads) spmm_vec_kernel(const DevOp op, const View X, const EpiArgs ea,
-                                                             const int m, const int32_t* rows, const int64_t nrows,
-                                                             const int partial_base) {
-    const int lane = threadIdx.x & 31;
-    const int sub = lane & (S - 1);
-    const unsigned gmask = S == 32 ? 0xffffffffu : (((1u << S) - 1u) << (lane & ~(S - 1)));
-    const int64_t g0 = (blockIdx.x * static_cast<int64_t>(kVThreads) + threadIdx.x) / S;
-    const int64_t ng = static_cast<int64_t>(gridDim.x) * kVThreads / S;
-    double sq[EPI == EPI_RESIDUAL ? MB : 1];
-#pragma unroll
-    for (int c = 0; c < (EPI == EPI_RESIDUAL ? MB : 1); ++c) sq[c] = 0.0;
-    for (int64_t r = g0; r < nrows; r += ng) {
-        const int64_t row = rows[r];
-        const int64_t grow = op.row0 + row;
-        const int64_t k0 = op.offs[row], k1 = op.offs[row + 1];
-        double acc[MB];
-#pragma unroll
-        for (int c = 0; c < MB; ++c) acc[c] = 0.0;
-        double nisdi = 0.0;
-        if (MODE == OP_NORMAL_UNIT) nisdi = -op.isd[grow];
-        for (int64_t k = k0 + sub; k < k1; k += S) {
-            const int64_t j = op.cols[k];
-            double w;
-            if (MODE == OP_EXPLICIT) w = op.vals[k];
-            else if (MODE == OP_NORMAL_UNIT) w = nisdi * op.isd[j];
-            else w = -1.0;
-            const double* xr = X.ptr + j * X.rs;
-#pragma unroll
-            for (int c = 0; c < MB; ++c)
-                if (c < m) acc[c] = fma(w, __ldg(xr + c), acc[c]);
-        }
-#pragma unroll
-        for (int c = 0; c < MB; ++c) {
-            if (c >= m) break;
-#pragma unroll
-            for (int off = S / 2; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(gmask, acc[c], off, S);
-        }
-#pragma unroll
-        for (int c = 0; c < MB; ++c) {
-            if (c >= m) break;
-            if ((c & (S - 1)) != sub) continue;
-            const double xi = X.at(grow, c);
-            double v = acc[c];
-            if (MODE == OP_LAPLACE_UNIT) v = __dadd_rn(v, __dmul_rn(op.diag[row], xi));
-            if (MODE == OP_NORMAL_UNIT) v = __dadd_rn(v, xi);
-            double dummy = 0.0;
-            epilogue<EPI>(ea, row, c, v, xi, EPI == EPI_RESIDUAL ? sq[EPI == EPI_RESIDUAL ? c : 0] : dummy);
-        }
-    }
-    if (EPI == EPI_RESIDUAL) {
-        // per-CTA column sums in a fixed order: warp butterfly, then warps in order
-        __shared__ double s_sq[kVThreads / 32][MB];
-        const int warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int c = 0; c < MB; ++c) {
-            double v = sq[c];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            if (lane == 0) s_sq[warp][c] = v;
-        }
-        __syncthreads();
-        for (int c = threadIdx.x; c < m; c += kVThreads) {
-            double s = 0.0;
-            for (int w = 0; w < kVThreads / 32; ++w) s += s_sq[w][c];
-            ea.partial[static_cast<int64_t>(partial_base + blockIdx.x) * m + c] = s;
-        }
-    }
-}
-
 // Binned rows (all four bins by default), lanes over columns: R rows per warp,
 // L = 32 / R lanes per row, G = pow2(m) lanes per entry (lane = column),
 // E = L / G entries per instruction, U instructions in flight; the E slot sums
 // combine by a fixed butterfly (deterministic). Coalesced whole-row gathers: 1-2
-// L1 wavefronts per entry instead of one per column and entry
-// (SPB_VEC_COLS=0 restores the per-lane form).
+// L1 wavefronts per entry instead of one per column and entry.
 template <int G, int R, int MODE, int EPI>
 __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op, const View X, const EpiArgs ea,
                                                                  const int m, const int32_t* rows,
@@ -172,62 +100,15 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
     }
 }
 
-// Long rows (bin 4) in chunks of kChunk entries, one CTA per chunk: every thread
-// strides over the chunk's entries gathering whole X rows; the CTA combines its
-// 256 partial rows (warp butterfly, then warps in order) into one partial per
-// chunk. long_finish_kernel then adds each row's chunk partials in order, the
-// diagonal term and the epilogue (one warp per row, lane = column).
+// Long rows (bin 4) in chunks of kChunk entries, one CTA per chunk, lanes over columns:
+// G = pow2(m) lanes per entry (lane = column), E = 32 / G entries per warp instruction,
+// U instructions in flight per warp; one warp instruction gathers E whole X rows coalesced
+// (an m*8-byte row is 1-2 L1 wavefronts). Deterministic: entry k of the chunk goes to
+// slot (k - kb) mod (NW*E), the slots combine in slot order into one partial per chunk;
+// long_finish_kernel then adds each row's chunk partials in order, the diagonal term and
+// the epilogue (one warp per row, lane = column).
 constexpr int64_t kChunk = 4096;
 
-template <int MB, int MODE>
-__global__ void __launch_bounds__(kVThreads) long_chunk_kernel(const DevOp op, const View X, const int m,
-                                                               const int32_t* chunk_row, const int64_t* chunk_k0,
-                                                               double* chunk_part) {
-    const int64_t row = chunk_row[blockIdx.x];
-    const int64_t grow = op.row0 + row;
-    const int64_t kb = chunk_k0[blockIdx.x];
-    const int64_t ke = min(kb + kChunk, op.offs[row + 1]);
-    double acc[MB];
-#pragma unroll
-    for (int c = 0; c < MB; ++c) acc[c] = 0.0;
-    double nisdi = 0.0;
-    if (MODE == OP_NORMAL_UNIT) nisdi = -op.isd[grow];
-    for (int64_t k = kb + threadIdx.x; k < ke; k += kVThreads) {
-        const int64_t j = op.cols[k];
-        double w;
-        if (MODE == OP_EXPLICIT) w = op.vals[k];
-        else if (MODE == OP_NORMAL_UNIT) w = nisdi * op.isd[j];
-        else w = -1.0;
-        const double* xr = X.ptr + j * X.rs;
-#pragma unroll
-        for (int c = 0; c < MB; ++c)
-            if (c < m) acc[c] = fma(w, __ldg(xr + c), acc[c]);
-    }
-    __shared__ double red[kVThreads / 32][MB];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int c = 0; c < MB; ++c) {
-        if (c >= m) break;
-        double v = acc[c];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) red[warp][c] = v;
-    }
-    __syncthreads();
-    if (threadIdx.x < m) {
-        double v = 0.0;
-        for (int w = 0; w < kVThreads / 32; ++w) v += red[w][threadIdx.x];
-        chunk_part[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x] = v;
-    }
-}
-
-// Long rows, lanes over columns: G = pow2(m) lanes per entry (lane = column),
-// E = 32 / G entries per warp instruction, U instructions in flight per warp.
-// One warp instruction gathers E whole X rows coalesced (an m*8-byte row is 1-2
-// L1 wavefronts), where the thread-per-entry form above spends one wavefront
-// per thread and column — that form is L1-request bound on the long rows.
-// Deterministic: entry k of the chunk goes to slot (k - kb) mod (NW*E), the slots
-// combine in slot order.
 template <int G, int MODE>
 __global__ void __launch_bounds__(kVThreads) long_chunk_cols_kernel(const DevOp op, const View X, const int m,
                                                                     const int32_t* chunk_row,
@@ -348,47 +229,20 @@ __global__ void bin_keys_kernel(int64_t n, const int64_t* offs, int64_t long_thr
 template <int S, int MODE, int EPI>
 int launch_bin(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const int32_t* rows,
                int64_t nrows, int partial_base) {
-    static const bool cols_form = [] {
-        const char* e = std::getenv("SPB_VEC_COLS");
-        return !(e && e[0] == '0');
-    }();
-    if (S >= 16 && cols_form) {
-        const int grid = grid_for(nrows, kVThreads / 32, 8);
-        if (m <= 8) spmm_rowcols_kernel<8, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-        else if (m <= 16) spmm_rowcols_kernel<16, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-        else spmm_rowcols_kernel<32, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-        SPB_LAUNCH_CHECK();
-        return grid;
+    // rows of the S = 4 / 8 bins: several rows per warp (L = 8 or 16 lanes per row) when m fits
+    constexpr int RS = S == 4 ? 4 : (S == 8 ? 2 : 1);
+    int grid;
+    if (m <= 8) {
+        grid = grid_for(nrows, (kVThreads / 32) * RS, 8);
+        spmm_rowcols_kernel<8, RS, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+    } else if (m <= 16) {
+        constexpr int R16 = RS > 2 ? 2 : RS;
+        grid = grid_for(nrows, (kVThreads / 32) * R16, 8);
+        spmm_rowcols_kernel<16, R16, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
+    } else {
+        grid = grid_for(nrows, kVThreads / 32, 8);
+        spmm_rowcols_kernel<32, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
     }
-    static const bool cols_short = [] {
-        const char* e = std::getenv("SPB_VEC_COLS_SHORT");
-        return !(e && e[0] == '0');
-    }();
-    if (S < 16 && cols_form && cols_short) {
-        // short rows: several rows per warp, L = 8 (S = 4) or 16 (S = 8) lanes per row when m fits
-        constexpr int RS = S == 4 ? 4 : 2;
-        if (m <= 8) {
-            const int grid = grid_for(nrows, (kVThreads / 32) * RS, 8);
-            spmm_rowcols_kernel<8, RS, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-            SPB_LAUNCH_CHECK();
-            return grid;
-        } else if (m <= 16) {
-            const int grid = grid_for(nrows, (kVThreads / 32) * 2, 8);
-            spmm_rowcols_kernel<16, 2, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-            SPB_LAUNCH_CHECK();
-            return grid;
-        } else {
-            const int grid = grid_for(nrows, kVThreads / 32, 8);
-            spmm_rowcols_kernel<32, 1, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-            SPB_LAUNCH_CHECK();
-            return grid;
-        }
-    }
-    const int grid = grid_for(nrows, kVThreads / S, 8);
-    if (m <= 8) spmm_vec_kernel<S, 8, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-    else if (m <= 16) spmm_vec_kernel<S, 16, MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);
-    else spmm_vec_kernel<S, 32, MODE, (EPI == EPI_RESIDUAL ? EPI_STORE : EPI)>
-        <<<grid, kVThreads, 0, s>>>(op, X, ea, m, rows, nrows, partial_base);  // (RESIDUAL m > 16 excluded by the caller)
     SPB_LAUNCH_CHECK();
     return grid;
 }
@@ -415,17 +269,9 @@ template <int MODE, int EPI>
 int launch_long(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, int partial_base) {
     if (op.n_long <= 0) return 0;
     const int nch = static_cast<int>(op.long_nchunks);
-    static const bool cols_form = [] {
-        const char* e = std::getenv("SPB_LONG_COLS");
-        return !(e && e[0] == '0');
-    }();
-    if (cols_form) {
-        if (m <= 8) long_chunk_cols_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
-        else if (m <= 16) long_chunk_cols_kernel<16, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
-        else long_chunk_cols_kernel<32, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
-    } else if (m <= 8) long_chunk_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
-    else if (m <= 16) long_chunk_kernel<16, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
-    else long_chunk_kernel<32, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+    if (m <= 8) long_chunk_cols_kernel<8, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+    else if (m <= 16) long_chunk_cols_kernel<16, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
+    else long_chunk_cols_kernel<32, MODE><<<nch, kVThreads, 0, s>>>(op, X, m, op.long_chunk_row, op.long_chunk_k0, op.long_part);
     SPB_LAUNCH_CHECK();
     const int grid = ceil_div(op.n_long, kVThreads / 32);
     long_finish_kernel<MODE, EPI><<<grid, kVThreads, 0, s>>>(op, X, ea, m, op.long_row_chunk0, op.long_part, partial_base);
