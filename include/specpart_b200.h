@@ -168,6 +168,8 @@ typedef struct sp_report {
     int32_t pad1;
     int64_t amg_n[SP_MAX_AMG_LEVELS];
     int64_t amg_nnz[SP_MAX_AMG_LEVELS];
+    /* SpMM launches that ran the structured-mesh TMA stencil kernel (one GPU or z-slab) */
+    int64_t mesh_launches;
 } sp_report;
 
 typedef struct sp_context sp_context;

@@ -108,7 +108,8 @@ class SpReport(C.Structure):
                 ("trace_capacity", C.c_int32), ("trace_len", C.c_int32),
                 ("eigenvectors_out", C.POINTER(C.c_double)),
                 ("amg_levels", C.c_int32), ("pad1", C.c_int32),
-                ("amg_n", C.c_int64 * SP_MAX_AMG_LEVELS), ("amg_nnz", C.c_int64 * SP_MAX_AMG_LEVELS)]
+                ("amg_n", C.c_int64 * SP_MAX_AMG_LEVELS), ("amg_nnz", C.c_int64 * SP_MAX_AMG_LEVELS),
+                ("mesh_launches", C.c_int64)]
 
 
 class SpGraphInfo(C.Structure):

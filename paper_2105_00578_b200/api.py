@@ -217,7 +217,7 @@ def report_from_c(r: abi.SpReport, part_weights: np.ndarray, trace_buf=None) -> 
                "partition_s": r.partition_s, "total_s": r.total_s},
         cutsize=r.cutsize, imbalance=r.imbalance, part_weights=list(part_weights), trace=trace,
         amg_levels=[(int(r.amg_n[i]), int(r.amg_nnz[i])) for i in range(r.amg_levels)],
-        device={"spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
+        device={"mesh_launches": r.mesh_launches, "spmm_launches": r.spmm_launches, "spmm_bytes": r.spmm_bytes, "spmm_ms": r.spmm_ms,
                 "kernel_launches": r.kernel_launches, "n_gpus": r.n_gpus,
                 "poly_launches": r.poly_launches, "poly_bytes": r.poly_bytes, "poly_ms": r.poly_ms,
                 "halo_launches": r.halo_launches, "halo_bytes": r.halo_bytes, "halo_ms": r.halo_ms,

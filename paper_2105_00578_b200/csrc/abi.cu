@@ -382,6 +382,9 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     build_laplacian(operator_kind(R.problem), go, false, A, s);
     A.op.bound = ctx->comm.max_f64(A.op.bound, s);  // Gershgorin bound of the whole operator
     if (!kind.regular) build_row_bins(A.op, kLongRow, A.bins, s);  // length bins + long-row list
+    // multi-GPU: a structured mesh whose row blocks are whole z planes keeps the TMA
+    // stencil kernel (halo planes after the own rows); recognised on global ids
+    if (ctx->comm.active() && kind.regular && !no_mesh_kernel()) mesh_plan_slab(A.op, ctx->comm.n_global, s);
     localize_operator(ctx->comm, go, A, s);  // multi-GPU: halo numbering + exchange plan
     const double* bdiag = nullptr;
     if (R.problem == SP_PROBLEM_GENERALIZED) {
@@ -476,6 +479,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     ctx->collect_spmm_times();
     R.total_s = since(t_total);
     R.spmm_launches = ctx->timers.spmm_launches;
+    R.mesh_launches = ctx->timers.mesh_launches;
     R.spmm_bytes = ctx->timers.spmm_bytes;
     R.spmm_ms = ctx->timers.spmm_ms;
     R.poly_launches = ctx->timers.poly_launches;

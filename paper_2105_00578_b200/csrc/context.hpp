@@ -146,6 +146,7 @@ struct PhaseProf {
 struct Timers {
     double spmm_ms = 0.0;
     int64_t spmm_launches = 0;
+    int64_t mesh_launches = 0;
     double spmm_bytes = 0.0;
     int64_t kernel_launches = 0;
     double poly_ms = 0.0;

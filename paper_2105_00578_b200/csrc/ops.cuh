@@ -68,6 +68,11 @@ struct DevOp {
     // structured mesh (spmm_mesh.cu): row (z*ny + y)*nx + x has exactly the in-bounds
     // points of its 5/7/27-point stencil (mesh_plan); 0 = not recognised
     int mesh_nx = 0, mesh_ny = 0, mesh_nz = 0;
+    // multi-GPU z-slab of a structured mesh (mesh_plan_slab): the rank's rows are planes
+    // [mesh_z0, mesh_z0 + mesh_nz) of mesh_nzg; its neighbours' boundary planes sit in the
+    // halo rows of the input block at mesh_halo_lo / mesh_halo_hi (-1: no such neighbour)
+    int mesh_z0 = 0, mesh_nzg = 0, mesh_box27 = 0;
+    int64_t mesh_halo_lo = -1, mesh_halo_hi = -1;
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -116,8 +121,15 @@ bool build_ell_patterns(DevOp& op, EllPatStore& st, cudaStream_t s);
 // Structured-mesh SpMM (spmm_mesh.cu): mesh_plan recognises a naturally ordered
 // 5/7/27-point box mesh behind a pattern-compressed ELL (false: op unchanged).
 bool mesh_plan(DevOp& op, cudaStream_t s);
+bool no_mesh_kernel();  // SPB_MESH=0: A/B diagnostics (ELL kernels on meshes)
+// Multi-GPU: on the rank's rows before localization (global column ids), recognises a
+// 3-D box mesh whose row block is whole z planes (sets the mesh_* fields, false: unchanged).
+bool mesh_plan_slab(DevOp& op, int64_t n_global, cudaStream_t s);
 bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
-int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s);
+// hf: the copy-engine halo of a z-slab (nopush): the producer waits for the peers'
+// flags before it loads a halo plane
+int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s,
+                     const HaloFuse* hf = nullptr);
 // Row-length bins for the vector SpMM (spmm_vec.cu); also sets the long-row list.
 struct RowBins {
     DBuf<int32_t> rows;

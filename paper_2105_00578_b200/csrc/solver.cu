@@ -103,15 +103,30 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     ld_ = colmajor_ ? ((rows_cap_ + 63) / 64) * 64 : max_cols;
     // meshes: fixed-slot ELL, pattern-compressed when the rows share <= 256 slot
     // patterns (any stencil with KL = KU in {2, 3, 13}: 5-, 7- and 27-point)
+    const bool slab = halo_ && A_.mesh_nx > 0;  // mesh_plan_slab ran before localization
     if (colmajor_ && build_ell(A_, n_, ell_, s_)) {
         const int kk = A_.ell_kl * 100 + A_.ell_ku;
-        if ((kk == 202 || kk == 303 || kk == 1313) && build_ell_patterns(A_, ellpat_, s_) && !halo_) {
-            static const bool no_mesh = [] {  // A/B diagnostics only
-                const char* e = std::getenv("SPB_MESH");
-                return e && e[0] == '0';
-            }();
-            if (!no_mesh) mesh_plan(A_, s_);
+        if ((kk == 202 || kk == 303 || kk == 1313) && build_ell_patterns(A_, ellpat_, s_) && !halo_ &&
+            !no_mesh_kernel())
+            mesh_plan(A_, s_);
+    }
+    if (slab) {
+        // the halo plan numbers the foreign rows ascending: the plane below, then the plane above
+        const int64_t nxny = static_cast<int64_t>(A_.mesh_nx) * A_.mesh_ny;
+        const bool lo = A_.mesh_z0 > 0, hi = A_.mesh_z0 + A_.mesh_nz < A_.mesh_nzg;
+        const HaloPlan& hp = ctx->comm.halo;
+        const int r = ctx->comm.rank;
+        const bool plan_ok = colmajor_ && hp.nhalo == ((lo ? 1 : 0) + (hi ? 1 : 0)) * nxny &&
+                             (!lo || (r > 0 && hp.recv_cnt[r - 1] == nxny)) &&
+                             (!hi || (r + 1 < ctx->comm.world && hp.recv_cnt[r + 1] == nxny)) && hp.halo_base % 2 == 0;
+        if (plan_ok) {
+            A_.mesh_halo_lo = lo ? hp.halo_base : -1;
+            A_.mesh_halo_hi = hi ? hp.halo_base + (lo ? nxny : 0) : -1;
+        } else {
+            A_.mesh_nx = A_.mesh_ny = A_.mesh_nz = 0;
         }
+    } else if (halo_) {
+        A_.mesh_nx = A_.mesh_ny = A_.mesh_nz = 0;
     }
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
@@ -225,8 +240,10 @@ void Solver::spmm(const View& Xlocal, int m, EpiArgs& ea) {
     const double nrows = static_cast<double>(A_.n);
     const double csr_b = idx_b * static_cast<double>(A_.nnz) + 8.0 * (nrows + 1);
     double op_b = csr_b;
-    if (!fused && !halo_ && spmm_mesh_ok(A_, Xg, m, ea))
+    if ((!fused || hf.nopush) && spmm_mesh_ok(A_, Xg, m, ea)) {
         op_b = 0.0;  // structured mesh: the stencil is implicit, no index bytes (spmm_mesh.cu)
+        ctx_->timers.mesh_launches += 1;
+    }
     else if (A_.ell_pat)
         op_b = nrows + 4.0 * A_.ell_npat * (A_.ell_kl + A_.ell_ku) + 8.0 * A_.ell_npat;
     else if (A_.ell)

@@ -840,7 +840,8 @@ int launch_mode_epi(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStre
             grid = grid_for(ntiles, kThreads / 32, per_sm);
             kern<<<grid, kThreads, smem, s>>>(op, ta, ea, hf ? *hf : HaloFuse{});
         };
-        if (MODE == OP_LAPLACE_UNIT && !hf && spmm_mesh_ok(op, X, m, ea)) return spmm_mesh_launch(op, X, m, ea, s);
+        if (MODE == OP_LAPLACE_UNIT && (!hf || hf->nopush) && spmm_mesh_ok(op, X, m, ea))
+            return spmm_mesh_launch(op, X, m, ea, s, hf);
         if (MODE == OP_LAPLACE_UNIT && op.ell) {
             // fixed-slot ELL (meshes), pattern-compressed when the solver found the patterns
             const bool pat = op.ell_pat != nullptr;

@@ -51,6 +51,16 @@ struct MeshGeo {
     int nst;            // ring stages
     int h_stage;        // stages carry the H box (POLY with an H read)
     int stage;          // doubles per stage
+    // z-slab of a multi-GPU row block: global z of local plane 0, global planes, the
+    // halo map's plane of the neighbour below / above (-1: none, the TMA zero-fills
+    // and the stencil presence excludes them), chunk rotation (boundary chunks last)
+    int z0, nzg, hlo, hhi, zrot;
+    // copy-engine halo: the producer waits for these flags before its first halo plane
+    const uint64_t* flags;
+    unsigned long long epoch;
+    uint32_t recv_mask;
+    int world;
+    int* err;
 };
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
@@ -64,8 +74,9 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 
 template <bool BOX27, int EPI>
 __global__ void __launch_bounds__(kMeshThreads, 2)
-    spmm_mesh_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, const DevOp op,
-                     const EpiArgs ea, const int m, const MeshGeo geo) {
+    spmm_mesh_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+                     const __grid_constant__ CUtensorMap lmap, const DevOp op, const EpiArgs ea, const int m,
+                     const MeshGeo geo) {
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
     __shared__ double s_theta[kMaxCols];
@@ -94,7 +105,8 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         tx = static_cast<int>(r % geo.ntx);
         r /= geo.ntx;
         ty = static_cast<int>(r % geo.nty);
-        const int zq = static_cast<int>(r / geo.nty);
+        int zq = static_cast<int>(r / geo.nty);
+        if (geo.zrot) zq = zq + 1 == geo.nzc ? 0 : zq + 1;  // the slab's first chunk (lower halo) last
         z0 = zq * geo.zc;
         z1 = min(geo.nz, z0 + geo.zc);
     };
@@ -105,15 +117,33 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
             int s = 0;
             unsigned eph = 0;
             int64_t g = 0;  // stage sequence number
+            bool waited = geo.flags == nullptr;
             for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
                 int c, tx, ty, z0, z1;
                 decode(it, c, tx, ty, z0, z1);
                 // stage p carries X plane p and (POLY) the H box of output plane p - 1
                 for (int p = z0 - 1; p <= z1; ++p, ++g) {
+                    // planes past the slab: the neighbours' boundary planes (halo rows)
+                    const CUtensorMap* mp = &xmap;
+                    int pz = p;
+                    if (p < 0 && geo.hlo >= 0) {
+                        mp = &lmap;
+                        pz = geo.hlo;
+                    } else if (p >= geo.nz && geo.hhi >= 0) {
+                        mp = &lmap;
+                        pz = geo.hhi;
+                    }
+                    if (mp == &lmap && !waited) {
+                        // the peers' copy engines wrote these rows, then raised our flags
+                        for (int q = 0; q < geo.world; ++q)
+                            if ((geo.recv_mask >> q) & 1u) wait_flag(geo.flags + q, geo.epoch, geo.err);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic -> TMA reads
+                        waited = true;
+                    }
                     if (g >= geo.nst) mbar_wait(empty + s, eph);
                     double* st = smem + static_cast<size_t>(s) * geo.stage;
                     mbar_expect_tx(full + s, xbytes + hbytes);
-                    tma_load_4d(st, &xmap, tx * kTile - 2, ty * kTile - 1, p, c, full + s);
+                    tma_load_4d(st, mp, tx * kTile - 2, ty * kTile - 1, pz, c, full + s);
                     if (geo.h_stage) tma_load_4d(st + kXPlanePad, &hmap, tx * kTile, ty * kTile, p - 1, c, full + s);
                     if (++s == geo.nst) {
                         s = 0;
@@ -184,7 +214,8 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
             const double* p1 = smem + static_cast<size_t>(sc) * geo.stage;  // plane z
             const double* p2 = smem + static_cast<size_t>(sn) * geo.stage;  // plane z + 1
             const double* hs = p2 + kXPlanePad;
-            const bool zm = z > 0, zp = z + 1 < geo.nz;
+            const int zg = geo.z0 + z;  // global plane: stencil presence
+            const bool zm = zg > 0, zp = zg + 1 < geo.nzg;
             // the rows' entries in storage (= ascending column = lexicographic (dz, dy, dx))
             // order: acc -= x_j before the diagonal, += deg * x_i, -= x_j after it —
             // build_combinatorial's order, so each sum is bit-identical to spmv_block
@@ -308,27 +339,44 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// the block as a 4-D tensor (x, y, z, column) of doubles
-void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_x, int box_y) {
+// the block as a 4-D tensor (x, y, z, column) of doubles; planes from row `row_off`
+void make_map(CUtensorMap* map, const View& v, int m, const DevOp& op, int box_x, int box_y, int nz = 0,
+              int64_t row_off = 0) {
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(op.mesh_nx), static_cast<cuuint64_t>(op.mesh_ny),
-                                static_cast<cuuint64_t>(op.mesh_nz), static_cast<cuuint64_t>(m)};
+                                static_cast<cuuint64_t>(nz > 0 ? nz : op.mesh_nz), static_cast<cuuint64_t>(m)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(op.mesh_nx) * 8,
                                    static_cast<cuuint64_t>(op.mesh_nx) * op.mesh_ny * 8,
                                    static_cast<cuuint64_t>(m > 1 ? v.cs : (op.n + 1) & ~int64_t(1)) * 8};
     const cuuint32_t box[4] = {static_cast<cuuint32_t>(box_x), static_cast<cuuint32_t>(box_y), 1, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
-    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, v.ptr, dims, strides, box, es,
+    const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, v.ptr + row_off, dims, strides, box, es,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw SpError(8, "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
 }
 
 template <bool BOX27, int EPI>
-int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
+int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     MeshGeo geo{};
     geo.nx = op.mesh_nx;
     geo.ny = op.mesh_ny;
     geo.nz = op.mesh_nz;
+    geo.z0 = op.mesh_z0;
+    geo.nzg = op.mesh_nzg > 0 ? op.mesh_nzg : op.mesh_nz;
+    const int64_t nxny = static_cast<int64_t>(op.mesh_nx) * op.mesh_ny;
+    const bool lo = op.mesh_halo_lo >= 0, hi = op.mesh_halo_hi >= 0;
+    // one map over the halo planes: [below | above] as the halo plan numbers them
+    const int64_t hrow = lo ? op.mesh_halo_lo : op.mesh_halo_hi;
+    geo.hlo = lo ? 0 : -1;
+    geo.hhi = hi ? static_cast<int>((op.mesh_halo_hi - hrow) / nxny) : -1;
+    geo.zrot = (lo || hi) ? 1 : 0;
+    if (hf && hf->on) {
+        geo.flags = hf->my_flags;
+        geo.epoch = hf->epoch;
+        geo.recv_mask = hf->recv_mask;
+        geo.world = hf->world;
+        geo.err = hf->err;
+    }
     geo.ntx = (geo.nx + kTile - 1) / kTile;
     geo.nty = (geo.ny + kTile - 1) / kTile;
     geo.h_stage = (EPI == EPI_POLY && !ea.first && ea.h_terms) ? 1 : 0;
@@ -360,11 +408,13 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
     geo.nzc = (geo.nz + geo.zc - 1) / geo.zc;
     const int64_t items = per_chunk * geo.nzc;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, ctas)));
-    CUtensorMap xmap, hmap;
+    CUtensorMap xmap, hmap, lmap;
     make_map(&xmap, X, m, op, kHaloW, kHaloH);
     if (geo.h_stage) make_map(&hmap, ea.H, m, op, kTile, kTile);
     else hmap = xmap;
-    kern<<<grid, kMeshThreads, smem, s>>>(xmap, hmap, op, ea, m, geo);
+    if (lo || hi) make_map(&lmap, X, m, op, kHaloW, kHaloH, (lo ? 1 : 0) + (hi ? 1 : 0), hrow);
+    else lmap = xmap;
+    kern<<<grid, kMeshThreads, smem, s>>>(xmap, hmap, lmap, op, ea, m, geo);
     SPB_LAUNCH_CHECK();
     return grid;
 }
@@ -395,7 +445,42 @@ __global__ void mesh_verify_kernel(const DevOp op, int nx, int ny, int nz, int W
     }
 }
 
+// the rank's rows [row0, row0 + n) of the global mesh: every row's global columns are
+// exactly the in-bounds points of its stencil, ascending, no diagonal
+__global__ void mesh_verify_csr_kernel(const DevOp op, int nx, int ny, int nzg, bool box27, int* bad) {
+    const int64_t nxny = static_cast<int64_t>(nx) * ny;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < op.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t gi = op.row0 + i;
+        const int x = static_cast<int>(gi % nx), y = static_cast<int>((gi / nx) % ny), z = static_cast<int>(gi / nxny);
+        const int64_t k0 = op.offs[i], k1 = op.offs[i + 1];
+        bool ok = true;
+        int64_t prev = -1;
+        for (int64_t k = k0; k < k1 && ok; ++k) {
+            const int64_t j = op.cols[k];
+            const int64_t d = j - gi;
+            const int jx = static_cast<int>(j % nx), jy = static_cast<int>((j / nx) % ny),
+                      jz = static_cast<int>(j / nxny);
+            const int dx = jx - x, dy = jy - y, dz = jz - z;
+            ok = j > prev && d != 0 && j >= 0 && jz < nzg && dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 &&
+                 dz <= 1 && (box27 || (dx != 0) + (dy != 0) + (dz != 0) == 1);
+            prev = j;
+        }
+        const int cx = 1 + (x > 0) + (x + 1 < nx), cy = 1 + (y > 0) + (y + 1 < ny), cz = 1 + (z > 0) + (z + 1 < nzg);
+        const int want = box27 ? cx * cy * cz - 1 : (cx - 1) + (cy - 1) + (cz - 1);
+        if (!ok || k1 - k0 != want) atomicExch(bad, 1);
+    }
+}
+
 } // namespace
+
+bool no_mesh_kernel() {
+    static const bool off = [] {
+        const char* e = std::getenv("SPB_MESH");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
 
 bool mesh_plan(DevOp& op, cudaStream_t s) {
     op.mesh_nx = op.mesh_ny = op.mesh_nz = 0;
@@ -437,11 +522,69 @@ bool mesh_plan(DevOp& op, cudaStream_t s) {
     op.mesh_nx = static_cast<int>(nx);
     op.mesh_ny = static_cast<int>(ny);
     op.mesh_nz = static_cast<int>(nz);
+    op.mesh_z0 = 0;
+    op.mesh_nzg = static_cast<int>(nz);
+    op.mesh_box27 = box27 ? 1 : 0;
+    op.mesh_halo_lo = op.mesh_halo_hi = -1;
     return true;
 }
 
+bool mesh_plan_slab(DevOp& op, int64_t n_global, cudaStream_t s) {
+    op.mesh_nx = op.mesh_ny = op.mesh_nz = 0;
+    if (op.mode != OP_LAPLACE_UNIT || op.n <= 0 || op.max_row > 26 || op.n_long > 0 || !encode_fn()) return false;
+    // candidate geometry from the positive offsets of a few rows near the middle of the block
+    const int64_t cand[3] = {op.n / 2, op.n / 2 + 7, op.n / 3 + 13};
+    for (int64_t ci : cand) {
+        const int64_t i = std::min<int64_t>(std::max<int64_t>(ci, 0), op.n - 1);
+        int64_t k[2];
+        SPB_CUDA(cudaMemcpyAsync(k, op.offs + i, sizeof(k), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        const int len = static_cast<int>(k[1] - k[0]);
+        if (len <= 0 || len > 26) continue;
+        std::vector<int32_t> c(len);
+        SPB_CUDA(cudaMemcpyAsync(c.data(), op.cols + k[0], sizeof(int32_t) * len, cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> pos;
+        for (int32_t j : c)
+            if (j > op.row0 + i) pos.push_back(j - (op.row0 + i));
+        int64_t nx = 0, nxny = 0;
+        bool box27 = false;
+        if (pos.size() == 3 && pos[0] == 1) {
+            nx = pos[1];
+            nxny = pos[2];
+        } else if (pos.size() == 13 && pos[0] == 1) {
+            nx = pos[2];
+            nxny = pos[8];
+            box27 = true;
+        } else {
+            continue;
+        }
+        if (nx < 4 || nx % 2 || nxny % nx || n_global % nxny || op.row0 % nxny || op.n % nxny) continue;
+        const int64_t ny = nxny / nx, nzg = n_global / nxny;
+        if (ny > (1 << 30) || nzg > (1 << 30)) continue;
+        DBuf<int> bad(1);
+        SPB_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+        mesh_verify_csr_kernel<<<grid_for(op.n, 256, 8), 256, 0, s>>>(op, static_cast<int>(nx), static_cast<int>(ny),
+                                                                      static_cast<int>(nzg), box27, bad.p);
+        SPB_LAUNCH_CHECK();
+        int hb = 1;
+        SPB_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SPB_CUDA(cudaStreamSynchronize(s));
+        if (hb) continue;
+        op.mesh_nx = static_cast<int>(nx);
+        op.mesh_ny = static_cast<int>(ny);
+        op.mesh_nz = static_cast<int>(op.n / nxny);
+        op.mesh_z0 = static_cast<int>(op.row0 / nxny);
+        op.mesh_nzg = static_cast<int>(nzg);
+        op.mesh_box27 = box27 ? 1 : 0;
+        op.mesh_halo_lo = op.mesh_halo_hi = -1;  // set once the halo plan exists (Solver)
+        return true;
+    }
+    return false;
+}
+
 bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
-    if (op.mesh_nx <= 0 || !op.ell_pat || op.mode != OP_LAPLACE_UNIT || op.row0 != 0 || op.dpos || m > kMaxCols)
+    if (op.mesh_nx <= 0 || op.mode != OP_LAPLACE_UNIT || op.row0 != 0 || m > kMaxCols)
         return false;
     // column-major blocks, 16-byte aligned bases and column strides (TMA global address rules)
     auto ok = [&](const View& v) {
@@ -452,11 +595,11 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
     return true;
 }
 
-int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s) {
-    const bool box27 = op.ell_kl == 13;
+int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
+    const bool box27 = op.mesh_box27 != 0;
     switch (ea.mode) {
 #define SPB_MESH(EPI_)                                                                  \
-    return box27 ? launch_mesh<true, EPI_>(op, X, m, ea, s) : launch_mesh<false, EPI_>(op, X, m, ea, s);
+    return box27 ? launch_mesh<true, EPI_>(op, X, m, ea, s, hf) : launch_mesh<false, EPI_>(op, X, m, ea, s, hf);
     case EPI_STORE: SPB_MESH(EPI_STORE)
     case EPI_RESIDUAL: SPB_MESH(EPI_RESIDUAL)
     default: SPB_MESH(EPI_POLY)

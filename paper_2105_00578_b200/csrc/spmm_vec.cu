@@ -20,6 +20,9 @@ namespace spb {
 namespace {
 
 constexpr int kVThreads = 256;
+#ifndef SPB_VEC_U
+#define SPB_VEC_U 4
+#endif
 
 // Binned rows (all four bins by default), lanes over columns: R rows per warp,
 // L = 32 / R lanes per row, G = pow2(m) lanes per entry (lane = column),
@@ -33,7 +36,7 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
     constexpr int L = 32 / R;
     static_assert(L >= G, "a row group must hold one entry's columns");
     constexpr int E = L / G;
-    constexpr int U = 4;
+    constexpr int U = SPB_VEC_U;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / L, gl = lane % L;
     const int sub = gl / G, c = gl % G;
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
         double acc = 0.0;
         int64_t k = k0 + sub;
         for (; k + (U - 1) * E < k1; k += U * E) {
-            int64_t j[U];
+            int32_t j[U];
             double w[U], x[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) j[u] = op.cols[k + u * E];
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(kVThreads) spmm_rowcols_kernel(const DevOp op,
                 else w[u] = -1.0;
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + j[u] * X.rs + c) : 0.0;
+            for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + static_cast<int64_t>(j[u]) * X.rs + c) : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u) acc = fma(w[u], x[u], acc);
         }
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kVThreads) long_chunk_cols_kernel(const DevOp 
     constexpr int E = 32 / G;
     constexpr int NW = kVThreads / 32;
     constexpr int STRIDE = NW * E;
-    constexpr int U = 4;
+    constexpr int U = SPB_VEC_U;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane / G, c = lane % G;
     const int slot = warp * E + sub;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(kVThreads) long_chunk_cols_kernel(const DevOp 
     double acc = 0.0;
     int64_t k = kb + slot;
     for (; k + (U - 1) * STRIDE < ke; k += U * STRIDE) {
-        int64_t j[U];
+        int32_t j[U];
         double w[U], x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) j[u] = op.cols[k + u * STRIDE];
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kVThreads) long_chunk_cols_kernel(const DevOp 
             else w[u] = -1.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + j[u] * X.rs + c) : 0.0;
+        for (int u = 0; u < U; ++u) x[u] = act ? __ldg(X.ptr + static_cast<int64_t>(j[u]) * X.rs + c) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u) acc = fma(w[u], x[u], acc);
     }
