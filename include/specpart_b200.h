@@ -223,6 +223,7 @@ sp_status sp_partition(sp_context* ctx, const sp_graph* g, const sp_config* cfg,
  * optionally copying it to assignment_out (host, may be NULL). */
 typedef struct sp_device_graph sp_device_graph;
 sp_status sp_graph_upload(sp_context* ctx, const sp_graph* g, sp_device_graph** out);
+/* Releases a device graph; call it before sp_context_destroy of the context that made it. */
 void sp_graph_free(sp_device_graph* dg);
 sp_status sp_partition_resident(sp_context* ctx, sp_device_graph* dg, const sp_config* cfg,
                                 int32_t* assignment_out, sp_report* report, const double* x0_colmajor);

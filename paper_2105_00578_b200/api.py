@@ -16,6 +16,7 @@ ImportError — there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -268,6 +269,7 @@ class Context:
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         self.lib = abi.load_library()
         self._h = C.c_void_p()
+        self._graphs = weakref.WeakSet()  # device graphs: released before the context
         if world > 1:
             buf = C.create_string_buffer(nccl_id, 128)
             st = self.lib.sp_context_create_dist(device, rank, world, buf, C.byref(self._h))
@@ -285,6 +287,8 @@ class Context:
         return buf.raw
 
     def close(self):
+        for dg in list(getattr(self, "_graphs", ())):
+            dg.free()
         if self._h:
             self.lib.sp_context_destroy(self._h)
             self._h = C.c_void_p()
@@ -345,7 +349,9 @@ class Context:
         h = C.c_void_p()
         gc = g.as_c()
         self._check(self.lib.sp_graph_upload(self._h, C.byref(gc), C.byref(h)))
-        return DeviceGraph(self, h, g.n)
+        dg = DeviceGraph(self, h, g.n)
+        self._graphs.add(dg)
+        return dg
 
     def partition_resident(self, dg: "DeviceGraph", cfg: RunConfig, copy_assignment: bool = True,
                            x0=None, return_eigenvectors: bool = False) -> RunResult:
@@ -528,6 +534,7 @@ class Context:
         self._check(self.lib.sp_ingest(self._h, offs.shape[0] - 1, offs.ctypes.data, cols.ctypes.data,
                                        int(lcc), C.byref(h)))
         dg = DeviceGraph(self, h, 0, ingested=True)
+        self._graphs.add(dg)
         dg.n = dg.info().n
         return dg
 
