@@ -66,6 +66,13 @@ __global__ void make_keys_kernel(int64_t n, const uint32_t* ids, const int64_t* 
     }
 }
 
+// equal (segment, coordinate) side by side after the sort on those bits: a tie the ids must break
+__global__ void tie_kernel(int64_t n, const MjKey* keys, int* flag) {
+    for (int64_t p = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (keys[p].seg == keys[p - 1].seg && keys[p].coord == keys[p - 1].coord) *flag = 1;
+}
+
 __global__ void keys_to_ids_kernel(int64_t n, const MjKey* keys, uint32_t* ids) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -178,6 +185,8 @@ void mj_partition_dev(int64_t n, int dims, const View& coords, const double* wei
     DBuf<int> d_dims;
     DBuf<char> temp;
     size_t temp_bytes = 0;
+    DBuf<int> tie(1);
+    int level = 0;
 
     auto upload_ranges = [&](const std::vector<Range>& rs, bool with_dims) {
         std::vector<int64_t> st(rs.size());
@@ -203,17 +212,34 @@ void mj_partition_dev(int64_t n, int dims, const View& coords, const double* wei
         SPB_LAUNCH_CHECK();
         int seg_bits = 1;
         while ((int64_t(1) << seg_bits) < nseg) ++seg_bits;
+        // key bits: id 0-31, coordinate 32-95, segment from 96 (MjDecomposer). The stable
+        // sort on (segment, coordinate) alone already gives the (coordinate, id) order when
+        // no two points of a segment share a coordinate, or when the input is in id order
+        // (the first level): only a tie needs the 4 extra digit passes of the ids
         const int end_bit = 64 + 32 + seg_bits;
-        size_t need = 0;
-        SPB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, kin.p, kout.p, n, MjDecomposer{}, 0,
-                                                end_bit, s));
-        if (need > temp_bytes) {
-            temp.alloc(need);
-            temp_bytes = need;
+        auto sort_from = [&](int begin_bit) {
+            size_t need = 0;
+            SPB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, need, kin.p, kout.p, n, MjDecomposer{}, begin_bit,
+                                                    end_bit, s));
+            if (need > temp_bytes) {
+                temp.alloc(need);
+                temp_bytes = need;
+            }
+            SPB_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, need, kin.p, kout.p, n, MjDecomposer{}, begin_bit,
+                                                    end_bit, s));
+            launch_counter() += (end_bit - begin_bit + 7) / 8 + 2;  // CUB onesweep: histogram + one pass per digit
+        };
+        sort_from(32);
+        if (level > 0) {
+            SPB_CUDA(cudaMemsetAsync(tie.p, 0, sizeof(int), s));
+            tie_kernel<<<g1(n), 256, 0, s>>>(n, kout.p, tie.p);
+            SPB_LAUNCH_CHECK();
+            int h = 0;
+            SPB_CUDA(cudaMemcpyAsync(&h, tie.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            SPB_CUDA(cudaStreamSynchronize(s));
+            if (h) sort_from(0);
         }
-        SPB_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, need, kin.p, kout.p, n, MjDecomposer{}, 0,
-                                                end_bit, s));
-        launch_counter() += (end_bit + 7) / 8 + 2;  // CUB onesweep: histogram + one pass per digit
+        ++level;
         keys_to_ids_kernel<<<g1(n), 256, 0, s>>>(n, kout.p, ids.p);
         SPB_LAUNCH_CHECK();
 
