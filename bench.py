@@ -365,8 +365,9 @@ def main():
         keff = sum(r.report.device["poly_eff_bytes"] for r in r_res)
         kb = sum(r.report.device["poly_bytes"] for r in r_res)
         kms = sum(r.report.device["poly_ms"] for r in r_res)
-        kl, kname = poly_launches, ("SpMM fused with the GMRES-polynomial step (spmm_mesh_kernel: structured "
-                                    "mesh, TMA 3-D tiles, z-marching)")
+        kl, kname = poly_launches, ("SpMM fused with the GMRES-polynomial steps (structured mesh, TMA 3-D tiles, "
+                                    "z-marching: spmm_mesh_poly2_kernel, two steps per pass on 5/7-point meshes "
+                                    "on one GPU; spmm_mesh_kernel, one step, otherwise)")
     else:
         kb, kms, kl, kname = spmm_bytes, spmm_ms, spmm_launches, "spmm (CSR SpMM + fused epilogues)"
         keff = sum(r.report.device["spmm_eff_bytes"] for r in r_res)
@@ -390,7 +391,8 @@ def main():
                      "ms_per_launch": round(kms / max(kl, 1), 5),
                      "bytes_basis": ("the operator's own stored format: none for a recognised structured mesh "
                                      "(implicit stencil), 1 B/row for pattern ELL, 4 B/nnz + offsets for CSR; "
-                                     "X and Y once per launch, H read+write on the steps that update it"),
+                                     "X and Y once per launch, H read+write on the steps that update it; the "
+                                     "two-step kernel reads p_i and writes p_{i+2} and H, p_{i+1} stays on chip"),
                      "effective": {"basis": "same launches counted as pattern CSR (4 B/nnz + 8 B/row offsets)",
                                    "gbs": round(keff / (kms / 1e3) / 1e9, 1) if kms > 0 else 0.0,
                                    "bytes_per_launch": round(keff / max(kl, 1))},

@@ -95,6 +95,10 @@ struct EpiArgs {
     double inv_next = 0.0;
     int first = 0;
     int h_terms = 1;         // 0: H untouched, 1: H += inv_next*p_{i+1}, 2: also inv_cur*p_i first
+    // two steps in one pass (spmm_mesh_poly2_launch): p_{i+2} = p_{i+1} - inv_next * A p_{i+1};
+    // H = (first ? inv_cur*p_i : H + inv_cur*p_i) + inv_next*p_{i+1} (+ inv_after*p_{i+2} when last)
+    double inv_after = 0.0;
+    int last = 0;
 };
 
 // Y-block SpMM with epilogue. X is the gathered block (rows = global columns of
@@ -126,6 +130,11 @@ bool no_mesh_kernel();  // SPB_MESH=0: A/B diagnostics (ELL kernels on meshes)
 // 3-D box mesh whose row block is whole z planes (sets the mesh_* fields, false: unchanged).
 bool mesh_plan_slab(DevOp& op, int64_t n_global, cudaStream_t s);
 bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+// Two polynomial steps (i even, then i + 1) in one z-marching pass on a one-GPU 5/7-point
+// mesh: p_{i+1} stays in shared memory (computed on the tile plus a one-point ring), only
+// p_i is read and p_{i+2} written; same arithmetic, hence bit-identical to two steps.
+bool spmm_mesh_poly2_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
+int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s);
 // hf: the copy-engine halo of a z-slab (nopush): the producer waits for the peers'
 // flags before it loads a halo plane
 int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s,

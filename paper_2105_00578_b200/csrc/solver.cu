@@ -576,8 +576,9 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         return;
     }
     View cur = R.sub(0, k);
-    for (int i = 0; i + 1 < deg; ++i) {
-        const View nxt = block((i % 2 == 0) ? pPA_ : pPB_, k);
+    bool in_a = false;  // cur is pPA_
+    for (int i = 0; i + 1 < deg;) {
+        const View nxt = block(in_a ? pPB_ : pPA_, k);
         EpiArgs ea;
         ea.mode = EPI_POLY;
         ea.Y = nxt;
@@ -587,9 +588,42 @@ void Solver::apply_precond(const View& R, int k, const View& H) {
         ea.first = (i == 0);
         // H absorbs (p_i, p_{i+1}) on even steps, the trailing p_{deg-1} on a final odd step
         ea.h_terms = (i % 2 == 0) ? 2 : (i + 2 == deg ? 1 : 0);
-        spmm(cur, k, ea);
+        if (i % 2 == 0 && i + 2 < deg && spmm_mesh_poly2_ok(A_, cur, k, ea)) {
+            // steps i and i + 1 in one pass: p_{i+1} never leaves shared memory
+            ea.inv_after = 1.0 / roots_[i + 2];
+            ea.last = (i + 2 == deg - 1);
+            spmm_poly2(cur, k, ea);
+            i += 2;
+        } else {
+            spmm(cur, k, ea);
+            ++i;
+        }
         cur = nxt;
+        in_a = !in_a;
     }
+}
+
+// two fused polynomial steps (spmm_mesh.cu): timing and algorithmic bytes as for spmm()
+void Solver::spmm_poly2(const View& X, int m, EpiArgs& ea) {
+    const bool timed = ctx_->time_spmm;
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (timed) {
+        ev = ctx_->next_event_pair(1);
+        SPB_CUDA(cudaEventRecord(ev.first, s_));
+    }
+    spmm_mesh_poly2_launch(A_, X, m, ea, s_);
+    if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
+    // p_i read, p_{i+2} written, H read (unless first) and written; no index bytes
+    const double nrows = static_cast<double>(A_.n);
+    const double bytes = 8.0 * m * nrows * (ea.first ? 3.0 : 4.0);
+    const double idx_b = 4.0 * static_cast<double>(A_.nnz) + 8.0 * (nrows + 1);
+    ctx_->timers.spmm_launches += 1;
+    ctx_->timers.mesh_launches += 1;
+    ctx_->timers.poly_launches += 1;
+    ctx_->timers.spmm_bytes += bytes;
+    ctx_->timers.poly_bytes += bytes;
+    ctx_->timers.spmm_eff_bytes += bytes + idx_b;
+    ctx_->timers.poly_eff_bytes += bytes + idx_b;
 }
 
 void Solver::build_amg(CsrDev&& A0, DBuf<double>&& diag0, const AmgCfg& cfg) {

@@ -73,6 +73,7 @@ public:
     SolveResult lobpcg(const View& X0, const SolveOpts& o, const View& X);
 
     // Y = A X (local rows, X local block) — exposed for the kernel-level ABI.
+    void spmm_poly2(const View& X, int m, EpiArgs& ea);
     void spmm_store(const View& X, int m, const View& Y);
 
     // Block layout used by this solver: column-major (ld = padded rows) for

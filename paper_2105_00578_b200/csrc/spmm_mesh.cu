@@ -321,6 +321,187 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
     }
 }
 
+// ---- two polynomial steps per pass (5/7-point meshes, one GPU) ----
+// Step i: q = p_i - inv_cur * A p_i is computed on the tile plus a one-point ring (34 x 34)
+// into a 4-plane shared-memory ring; step i + 1: r = q - inv_next * A q on the 32 x 32 tile
+// of the plane behind it. X boxes are 36 x 36 (two-point ring). Only p_i is read, r (p_{i+2})
+// and H written: H = (first ? inv_cur p_i : H + inv_cur p_i) + inv_next q (+ inv_after r when
+// last) — the operations, and their order, of the two single steps (bit-identical).
+constexpr int kBox2 = kTile + 4;                   // 36
+constexpr int kXPlane2 = kBox2 * kBox2;            // 1296 doubles (10368 B, a multiple of 128 B)
+constexpr int kQW = kTile + 2;                     // 34
+constexpr int kQPlane = ((kQW * kQW + 15) / 16) * 16;  // 1168 doubles
+constexpr int kQPts = kQW * kQW;                   // 1156 points of q per plane
+
+__global__ void __launch_bounds__(kMeshThreads, 2)
+    spmm_mesh_poly2_kernel(const __grid_constant__ CUtensorMap xmap, const DevOp op, const EpiArgs ea, const int m,
+                           const MeshGeo geo) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    double* qring = smem + static_cast<size_t>(geo.nst) * kXPlane2;
+    if (tid == 0) {
+        for (int s = 0; s < geo.nst; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumers / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t items = static_cast<int64_t>(geo.ntx) * geo.nty * geo.nzc * m;
+    auto decode = [&](int64_t it, int& c, int& tx, int& ty, int& z0, int& z1) {
+        c = static_cast<int>(it % m);
+        int64_t r = it / m;
+        tx = static_cast<int>(r % geo.ntx);
+        r /= geo.ntx;
+        ty = static_cast<int>(r % geo.nty);
+        const int zq = static_cast<int>(r / geo.nty);
+        z0 = zq * geo.zc;
+        z1 = min(geo.nz, z0 + geo.zc);
+    };
+    if (warp == kConsumers / 32) {
+        if (lane == 0) {
+            int s = 0;
+            unsigned eph = 0;
+            int64_t g = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                int c, tx, ty, z0, z1;
+                decode(it, c, tx, ty, z0, z1);
+                for (int p = z0 - 2; p <= z1 + 1; ++p, ++g) {
+                    if (g >= geo.nst) mbar_wait(empty + s, eph);
+                    double* st = smem + static_cast<size_t>(s) * kXPlane2;
+                    mbar_expect_tx(full + s, kXPlane2 * 8u);
+                    tma_load_4d(st, &xmap, tx * kTile - 2, ty * kTile - 2, p, c, full + s);
+                    if (++s == geo.nst) {
+                        s = 0;
+                        if (g >= geo.nst) eph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    int qs = 0;
+    unsigned qph = 0;
+    auto advance = [&](int& sl, unsigned& ph) {
+        if (++sl == geo.nst) {
+            sl = 0;
+            ph ^= 1u;
+        }
+    };
+    auto release = [&](int sl) {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + sl)) : "memory");
+    };
+    auto cbar = [] { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); };
+    const int64_t nxny = static_cast<int64_t>(geo.nx) * geo.ny;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int c, tx, ty, z0, z1;
+        decode(it, c, tx, ty, z0, z1);
+        double* ycol = ea.Y.ptr + static_cast<int64_t>(c) * ea.Y.cs;
+        double* hcol = ea.H.ptr + static_cast<int64_t>(c) * ea.H.cs;
+        // X stages of planes zA - 1, zA, zA + 1 (zA = the plane step i computes next)
+        int sm = qs, sc = qs;
+        unsigned pm = qph, pc = qph;
+        advance(sc, pc);
+        mbar_wait(full + sm, pm);
+        mbar_wait(full + sc, pc);
+        cbar();  // the previous item's step-2 reads of the q ring are done
+        for (int zA = z0 - 1; zA <= z1; ++zA) {
+            int sn = sc;
+            unsigned pn = pc;
+            advance(sn, pn);
+            mbar_wait(full + sn, pn);
+            const double* x0p = smem + static_cast<size_t>(sm) * kXPlane2;  // plane zA - 1
+            const double* x1p = smem + static_cast<size_t>(sc) * kXPlane2;  // plane zA
+            const double* x2p = smem + static_cast<size_t>(sn) * kXPlane2;  // plane zA + 1
+            const int zB = zA - 1;
+            const bool doB = zB >= z0;
+            // H of the step-2 outputs, loaded before step 1 runs (latency hidden behind it)
+            double hv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int x = tx * kTile + lane, y = ty * kTile + warp + 8 * j;
+                hv[j] = (doB && !ea.first && x < geo.nx && y < geo.ny)
+                            ? hcol[static_cast<int64_t>(zB) * nxny + static_cast<int64_t>(y) * geo.nx + x]
+                            : 0.0;
+            }
+            // step i on plane zA, tile + one-point ring
+            {
+                double* q = qring + static_cast<size_t>((zA - z0 + 1) & 3) * kQPlane;
+                const int zg = geo.z0 + zA;
+                const bool zm = zg > 0, zp = zg + 1 < geo.nzg;
+                for (int p = tid; p < kQPts; p += kConsumers) {
+                    const int rr = p / kQW, cc = p - rr * kQW;
+                    const int x = tx * kTile - 1 + cc, y = ty * kTile - 1 + rr;
+                    const bool xm = x > 0, xp = x + 1 < geo.nx, ym = y > 0, yp = y + 1 < geo.ny;
+                    const int ctr = (rr + 1) * kBox2 + cc + 1;
+                    const double xi = x1p[ctr];
+                    double acc = 0.0;
+                    const int deg = zm + ym + xm + xp + yp + zp;
+                    if (zm) acc = __dsub_rn(acc, x0p[ctr]);
+                    if (ym) acc = __dsub_rn(acc, x1p[ctr - kBox2]);
+                    if (xm) acc = __dsub_rn(acc, x1p[ctr - 1]);
+                    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), xi));
+                    if (xp) acc = __dsub_rn(acc, x1p[ctr + 1]);
+                    if (yp) acc = __dsub_rn(acc, x1p[ctr + kBox2]);
+                    if (zp) acc = __dsub_rn(acc, x2p[ctr]);
+                    q[p] = __dsub_rn(xi, __dmul_rn(ea.inv_cur, acc));
+                }
+            }
+            cbar();
+            if (doB) {
+                // step i + 1 on plane zB = zA - 1 from q planes zB - 1, zB, zB + 1
+                const double* q0 = qring + static_cast<size_t>((zB - z0) & 3) * kQPlane;
+                const double* q1 = qring + static_cast<size_t>((zB - z0 + 1) & 3) * kQPlane;
+                const double* q2 = qring + static_cast<size_t>((zB - z0 + 2) & 3) * kQPlane;
+                const int zg = geo.z0 + zB;
+                const bool zm = zg > 0, zp = zg + 1 < geo.nzg;
+                const int x = tx * kTile + lane;
+                const bool xm = x > 0, xp = x + 1 < geo.nx;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int ly = warp + 8 * j;
+                    const int y = ty * kTile + ly;
+                    const bool ym = y > 0, yp = y + 1 < geo.ny;
+                    const int qc = (ly + 1) * kQW + lane + 1;
+                    const double qi = q1[qc];
+                    double acc = 0.0;
+                    const int deg = zm + ym + xm + xp + yp + zp;
+                    if (zm) acc = __dsub_rn(acc, q0[qc]);
+                    if (ym) acc = __dsub_rn(acc, q1[qc - kQW]);
+                    if (xm) acc = __dsub_rn(acc, q1[qc - 1]);
+                    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(deg), qi));
+                    if (xp) acc = __dsub_rn(acc, q1[qc + 1]);
+                    if (yp) acc = __dsub_rn(acc, q1[qc + kQW]);
+                    if (zp) acc = __dsub_rn(acc, q2[qc]);
+                    const double r = __dsub_rn(qi, __dmul_rn(ea.inv_next, acc));
+                    if (x < geo.nx && y < geo.ny) {
+                        const int64_t row = static_cast<int64_t>(zB) * nxny + static_cast<int64_t>(y) * geo.nx + x;
+                        ycol[row] = r;
+                        const double pi = x0p[(ly + 2) * kBox2 + lane + 2];  // p_i on plane zB
+                        double h = ea.first ? __dmul_rn(ea.inv_cur, pi) : __dadd_rn(hv[j], __dmul_rn(ea.inv_cur, pi));
+                        h = __dadd_rn(h, __dmul_rn(ea.inv_next, qi));
+                        if (ea.last) h = __dadd_rn(h, __dmul_rn(ea.inv_after, r));
+                        hcol[row] = h;
+                    }
+                }
+            }
+            release(sm);  // plane zA - 1: steps i (zA) and i + 1 (zA - 1) are done with it
+            sm = sc;
+            pm = pc;
+            sc = sn;
+            pc = pn;
+        }
+        release(sm);  // planes z1 and z1 + 1
+        release(sc);
+        qs = sc;
+        qph = pc;
+        advance(qs, qph);
+    }
+}
+
 // ---- tensor maps (driver entry point: the library links only the runtime) ----
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -387,13 +568,9 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
         SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    // ring: up to 6 stages, sized so `ctas` CTAs share an SM
-    static const int ring_ctas = [] {  // A/B diagnostics only
-        const char* e = std::getenv("SPB_MESH_CTAS");
-        return e ? std::max(2, std::atoi(e)) : 2;
-    }();
+    // ring: up to 6 stages within 100 KB, two CTAs per SM
     const size_t per_stage = sizeof(double) * geo.stage;
-    const size_t budget = ring_ctas >= 3 ? 72 * 1024 : 100 * 1024;
+    const size_t budget = 100 * 1024;
     geo.nst = static_cast<int>(std::min<size_t>(6, budget / per_stage));
     const size_t smem = per_stage * geo.nst;
     int per_sm = 0;
@@ -415,6 +592,43 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
     if (lo || hi) make_map(&lmap, X, m, op, kHaloW, kHaloH, (lo ? 1 : 0) + (hi ? 1 : 0), hrow);
     else lmap = xmap;
     kern<<<grid, kMeshThreads, smem, s>>>(xmap, hmap, lmap, op, ea, m, geo);
+    SPB_LAUNCH_CHECK();
+    return grid;
+}
+
+int launch_mesh_poly2(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
+    MeshGeo geo{};
+    geo.nx = op.mesh_nx;
+    geo.ny = op.mesh_ny;
+    geo.nz = op.mesh_nz;
+    geo.z0 = 0;
+    geo.nzg = op.mesh_nz;
+    geo.hlo = geo.hhi = -1;
+    geo.ntx = (geo.nx + kTile - 1) / kTile;
+    geo.nty = (geo.ny + kTile - 1) / kTile;
+    auto kern = spmm_mesh_poly2_kernel;
+    static bool attr = false;
+    if (!attr) {
+        SPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    // X ring + the 4-plane q ring, two CTAs per SM
+    const size_t qbytes = sizeof(double) * 4 * kQPlane;
+    geo.nst = static_cast<int>(std::min<size_t>(6, (108 * 1024 - qbytes) / (sizeof(double) * kXPlane2)));
+    const size_t smem = sizeof(double) * kXPlane2 * geo.nst + qbytes;
+    int per_sm = 0;
+    SPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kMeshThreads, smem));
+    const int ctas = device_sm_count() * std::max(per_sm, 1);
+    const int64_t per_chunk = static_cast<int64_t>(geo.ntx) * geo.nty * m;
+    int nzc = static_cast<int>(std::min<int64_t>(geo.nz, std::max<int64_t>(1, (4LL * ctas + per_chunk - 1) / per_chunk)));
+    nzc = std::min(nzc, std::max(1, geo.nz / 8));
+    geo.zc = (geo.nz + nzc - 1) / nzc;
+    geo.nzc = (geo.nz + geo.zc - 1) / geo.zc;
+    const int64_t items = per_chunk * geo.nzc;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, ctas)));
+    CUtensorMap xmap;
+    make_map(&xmap, X, m, op, kBox2, kBox2);
+    kern<<<grid, kMeshThreads, smem, s>>>(xmap, op, ea, m, geo);
     SPB_LAUNCH_CHECK();
     return grid;
 }
@@ -593,6 +807,17 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
     if (!ok(X) || ea.Y.rs != 1 || (ea.mode == EPI_POLY && ea.h_terms && ea.H.rs != 1)) return false;
     if (ea.mode == EPI_POLY && ea.h_terms && !ea.first && !ok(ea.H)) return false;
     return true;
+}
+
+bool spmm_mesh_poly2_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
+    if (!spmm_mesh_ok(op, X, m, ea) || op.mesh_box27 || ea.mode != EPI_POLY) return false;
+    // one GPU (no slab halo), H column-major
+    return op.mesh_halo_lo < 0 && op.mesh_halo_hi < 0 && op.mesh_z0 == 0 && op.mesh_nzg == op.mesh_nz &&
+           ea.H.rs == 1 && ea.Y.rs == 1;
+}
+
+int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
+    return launch_mesh_poly2(op, X, m, ea, s);
 }
 
 int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
