@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a,
     const int gid = lane >> 2, tig = lane & 3;
     const int TR = g.TR, SC = g.SC;
     const int u = a.u0 + a.u1;
-    const int inner = a.transform == TS_UPDATE ? u : a.kv;
+    const int inner = a.transform == TS_UPDATE ? u : (a.transform == TS_COMBINE_UV ? u + a.kv : a.kv);
     const int KBp = (inner + 3) / 4 * 4, NWp = (a.kw + 7) / 8 * 8;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // full[nst] then empty[nst]
     uint64_t* ebar = bar + g.nst;
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a,
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         int c = 0;
-        if ((a.transform == TS_UPDATE) || (a.gram && a.left_u)) {
+        if ((a.transform == TS_UPDATE) || (a.transform == TS_COMBINE_UV) || (a.gram && a.left_u)) {
             for (int j = 0; j < a.u0; ++j, ++c) { src[c] = a.U0.ptr + static_cast<int64_t>(j) * a.U0.cs; scol[c] = j; }
             for (int j = 0; j < a.u1; ++j, ++c) { src[c] = a.U1.ptr + static_cast<int64_t>(j) * a.U1.cs; scol[c] = a.u0 + j; }
         }
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(kBulkThreads, 2) ts_bulk_kernel(const TsDev a,
             }
         }
     }
-    const int a_col = a.transform == TS_UPDATE ? 0 : g.cV;
+    const int a_col = (a.transform == TS_UPDATE || a.transform == TS_COMBINE_UV) ? 0 : g.cV;
     const int w1 = a.W.cols;
     const int spw = TR / 64;  // strips per warp per tile (warp w: strips w, w+8, ...)
 
@@ -843,7 +843,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
     a.kv = s.V.cols;
     a.kw = 0;
     if (s.transform == TS_UPDATE) a.kw = a.kv;
-    if (s.transform == TS_COMBINE) a.kw = s.W.cols + (s.W2.ptr ? s.W2.cols : 0);
+    if (s.transform == TS_COMBINE || s.transform == TS_COMBINE_UV) a.kw = s.W.cols + (s.W2.ptr ? s.W2.cols : 0);
     a.gram = s.gram ? 1 : 0;
     a.left_u = s.gram_left_u ? 1 : 0;
     a.left_self = s.gram_left_self ? 1 : 0;
@@ -866,9 +866,9 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
         a.slices = 1;
     }
     const int u = a.u0 + a.u1;
-    const int inner = s.transform == TS_UPDATE ? u : a.kv;
+    const int inner = s.transform == TS_UPDATE ? u : (s.transform == TS_COMBINE_UV ? u + a.kv : a.kv);
     a.ldc = s.ldc > 0 ? s.ldc : inner;
-    const bool need_u = (s.transform == TS_UPDATE) || (s.gram && s.gram_left_u);
+    const bool need_u = (s.transform == TS_UPDATE) || (s.transform == TS_COMBINE_UV) || (s.gram && s.gram_left_u);
     const int LDT = ((need_u ? u : 0) + a.kv + a.kw + 1) | 1;
     size_t sm = sizeof(double) * (static_cast<size_t>(kStages) * kTR * LDT +
                                   (s.transform != TS_NONE ? static_cast<size_t>(inner) * a.kw : 0));
@@ -968,6 +968,7 @@ int ts_run(const TsSpec& s, double* gram_out, double* scratch, size_t scratch_el
             return a.P;
         }
     }
+    if (s.transform == TS_COMBINE_UV) throw SpError(1, "ts_run: combine over [U | V] needs aligned column-major operands");
     const bool mma_ok = (!a.gram || nblk <= kMaxItems * (kTsThreads / 32));
     if (mma_ok) {
         // reduction scratch: nitems x 64 doubles must fit in the staged smem

@@ -164,13 +164,14 @@ struct TsSpec {
     const double* C = nullptr;  // device, column-major
     int ldc = 0;                // leading dimension of C (0 = inner dimension)
     const double* b = nullptr;  // B diagonal (device) or null
-    int transform = 0;      // 0 none, 1 update, 2 combine
+    int transform = 0;      // 0 none, 1 update, 2 combine, 3 combine over [U | V]
     // gram request: left = [U0?][U1?][V or W?], right = V or W (post-transform)
     bool gram = false;
     bool gram_left_u = false;   // include U0, U1 on the left
     bool gram_left_self = true; // include the right block itself on the left
 };
-enum { TS_NONE = 0, TS_UPDATE = 1, TS_COMBINE = 2 };
+// TS_COMBINE_UV: W = [U0 | U1 | V] C (aligned column-major operands: the bulk kernel only)
+enum { TS_NONE = 0, TS_UPDATE = 1, TS_COMBINE = 2, TS_COMBINE_UV = 3 };
 
 // Runs the tile kernel; if spec.gram, writes the (P x Q) column-major Gram to
 // gram_out (device) and returns P. Deterministic for a fixed n. The last element

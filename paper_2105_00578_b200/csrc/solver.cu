@@ -338,7 +338,8 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
     std::vector<double> G0(static_cast<size_t>(P) * Q);
     std::vector<double> orig(k);
     View src = Vin;
-    std::vector<double> G2;
+    std::vector<double> G2, C1h;
+    bool fold2 = false;  // second CGS pass folded into the final combine (src = W1)
     if (a > 0) {
         // keep C0 = G0[0:a, :] on the device (leading dimension P)
         SPB_CUDA(cudaMemcpyAsync(cmat_.p, gram_.p, sizeof(double) * P * Q, cudaMemcpyDeviceToDevice, s_));
@@ -361,29 +362,61 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
             m1.W = Adst->sub(0, k);
             ts_mirror(m1);
         }
+        // column-major blocks: [against | W1]^T B W1 in the same pass, so the second pass can
+        // be folded into the final combine (fold2 below); otherwise C1 = against^T B W1 only
+        p1.gram_left_self = colmajor_;
         int P1, Q1;
-        gram_dev(p1, P1, Q1);  // a x k
-        SPB_CUDA(cudaMemcpyAsync(cmat2_.p, gram_.p, sizeof(double) * P1 * Q1, cudaMemcpyDeviceToDevice, s_));
-        // pass 2: W2 = W1 - A C1 (in place) ; G2 = W2^T B W2
-        TsSpec p2;
-        p2.U0 = against.sub(0, a);
-        p2.V = D;
-        p2.W = D;
-        p2.C = cmat2_.p;
-        p2.ldc = a;
-        p2.b = bdiag_;
-        p2.transform = TS_UPDATE;
-        p2.gram_left_u = false;
-        p2.gram_left_self = true;
-        if (mirror) {
-            TsSpec m2 = p2;  // A W2 = A W1 - (A against) C1
-            m2.U0 = Aagainst->sub(0, a);
-            m2.V = Adst->sub(0, k);
-            m2.W = Adst->sub(0, k);
-            ts_mirror(m2);
+        if (colmajor_) {
+            std::vector<double> G1 = gram_to_host(p1, P1, Q1);  // (a + k) x k
+            // W2 = W1 - against C1 has Gram W1^T B W1 - C1^T C1 (against^T B against = I). The
+            // second pass is folded when its correction is negligible against W1 (the usual
+            // case: |C1| ~ eps |W1|), which keeps that identity exact to rounding
+            C1h.assign(static_cast<size_t>(a) * k, 0.0);
+            G2.assign(static_cast<size_t>(k) * k, 0.0);
+            fold2 = true;
+            for (int j = 0; j < k; ++j) {
+                double c2 = 0.0;
+                for (int i = 0; i < a; ++i) {
+                    const double c = G1[static_cast<size_t>(j) * P1 + i];
+                    C1h[static_cast<size_t>(j) * a + i] = c;
+                    c2 += c * c;
+                }
+                if (!(c2 <= 1e-8 * G1[static_cast<size_t>(j) * P1 + a + j])) fold2 = false;
+            }
+            if (fold2) {
+                for (int j = 0; j < k; ++j)
+                    for (int i = 0; i < k; ++i) {
+                        double c = 0.0;
+                        for (int r = 0; r < a; ++r) c += C1h[static_cast<size_t>(i) * a + r] * C1h[static_cast<size_t>(j) * a + r];
+                        G2[static_cast<size_t>(j) * k + i] = G1[static_cast<size_t>(j) * P1 + a + i] - c;
+                    }
+            }
+        } else {
+            gram_dev(p1, P1, Q1);  // a x k
         }
-        int P2, Q2;
-        G2 = gram_to_host(p2, P2, Q2);
+        if (!fold2) {
+            SPB_CUDA(cudaMemcpyAsync(cmat2_.p, gram_.p, sizeof(double) * P1 * Q1, cudaMemcpyDeviceToDevice, s_));
+            // pass 2: W2 = W1 - A C1 (in place) ; G2 = W2^T B W2
+            TsSpec p2;
+            p2.U0 = against.sub(0, a);
+            p2.V = D;
+            p2.W = D;
+            p2.C = cmat2_.p;
+            p2.ldc = P1;
+            p2.b = bdiag_;
+            p2.transform = TS_UPDATE;
+            p2.gram_left_u = false;
+            p2.gram_left_self = true;
+            if (mirror) {
+                TsSpec m2 = p2;  // A W2 = A W1 - (A against) C1
+                m2.U0 = Aagainst->sub(0, a);
+                m2.V = Adst->sub(0, k);
+                m2.W = Adst->sub(0, k);
+                ts_mirror(m2);
+            }
+            int P2, Q2;
+            G2 = gram_to_host(p2, P2, Q2);
+        }
         src = D;
         for (int j = 0; j < k; ++j) orig[j] = std::sqrt(std::max(0.0, G0[static_cast<size_t>(j) * P + a + j]));
     } else {
@@ -450,20 +483,39 @@ Solver::Orth Solver::b_orth(const View& V, int k, const View& against, int a, co
     out.kept = static_cast<int>(T.size());
     if (out.kept == 0) return out;
 
-    // dst[:, 0:kept] = src * T  (+ Gram of the result)
-    std::vector<double> Th(static_cast<size_t>(k) * out.kept);
-    for (int c = 0; c < out.kept; ++c)
-        for (int r = 0; r < k; ++r) Th[static_cast<size_t>(c) * k + r] = T[c][r];
-    upload(Th, cmat_);
+    // dst[:, 0:kept] = src * T  (+ Gram of the result); folded second pass:
+    // dst = (W1 - against C1) T = [against | W1] [-C1 T ; T]
     TsSpec cb;
+    if (fold2) {
+        const int rows = a + k;
+        std::vector<double> Cuv(static_cast<size_t>(rows) * out.kept);
+        for (int c = 0; c < out.kept; ++c) {
+            for (int i = 0; i < a; ++i) {
+                double v = 0.0;
+                for (int r = 0; r < k; ++r) v += C1h[static_cast<size_t>(r) * a + i] * T[c][r];
+                Cuv[static_cast<size_t>(c) * rows + i] = -v;
+            }
+            for (int r = 0; r < k; ++r) Cuv[static_cast<size_t>(c) * rows + a + r] = T[c][r];
+        }
+        upload(Cuv, cmat_);
+        cb.U0 = against.sub(0, a);
+        cb.ldc = rows;
+        cb.transform = TS_COMBINE_UV;
+    } else {
+        std::vector<double> Th(static_cast<size_t>(k) * out.kept);
+        for (int c = 0; c < out.kept; ++c)
+            for (int r = 0; r < k; ++r) Th[static_cast<size_t>(c) * k + r] = T[c][r];
+        upload(Th, cmat_);
+        cb.transform = TS_COMBINE;
+    }
     cb.V = src;
     cb.W = dst.sub(0, out.kept);
     cb.C = cmat_.p;
     cb.b = bdiag_;
-    cb.transform = TS_COMBINE;
     cb.gram_left_self = true;
     if (mirror) {
-        TsSpec mc = cb;  // A dst = (A src) T
+        TsSpec mc = cb;  // A dst = (A src) T  (folded: [A against | A W1] [-C1 T ; T])
+        if (fold2) mc.U0 = Aagainst->sub(0, a);
         mc.V = a > 0 ? Adst->sub(0, k) : AV->sub(0, k);
         mc.W = Adst->sub(0, out.kept);
         ts_mirror(mc);
