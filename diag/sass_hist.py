@@ -13,7 +13,7 @@ import sys
 from pathlib import Path
 
 LIB = Path(__file__).resolve().parent.parent / "paper_2105_00578_b200" / "libspecpart_b200.so"
-FAMILIES = ["spmm_ell_kernel", "spmm_mesh_kernel", "spmm_col_kernel", "spmm_rowcols_kernel", "long_chunk_cols_kernel",
+FAMILIES = ["spmm_ell_kernel", "spmm_mesh_kernel", "spmm_mesh_poly2_kernel", "spmm_col_kernel", "spmm_rowcols_kernel", "long_chunk_cols_kernel",
             "spmm_group_kernel", "ts_bulk_kernel", "ts_mma_kernel", "mt_fill_kernel", "halo_push_kernel",
             "cheb_step_kernel", "spgemm_expand_kernel", "hook_kernel"]
 KEY = ["UTMALDG", "UBLKCP", "SYNCS", "DMMA", "LDG", "STG", "LDS", "STS", "DADD", "DMUL", "DFMA", "SHFL", "BAR"]
