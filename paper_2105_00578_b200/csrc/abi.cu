@@ -400,6 +400,34 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     const auto t_eig = Clock::now();
     Solver solver(ctx, A.op, bdiag, d);
     solver.set_recurrence(ctx->recurrence);
+    const int64_t nloc = g.n_local;
+    DBuf<double> Xb, X0b;
+    const View X = solver.block(solver.input_block(d, Xb), d);
+    // the initial block in the reference's vertex order (then permuted into the relabel);
+    // random draws run on the side stream, overlapping the preconditioner build
+    if (rl.on) X0b.alloc(solver.block_elems(d));
+    const View X0 = rl.on ? solver.block(X0b.p, d) : X;
+    const bool side_rng = !x0 && R.init == SP_INIT_RANDOM;
+    // however this scope ends, s waits for the side stream before the blocks are released
+    struct AuxJoin {
+        sp_context* c;
+        bool on;
+        ~AuxJoin() {
+            if (on) cudaStreamWaitEvent(c->stream, c->aux_done, 0);
+        }
+    } aux_join{ctx, false};
+    if (side_rng) {
+        if (!ctx->aux) {
+            SPB_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+            SPB_CUDA(cudaEventCreateWithFlags(&ctx->aux_ready, cudaEventDisableTiming));
+            SPB_CUDA(cudaEventCreateWithFlags(&ctx->aux_done, cudaEventDisableTiming));
+        }
+        SPB_CUDA(cudaEventRecord(ctx->aux_ready, s));
+        SPB_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->aux_ready, 0));
+        initial_block_random(n, d, cfg->seed, g.row0, nloc, X0, ctx->aux);
+        SPB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux));
+        aux_join.on = true;
+    }
     DBuf<double> inv;
     if (R.precond == SP_PRECOND_JACOBI) {
         inverse_diagonal(A, inv, s);
@@ -421,15 +449,8 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
         solver.set_none();
     }
     ctx->prof.mark(s, "precond_build");
-    const int64_t nloc = g.n_local;
-    DBuf<double> Xb, X0b;
-    const View X = solver.block(solver.input_block(d, Xb), d);
-    // the initial block in the reference's vertex order (then permuted into the relabel)
-    if (rl.on) X0b.alloc(solver.block_elems(d));
-    const View X0 = rl.on ? solver.block(X0b.p, d) : X;
-    ctx->prof.mark(s, "initial_alloc");
     if (x0) upload_block(x0, n, g.row0, nloc, d, X0, s);
-    else if (R.init == SP_INIT_RANDOM) initial_block_random(n, d, cfg->seed, g.row0, nloc, X0, s);
+    else if (side_rng) SPB_CUDA(cudaStreamWaitEvent(s, ctx->aux_done, 0));
     else initial_block_piecewise(n, d, g.row0, nloc, X0, s);
     ctx->prof.mark(s, "initial_block");
     if (rl.on) permute_rows_in(rl, nloc, d, X0, X, s);
@@ -669,6 +690,12 @@ void sp_context_destroy(sp_context* c) {
     if (c->comm.nccl) nccl().CommDestroy(c->comm.nccl);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->aux) {
+        cudaStreamSynchronize(c->aux);
+        cudaEventDestroy(c->aux_ready);
+        cudaEventDestroy(c->aux_done);
+        cudaStreamDestroy(c->aux);
+    }
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

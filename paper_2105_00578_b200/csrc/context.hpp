@@ -193,6 +193,10 @@ struct sp_context {
     bool recurrence = false;  // LOBPCG AX/AH/AP recurrence (Solver::set_recurrence)
     bool relabel = true;      // irregular graphs: degree-descending relabel (relabel.cu)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // side stream: the initial block's mt19937_64 draws run there while the
+    // preconditioner is built (partition_core)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t aux_ready = nullptr, aux_done = nullptr;
     // event pairs recorded around SpMM launches; resolved without extra syncs
     // once the pipeline has synchronized (collect_spmm_times)
     std::vector<cudaEvent_t> evpool;

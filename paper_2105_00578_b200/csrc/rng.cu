@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(kThreads, 1) mt_fill_kernel(const FillArgs a) 
     // twist/temper: after each twist W[i] = y_{t+312+i} = draw (kJ + q0 + i)
     const int64_t o_begin = k * kChunk;
     const int64_t o_end = min(a.total, o_begin + kChunk);
+    // (column, row) of this thread's draw, advanced by NN draws per round without a division
+    int64_t oj = (o_begin + tid) / a.n, oi = (o_begin + tid) - oj * a.n;
     for (int64_t q0 = o_begin; q0 < o_end; q0 += NN) {
         uint64_t v = 0;
         if (tid < MM) v = next_word(Y[tid], Y[tid + 1], Y[tid + MM]);
@@ -96,13 +98,15 @@ __global__ void __launch_bounds__(kThreads, 1) mt_fill_kernel(const FillArgs a) 
         __syncthreads();
         if (tid < NN) {
             const int64_t o = q0 + tid;
-            if (o < o_end) {
-                const int64_t j = o / a.n, i = o - j * a.n;
-                if (i >= a.row0 && i < a.row0 + a.nloc) {
-                    const uint64_t r = temper(Y[tid]);
-                    const double u = __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
-                    a.out.at(i - a.row0, static_cast<int>(j)) = __dsub_rn(__dmul_rn(2.0, u), 1.0);
-                }
+            if (o < o_end && oi >= a.row0 && oi < a.row0 + a.nloc) {
+                const uint64_t r = temper(Y[tid]);
+                const double u = __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
+                a.out.at(oi - a.row0, static_cast<int>(oj)) = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+            }
+            oi += NN;
+            while (oi >= a.n) {
+                oi -= a.n;
+                ++oj;
             }
         }
     }
@@ -149,6 +153,7 @@ void mt_uniform_block(uint64_t seed, int64_t n, int d, int64_t row0, int64_t nlo
     std::sort(chunks.begin(), chunks.end());
     chunks.erase(std::unique(chunks.begin(), chunks.end()), chunks.end());
     Tables& t = tables();
+    AllocStreamScope scope(s);  // the chunk list lives and dies on s (which may be a side stream)
     DBuf<int64_t> dch(chunks.size());
     SPB_CUDA(cudaMemcpyAsync(dch.p, chunks.data(), sizeof(int64_t) * chunks.size(), cudaMemcpyHostToDevice, s));
     FillArgs a{seed, total, n, row0, nloc, out, dch.p, t.off.p, t.exps.p};
@@ -158,7 +163,6 @@ void mt_uniform_block(uint64_t seed, int64_t n, int d, int64_t row0, int64_t nlo
     SPB_CUDA(cudaFuncSetAttribute(mt_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     mt_fill_kernel<<<static_cast<int>(chunks.size()), kThreads, smem, s>>>(a);
     SPB_LAUNCH_CHECK();
-    SPB_CUDA(cudaStreamSynchronize(s));  // dch is freed on return
-}
+}  // dch: stream-ordered free on s
 
 } // namespace spb
