@@ -145,6 +145,317 @@ void build_plan(MjPlanNode& node, int64_t target, int dim, int remaining) {
     for (int64_t s = 0; s < m; ++s) build_plan(node.kids[s], base + (s < rem ? 1 : 0), dim + 1, remaining - 1);
 }
 
+// ---- unit weights: radix select instead of sorting ----
+// Points never move: seg[v] is the tree node of vertex v at the current level. A node
+// with m kids cuts its points, in (coordinate, id) order, at m - 1 ranks that follow in
+// closed form from the sizes (partitioner.cpp:100-132 with unit weights), so the level
+// only needs the m - 1 keys at those ranks (queries) and one labelling pass: a point's
+// kid is the number of cut keys <= its own key. The keys are found by radix select over
+// the 96-bit composite (orderable coordinate, id), 8 bits per pass: histogram passes over
+// every point until each query's bucket holds at most kCandMax points, then those
+// candidates are gathered and one CTA per query finishes the select in shared memory.
+constexpr int kCandMax = 4096;
+
+struct SelState {
+    unsigned long long hi;   // processed bits of the coordinate key (left-aligned value prefix)
+    unsigned int lo;         // processed bits of the id (after all 64 coordinate bits)
+    long long rank;          // rank within the bucket still to resolve
+    long long cnt;           // points in the current bucket (-1: the rank is past the node's points)
+    int bits;                // bits of the composite key the prefix covers
+    int pad;
+};
+
+__device__ __forceinline__ unsigned digit_of(uint64_t key, uint32_t id, int bits) {
+    return bits < 64 ? static_cast<unsigned>((key >> (56 - bits)) & 255u)
+                     : static_cast<unsigned>((id >> (24 - (bits - 64))) & 255u);
+}
+__device__ __forceinline__ bool prefix_match(uint64_t key, uint32_t id, int bits, const SelState& q) {
+    if (bits == 0) return true;
+    if (bits <= 64) return (key >> (64 - bits)) == q.hi;
+    return key == q.hi && (id >> (32 - (bits - 64))) == q.lo;
+}
+
+// histogram of the next digit of every point matching a query's prefix (privatized in
+// shared memory when the level's histograms fit, else straight to global memory)
+template <bool SMEM>
+__global__ void sel_hist_kernel(int64_t n, const int32_t* seg, View coords, const int* seg_q0, const int* seg_dim,
+                                const SelState* qs, int nq, int bits, unsigned* hist) {
+    extern __shared__ unsigned sh_dyn[];
+    unsigned* sh = SMEM ? sh_dyn : hist;
+    if (SMEM) {
+        for (int i = threadIdx.x; i < nq * 256; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+    }
+    for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int sgi = seg[v];
+        const int q0 = seg_q0[sgi], q1 = seg_q0[sgi + 1];
+        if (q0 == q1) continue;
+        const uint64_t key = orderable(coords.at(v, seg_dim[sgi]));
+        const uint32_t id = static_cast<uint32_t>(v);
+        const unsigned d = digit_of(key, id, bits);
+        for (int q = q0; q < q1; ++q)
+            if (qs[q].cnt > kCandMax && prefix_match(key, id, bits, qs[q])) atomicAdd(&sh[q * 256 + d], 1u);
+    }
+    if (!SMEM) return;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nq * 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// one block of 256 threads per query: pick the bucket holding the query's rank
+__global__ void sel_pick_kernel(SelState* qs, int bits, unsigned* hist) {
+    __shared__ unsigned long long cum[256];
+    const int q = blockIdx.x, t = threadIdx.x;
+    SelState st = qs[q];
+    if (st.cnt <= kCandMax) return;  // small enough for the candidate stage
+    const unsigned h = hist[q * 256 + t];
+    cum[t] = h;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {
+        const unsigned long long v = t >= off ? cum[t - off] : 0ull;
+        __syncthreads();
+        cum[t] += v;
+        __syncthreads();
+    }
+    const unsigned long long below = cum[t] - h;
+    if (static_cast<unsigned long long>(st.rank) >= below && static_cast<unsigned long long>(st.rank) < cum[t]) {
+        if (bits < 64) st.hi = (st.hi << 8) | t;
+        else st.lo = (st.lo << 8) | t;
+        st.rank -= static_cast<long long>(below);
+        st.cnt = h;
+        st.bits = bits + 8;
+        qs[q] = st;
+    }
+    hist[q * 256 + t] = 0;  // ready for the next pass
+}
+
+struct Cand {
+    uint64_t key;
+    uint32_t id;
+};
+
+// candidates: the points in each query's final bucket (at most kCandMax per query)
+__global__ void sel_collect_kernel(int64_t n, const int32_t* seg, View coords, const int* seg_q0, const int* seg_dim,
+                                   const SelState* qs, unsigned* fill, Cand* cand) {
+    for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int sgi = seg[v];
+        const int q0 = seg_q0[sgi], q1 = seg_q0[sgi + 1];
+        if (q0 == q1) continue;
+        const uint64_t key = orderable(coords.at(v, seg_dim[sgi]));
+        const uint32_t id = static_cast<uint32_t>(v);
+        for (int q = q0; q < q1; ++q)
+            if (qs[q].cnt >= 0 && prefix_match(key, id, qs[q].bits, qs[q])) {
+                const unsigned slot = atomicAdd(&fill[q], 1u);
+                if (slot < kCandMax) cand[static_cast<int64_t>(q) * kCandMax + slot] = Cand{key, id};
+            }
+    }
+}
+
+// one block per query: radix select of the remaining bits among the candidates -> cut key
+__global__ void sel_finish_kernel(const SelState* qs, const unsigned* fill, const Cand* cand,
+                                  unsigned long long* cut_key, unsigned* cut_id, int* cut_inf) {
+    __shared__ unsigned hist[256];
+    __shared__ unsigned long long cum[256];
+    __shared__ unsigned long long s_hi;
+    __shared__ unsigned s_lo;
+    __shared__ long long s_rank;
+    const int q = blockIdx.x, t = threadIdx.x;
+    const SelState st = qs[q];
+    if (st.cnt < 0) {  // rank past the node's points: no point reaches this cut
+        if (t == 0) cut_inf[q] = 1;
+        return;
+    }
+    const int c = static_cast<int>(min(fill[q], static_cast<unsigned>(kCandMax)));
+    const Cand* cq = cand + static_cast<int64_t>(q) * kCandMax;
+    if (t == 0) {
+        s_hi = st.hi;
+        s_lo = st.lo;
+        s_rank = st.rank;
+    }
+    __syncthreads();
+    for (int bits = st.bits; bits < 96; bits += 8) {
+        hist[t] = 0;
+        __syncthreads();
+        SelState cur{s_hi, s_lo, 0, 0, bits, 0};
+        for (int i = t; i < c; i += blockDim.x)
+            if (prefix_match(cq[i].key, cq[i].id, bits, cur)) atomicAdd(&hist[digit_of(cq[i].key, cq[i].id, bits)], 1u);
+        __syncthreads();
+        cum[t] = hist[t];
+        __syncthreads();
+        for (int off = 1; off < 256; off <<= 1) {
+            const unsigned long long v = t >= off ? cum[t - off] : 0ull;
+            __syncthreads();
+            cum[t] += v;
+            __syncthreads();
+        }
+        const unsigned long long below = cum[t] - hist[t];
+        const long long r = s_rank;
+        __syncthreads();
+        if (static_cast<unsigned long long>(r) >= below && static_cast<unsigned long long>(r) < cum[t]) {
+            if (bits < 64) s_hi = (s_hi << 8) | t;
+            else s_lo = (s_lo << 8) | t;
+            s_rank = r - static_cast<long long>(below);
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        cut_key[q] = s_hi;
+        cut_id[q] = s_lo;
+        cut_inf[q] = 0;
+    }
+}
+
+// kid = number of the node's cut keys <= the point's key; new node = first kid's index + kid
+__global__ void sel_label_kernel(int64_t n, int32_t* seg, View coords, const int* seg_q0, const int* seg_dim,
+                                 const int* seg_base, const unsigned long long* cut_key, const unsigned* cut_id,
+                                 const int* cut_inf) {
+    for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+         v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int sgi = seg[v];
+        const int q0 = seg_q0[sgi], q1 = seg_q0[sgi + 1];
+        int kid = 0;
+        if (q0 != q1) {
+            const uint64_t key = orderable(coords.at(v, seg_dim[sgi]));
+            const uint32_t id = static_cast<uint32_t>(v);
+            for (int q = q0; q < q1; ++q)
+                if (!cut_inf[q] && (key > cut_key[q] || (key == cut_key[q] && id >= cut_id[q]))) ++kid;
+        }
+        seg[v] = seg_base[sgi] + kid;
+    }
+}
+
+// child sizes of a unit-weight node (partitioner.cpp:100-132 in closed form)
+std::vector<int64_t> unit_takes(const MjPlanNode& node, int64_t size) {
+    const int64_t L = node.leaves;
+    const double W = static_cast<double>(size);
+    int64_t pos = 0, leaves_done = 0;
+    const size_t nc = node.kids.size();
+    std::vector<int64_t> takes(nc);
+    for (size_t c = 0; c < nc; ++c) {
+        const int64_t cl = node.kids[c].leaf_count();
+        leaves_done += cl;
+        int64_t take;
+        if (c + 1 == nc) {
+            take = size - pos;
+        } else {
+            const double target = W * static_cast<double>(leaves_done) / static_cast<double>(L);
+            const int64_t max_take = size - pos - (L - leaves_done);
+            const int64_t t_target = std::max<int64_t>(0, static_cast<int64_t>(std::ceil(target)) - pos);
+            take = std::max(cl, t_target);
+            take = std::min(take, max_take);
+            take = std::min(take, size - pos);
+            take = std::max<int64_t>(take, 0);
+        }
+        takes[c] = take;
+        pos += take;
+    }
+    return takes;
+}
+
+void mj_select_unit(int64_t n, int dims, const View& coords, const MjPlanNode& plan, int32_t* assignment,
+                    cudaStream_t s) {
+    struct Node {
+        const MjPlanNode* node;
+        int64_t size;
+    };
+    std::vector<Node> nodes{{&plan, n}};
+    SPB_CUDA(cudaMemsetAsync(assignment, 0, sizeof(int32_t) * n, s));  // seg: every point in the root
+    DBuf<int> d_q0, d_dim, d_base, d_inf;
+    DBuf<SelState> d_qs;
+    DBuf<unsigned> d_hist, d_fill, d_cid;
+    DBuf<unsigned long long> d_ckey;
+    DBuf<Cand> d_cand;
+    for (;;) {
+        bool any_internal = false;
+        for (const Node& nd : nodes) any_internal |= !nd.node->kids.empty();
+        if (!any_internal) break;
+        const int ns = static_cast<int>(nodes.size());
+        std::vector<int> q0(ns + 1, 0), dim(ns, 0), base(ns, 0);
+        std::vector<SelState> qs;
+        std::vector<Node> next;
+        for (int i = 0; i < ns; ++i) {
+            const Node& nd = nodes[i];
+            q0[i] = static_cast<int>(qs.size());
+            base[i] = static_cast<int>(next.size());
+            if (nd.node->kids.empty()) {
+                next.push_back(nd);
+                continue;
+            }
+            dim[i] = nd.node->dim % dims;
+            const std::vector<int64_t> takes = unit_takes(*nd.node, nd.size);
+            int64_t b = 0;
+            for (size_t c = 0; c < takes.size(); ++c) {
+                if (c > 0) {
+                    // the cut at rank b: cnt = the node's size (the bucket before any digit)
+                    SelState st{0ull, 0u, b, b < nd.size ? nd.size : -1, 0, 0};
+                    qs.push_back(st);
+                }
+                b += takes[c];
+                next.push_back({&nd.node->kids[c], takes[c]});
+            }
+        }
+        q0[ns] = static_cast<int>(qs.size());
+        const int nq = static_cast<int>(qs.size());
+        d_q0.alloc(ns + 1);
+        d_dim.alloc(ns);
+        d_base.alloc(ns);
+        d_qs.alloc(nq);
+        d_hist.alloc(static_cast<size_t>(nq) * 256);
+        d_fill.alloc(nq);
+        d_ckey.alloc(nq);
+        d_cid.alloc(nq);
+        d_inf.alloc(nq);
+        d_cand.alloc(static_cast<size_t>(nq) * kCandMax);
+        SPB_CUDA(cudaMemcpyAsync(d_q0.p, q0.data(), sizeof(int) * (ns + 1), cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemcpyAsync(d_dim.p, dim.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemcpyAsync(d_base.p, base.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemcpyAsync(d_qs.p, qs.data(), sizeof(SelState) * nq, cudaMemcpyHostToDevice, s));
+        SPB_CUDA(cudaMemsetAsync(d_hist.p, 0, sizeof(unsigned) * nq * 256, s));
+        SPB_CUDA(cudaMemsetAsync(d_fill.p, 0, sizeof(unsigned) * nq, s));
+        const size_t hsm = sizeof(unsigned) * nq * 256;
+        // histogram passes until every bucket is small enough for the candidate stage
+        long long worst = 0;
+        for (const SelState& st : qs) worst = std::max(worst, st.cnt);
+        for (int bits = 0; bits < 96 && worst > kCandMax; bits += 8) {
+            if (bits >= 16) {  // from the third digit on, check first (one small read back)
+                SPB_CUDA(cudaMemcpyAsync(qs.data(), d_qs.p, sizeof(SelState) * nq, cudaMemcpyDeviceToHost, s));
+                SPB_CUDA(cudaStreamSynchronize(s));
+                worst = 0;
+                for (const SelState& st : qs) worst = std::max(worst, st.cnt);
+                if (worst <= kCandMax) break;
+            }
+            if (hsm <= 96 * 1024) {
+                static bool attr = false;
+                if (!attr) {
+                    SPB_CUDA(cudaFuncSetAttribute(sel_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  96 * 1024));
+                    attr = true;
+                }
+                sel_hist_kernel<true><<<grid_for(n, 256, 4), 256, hsm, s>>>(n, assignment, coords, d_q0.p, d_dim.p,
+                                                                            d_qs.p, nq, bits, d_hist.p);
+            } else {
+                sel_hist_kernel<false><<<grid_for(n, 256, 8), 256, 0, s>>>(n, assignment, coords, d_q0.p, d_dim.p,
+                                                                           d_qs.p, nq, bits, d_hist.p);
+            }
+            SPB_LAUNCH_CHECK();
+            sel_pick_kernel<<<nq, 256, 0, s>>>(d_qs.p, bits, d_hist.p);
+            SPB_LAUNCH_CHECK();
+        }
+        sel_collect_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, assignment, coords, d_q0.p, d_dim.p, d_qs.p,
+                                                               d_fill.p, d_cand.p);
+        SPB_LAUNCH_CHECK();
+        sel_finish_kernel<<<nq, 256, 0, s>>>(d_qs.p, d_fill.p, d_cand.p, d_ckey.p, d_cid.p, d_inf.p);
+        SPB_LAUNCH_CHECK();
+        sel_label_kernel<<<grid_for(n, 256, 8), 256, 0, s>>>(n, assignment, coords, d_q0.p, d_dim.p, d_base.p, d_ckey.p,
+                                                             d_cid.p, d_inf.p);
+        SPB_LAUNCH_CHECK();
+        nodes.swap(next);
+    }
+    SPB_CUDA(cudaStreamSynchronize(s));
+}
+
 } // namespace
 
 int64_t MjPlanNode::leaf_count() const {
@@ -170,6 +481,10 @@ void mj_partition_dev(int64_t n, int dims, const View& coords, const double* wei
                          ", K=" + std::to_string(num_parts) + ")");
     if (n >= (int64_t(1) << 32)) throw_dimension("mj_partition: n too large");
     const MjPlanNode plan = mj_plan(num_parts, dims);
+    if (unit_weights) {
+        mj_select_unit(n, dims, coords, plan, assignment_dev, s);
+        return;
+    }
 
     DBuf<uint32_t> ids(n);
     DBuf<MjKey> kin(n), kout(n);

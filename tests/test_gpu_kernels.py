@@ -186,6 +186,30 @@ def test_mj_large_identical(ctx, ref):
         assert np.array_equal(a.assignment, b.assignment)
 
 
+@pytest.mark.parametrize("case", ["ties", "clustered", "tiny_nodes", "signed_zero"])
+def test_mj_select_unit_weights(ctx, ref, case):
+    # the unit-weight MJ cuts by radix select (mj.cu): buckets past 4,096 points need more
+    # digit passes (heavy ties reach the id digits), nodes of a few points skip them
+    rng = np.random.default_rng(11)
+    if case == "ties":
+        coords = np.round(rng.uniform(-1, 1, (150000, 3)), 2)  # ~200 distinct values per axis
+        ks = (2, 7, 64, 100)
+    elif case == "clustered":
+        coords = 1e-3 * (1.0 + 1e-9 * rng.standard_normal((120000, 4)))  # one binade, 12+ equal top bits
+        ks = (3, 64, 256)
+    elif case == "tiny_nodes":
+        coords = rng.uniform(-1, 1, (300, 2))
+        ks = (150, 299, 300)
+    else:
+        coords = rng.choice(np.array([0.0, -0.0, 1e-300, -1e-300, 2.0]), size=(20000, 2))
+        ks = (5, 17)
+    for K in ks:
+        a = ctx.mj_partition(coords, None, K)
+        b = ref.mj_partition(coords, None, K)
+        assert np.array_equal(a.assignment, b.assignment), (case, K)
+        assert np.array_equal(a.part_weights, b.part_weights), (case, K)
+
+
 def test_make_partition_exact(ctx, ref):
     g = gen.stencil3d(12, 11, 10, 27)
     rng = np.random.default_rng(8)
