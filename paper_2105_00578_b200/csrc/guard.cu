@@ -35,7 +35,7 @@ Registry& reg() {
 
 // both bands of one buffer; returns the number of bytes that changed
 long long check_bands(void* user, size_t bytes) {
-    static thread_local std::vector<unsigned char> h(2 * kGuard);
+    std::vector<unsigned char> h(2 * kGuard);  // not a static: buffers are also released at exit
     unsigned char* base = static_cast<unsigned char*>(user) - kGuard;
     if (cudaMemcpy(h.data(), base, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
     if (cudaMemcpy(h.data() + kGuard, static_cast<unsigned char*>(user) + bytes, kGuard, cudaMemcpyDeviceToHost) !=
