@@ -81,33 +81,70 @@ __global__ void __launch_bounds__(kThreads, 1) mt_fill_kernel(const FillArgs a) 
         __syncthreads();
     }
 
-    // twist/temper: after each twist W[i] = y_{t+312+i} = draw (kJ + q0 + i)
+    // twist/temper: after each twist W[i] = y_{t+312+i} = draw (kJ + q0 + i). Thread t < 156
+    // keeps words t and t + 156 in registers; word t + 1 comes from the next lane (shuffle), or
+    // across a warp boundary / the wrap-around through a small double-buffered exchange, so a
+    // round costs two barriers instead of four and no shared-memory round trips of the state
+    __shared__ uint64_t xlo[2][8], xhi[2][8], xnew0[2];
+    uint64_t ylo = 0, yhi = 0;
+    if (tid < MM) {
+        ylo = Y[tid];
+        yhi = Y[tid + MM];
+    }
+    __syncthreads();
+    if (tid >= 160) return;  // warps 0-4 hold the 156 state threads (named barrier 1)
+    const bool live = tid < MM;
+    const int lane = tid & 31, warp = tid >> 5;
     const int64_t o_begin = k * kChunk;
     const int64_t o_end = min(a.total, o_begin + kChunk);
-    // (column, row) of this thread's draw, advanced by NN draws per round without a division
-    int64_t oj = (o_begin + tid) / a.n, oi = (o_begin + tid) - oj * a.n;
-    for (int64_t q0 = o_begin; q0 < o_end; q0 += NN) {
-        uint64_t v = 0;
-        if (tid < MM) v = next_word(Y[tid], Y[tid + 1], Y[tid + MM]);
-        __syncthreads();
-        if (tid < MM) Y[tid] = v;
-        __syncthreads();
-        if (tid >= MM && tid < NN) v = next_word(Y[tid], Y[tid + 1 == NN ? 0 : tid + 1], Y[tid - MM]);
-        __syncthreads();
-        if (tid >= MM && tid < NN) Y[tid] = v;
-        __syncthreads();
-        if (tid < NN) {
-            const int64_t o = q0 + tid;
-            if (o < o_end && oi >= a.row0 && oi < a.row0 + a.nloc) {
-                const uint64_t r = temper(Y[tid]);
-                const double u = __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
-                a.out.at(oi - a.row0, static_cast<int>(oj)) = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+    // (column, row) of this thread's two draws, advanced by NN draws per round without a division
+    int64_t oj1 = (o_begin + tid) / a.n, oi1 = (o_begin + tid) - oj1 * a.n;
+    int64_t oj2 = (o_begin + tid + MM) / a.n, oi2 = (o_begin + tid + MM) - oj2 * a.n;
+    auto emit = [&](uint64_t y, int64_t o, int64_t oi, int64_t oj) {
+        if (o < o_end && oi >= a.row0 && oi < a.row0 + a.nloc) {
+            const uint64_t r = temper(y);
+            const double u = __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
+            a.out.at(oi - a.row0, static_cast<int>(oj)) = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+        }
+    };
+    auto step = [&](int64_t& oi, int64_t& oj) {
+        oi += NN;
+        while (oi >= a.n) {
+            oi -= a.n;
+            ++oj;
+        }
+    };
+    const unsigned mask = warp == MM / 32 ? ((1u << (MM % 32)) - 1u) : 0xffffffffu;  // 156 = 4 * 32 + 28
+    int par = 0;
+    for (int64_t q0 = o_begin; q0 < o_end; q0 += NN, par ^= 1) {
+        if (lane == 0) {
+            xlo[par][warp] = ylo;
+            xhi[par][warp] = yhi;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(160) : "memory");  // warps 0-4
+        // old words t + 1 and t + 157
+        uint64_t n_lo = 0, n_hi = 0, new_lo = 0;
+        if (live) {
+            n_lo = __shfl_down_sync(mask, ylo, 1);
+            n_hi = __shfl_down_sync(mask, yhi, 1);
+            if (lane == 31 && tid + 1 < MM) {
+                n_lo = xlo[par][warp + 1];
+                n_hi = xhi[par][warp + 1];
             }
-            oi += NN;
-            while (oi >= a.n) {
-                oi -= a.n;
-                ++oj;
-            }
+            if (tid == MM - 1) n_lo = xhi[par][0];  // word 156 = thread 0's upper word
+            new_lo = next_word(ylo, n_lo, yhi);
+            if (tid == 0) xnew0[par] = new_lo;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(160) : "memory");
+        if (live) {
+            if (tid == MM - 1) n_hi = xnew0[par];  // word 312 wraps to the new word 0
+            const uint64_t new_hi = next_word(yhi, n_hi, new_lo);
+            ylo = new_lo;
+            yhi = new_hi;
+            emit(ylo, q0 + tid, oi1, oj1);
+            emit(yhi, q0 + MM + tid, oi2, oj2);
+            step(oi1, oj1);
+            step(oi2, oj2);
         }
     }
 }
