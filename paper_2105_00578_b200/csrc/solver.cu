@@ -727,6 +727,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
     }
     SPB_LAUNCH_CHECK();
 
+    ctx_->prof.mark(s_, "poly_seed");
     // Arnoldi with two-pass classical Gram-Schmidt (block form of the
     // reference's two-pass MGS, preconditioners.cpp:339-372)
     Mat Hess(k_req + 1, k_req);
@@ -783,6 +784,7 @@ void Solver::build_poly(uint64_t seed, int degree) {
     SPB_CUDA(cudaMemcpyAsync(Hess.a.data(), hess_d.p, sizeof(double) * ldh * k_req, cudaMemcpyDeviceToHost, s_));
     SPB_CUDA(cudaMemcpyAsync(&first_bd, bd.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
     SPB_CUDA(cudaStreamSynchronize(s_));
+    ctx_->prof.mark(s_, "poly_arnoldi");
     if (first_bd < k_req) {
         k_got = first_bd + 1;  // the reference stops at the breakdown step (beta = 0)
         beta = 0.0;
