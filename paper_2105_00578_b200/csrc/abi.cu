@@ -400,6 +400,7 @@ void partition_core(sp_context* ctx, DevGraph& g, const sp_config* cfg, const do
     const auto t_eig = Clock::now();
     Solver solver(ctx, A.op, bdiag, d);
     solver.set_recurrence(ctx->recurrence);
+    ctx->prof.mark(s, "solver_setup");  // operator analysis (ELL, slot patterns, mesh plan), blocks
     const int64_t nloc = g.n_local;
     DBuf<double> Xb, X0b;
     const View X = solver.block(solver.input_block(d, Xb), d);
