@@ -168,7 +168,10 @@ bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_
 // stream, each followed by a stream-ordered flag write; hf is set to wait only.
 // After launching the SpMM the caller must call halo_ce_finish (the main stream
 // may not overwrite X before the copies have read it).
-bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s);
+// segs: another copy plan over the same peers (the two-plane halo of the two-step
+// polynomial kernel, Solver); default the halo plan's own
+bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s,
+                   const std::vector<HaloPlan::CeSeg>* segs = nullptr);
 void halo_ce_finish(Comm& cm, cudaStream_t s);
 void halo_wait_flags(const HaloFuse& hf, cudaStream_t s);  // one warp waits for the peers' flags
 bool sum_p2p(Comm& cm, double* dev, int count, cudaStream_t s);

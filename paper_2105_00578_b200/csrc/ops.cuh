@@ -73,6 +73,9 @@ struct DevOp {
     // halo rows of the input block at mesh_halo_lo / mesh_halo_hi (-1: no such neighbour)
     int mesh_z0 = 0, mesh_nzg = 0, mesh_box27 = 0;
     int64_t mesh_halo_lo = -1, mesh_halo_hi = -1;
+    // two-plane halo of the two-step polynomial kernel: planes z0-2, z0-1 then z1, z1+1
+    // (4 planes) from this row of the input block; -1: not set up (Solver)
+    int64_t mesh_halo2 = -1;
     double bound = 0.0;
     bool is_diagonal = false;
 };
@@ -134,7 +137,8 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
 // mesh: p_{i+1} stays in shared memory (computed on the tile plus a one-point ring), only
 // p_i is read and p_{i+2} written; same arithmetic, hence bit-identical to two steps.
 bool spmm_mesh_poly2_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea);
-int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s);
+int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s,
+                           const HaloFuse* hf = nullptr);
 // hf: the copy-engine halo of a z-slab (nopush): the producer waits for the peers'
 // flags before it loads a halo plane
 int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s,

@@ -128,6 +128,25 @@ Solver::Solver(sp_context* ctx, const DevOp& A, const double* bdiag, int max_col
     } else if (halo_) {
         A_.mesh_nx = A_.mesh_ny = A_.mesh_nz = 0;
     }
+    if (halo_) {
+        // two-step polynomial kernel on z-slabs: it needs two planes from each neighbour,
+        // copied (copy engine) into four planes after the block's rows; every rank must agree
+        const int64_t nxny = static_cast<int64_t>(A_.mesh_nx) * A_.mesh_ny;
+        const bool ok = A_.mesh_nx > 0 && !A_.mesh_box27 && sym_ && A_.mesh_nz >= 2;
+        const bool all_ok = ctx->comm.max_f64(ok ? 0.0 : 1.0, s_) == 0.0;
+        if (all_ok) {
+            const int64_t h2 = (rows_cap_ + 31) / 32 * 32;  // the same row on every rank (rows_cap_ is common)
+            const int r = ctx->comm.rank;
+            const int64_t nloc = A_.n;
+            if (A_.mesh_halo_lo >= 0)  // my bottom two planes -> the lower neighbour's upper halo planes
+                ce2_.push_back({r - 1, 0, h2 + 2 * nxny, 2 * nxny});
+            if (A_.mesh_halo_hi >= 0)  // my top two planes -> the upper neighbour's lower halo planes
+                ce2_.push_back({r + 1, nloc - 2 * nxny, h2, 2 * nxny});
+            A_.mesh_halo2 = h2;
+            rows_cap_ = h2 + 4 * nxny;
+            ld_ = ((rows_cap_ + 63) / 64) * 64;
+        }
+    }
     const int m3 = 3 * max_cols;
     gram_.alloc(static_cast<size_t>(m3) * m3 + 64);
     scratch_.alloc(static_cast<size_t>(device_sm_count()) * 8 * (static_cast<size_t>(m3) * m3 + 64));
@@ -663,7 +682,17 @@ void Solver::spmm_poly2(const View& X, int m, EpiArgs& ea) {
         ev = ctx_->next_event_pair(1);
         SPB_CUDA(cudaEventRecord(ev.first, s_));
     }
-    spmm_mesh_poly2_launch(A_, X, m, ea, s_);
+    HaloFuse hf;
+    bool ce = false;
+    if (halo_) {
+        ce = halo_ce_start(ctx_->comm, X, m, hf, s_, &ce2_);  // two planes per neighbour
+        if (!ce) throw SpError(1, "spmm_poly2: the two-plane halo needs the symmetric heap");
+        ctx_->timers.halo_launches += 1;
+        ctx_->timers.halo_bytes += 2.0 * static_cast<double>(A_.mesh_nx) * A_.mesh_ny * 8.0 * m *
+                                   static_cast<double>(ce2_.size());
+    }
+    spmm_mesh_poly2_launch(A_, X, m, ea, s_, ce ? &hf : nullptr);
+    if (ce) halo_ce_finish(ctx_->comm, s_);
     if (timed) SPB_CUDA(cudaEventRecord(ev.second, s_));
     // p_i read, p_{i+2} written, H read (unless first) and written; no index bytes
     const double nrows = static_cast<double>(A_.n);

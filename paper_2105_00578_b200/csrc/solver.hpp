@@ -119,6 +119,8 @@ private:
     bool sym_ = false;      // SpMM inputs live in the symmetric heap (P2P halo push)
     double *pR_ = nullptr, *pS_ = nullptr, *pW_ = nullptr, *pPA_ = nullptr, *pPB_ = nullptr;
     int64_t rows_cap_ = 1;  // own rows + halo rows
+    // z-slab: copy plan of the two-plane halo of the two-step polynomial kernel
+    std::vector<HaloPlan::CeSeg> ce2_;
     int64_t ld_ = 1;
     PrecKind prec_ = PREC_NONE;
     const double* inv_diag_ = nullptr;

@@ -334,8 +334,8 @@ constexpr int kQPlane = ((kQW * kQW + 15) / 16) * 16;  // 1168 doubles
 constexpr int kQPts = kQW * kQW;                   // 1156 points of q per plane
 
 __global__ void __launch_bounds__(kMeshThreads, 2)
-    spmm_mesh_poly2_kernel(const __grid_constant__ CUtensorMap xmap, const DevOp op, const EpiArgs ea, const int m,
-                           const MeshGeo geo) {
+    spmm_mesh_poly2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lmap,
+                           const DevOp op, const EpiArgs ea, const int m, const MeshGeo geo) {
     extern __shared__ __align__(128) double smem[];
     __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
     const int tid = threadIdx.x;
@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
         tx = static_cast<int>(r % geo.ntx);
         r /= geo.ntx;
         ty = static_cast<int>(r % geo.nty);
-        const int zq = static_cast<int>(r / geo.nty);
+        int zq = static_cast<int>(r / geo.nty);
+        if (geo.zrot) zq = zq + 1 == geo.nzc ? 0 : zq + 1;  // the slab's first chunk (lower halo) last
         z0 = zq * geo.zc;
         z1 = min(geo.nz, z0 + geo.zc);
     };
@@ -365,14 +366,31 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
             int s = 0;
             unsigned eph = 0;
             int64_t g = 0;
+            bool waited = geo.flags == nullptr;
             for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
                 int c, tx, ty, z0, z1;
                 decode(it, c, tx, ty, z0, z1);
                 for (int p = z0 - 2; p <= z1 + 1; ++p, ++g) {
+                    // z-slab: planes -2, -1 and nz, nz + 1 are the neighbours' (4-plane halo map)
+                    const CUtensorMap* mp = &xmap;
+                    int pz = p;
+                    if (p < 0 && geo.hlo >= 0) {
+                        mp = &lmap;
+                        pz = p + 2;
+                    } else if (p >= geo.nz && geo.hhi >= 0) {
+                        mp = &lmap;
+                        pz = 2 + p - geo.nz;
+                    }
+                    if (mp == &lmap && !waited) {
+                        for (int q = 0; q < geo.world; ++q)
+                            if ((geo.recv_mask >> q) & 1u) wait_flag(geo.flags + q, geo.epoch, geo.err);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        waited = true;
+                    }
                     if (g >= geo.nst) mbar_wait(empty + s, eph);
                     double* st = smem + static_cast<size_t>(s) * kXPlane2;
                     mbar_expect_tx(full + s, kXPlane2 * 8u);
-                    tma_load_4d(st, &xmap, tx * kTile - 2, ty * kTile - 2, p, c, full + s);
+                    tma_load_4d(st, mp, tx * kTile - 2, ty * kTile - 2, pz, c, full + s);
                     if (++s == geo.nst) {
                         s = 0;
                         if (g >= geo.nst) eph ^= 1u;
@@ -596,14 +614,24 @@ int launch_mesh(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaSt
     return grid;
 }
 
-int launch_mesh_poly2(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
+int launch_mesh_poly2(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {
     MeshGeo geo{};
     geo.nx = op.mesh_nx;
     geo.ny = op.mesh_ny;
     geo.nz = op.mesh_nz;
-    geo.z0 = 0;
-    geo.nzg = op.mesh_nz;
-    geo.hlo = geo.hhi = -1;
+    geo.z0 = op.mesh_z0;
+    geo.nzg = op.mesh_nzg > 0 ? op.mesh_nzg : op.mesh_nz;
+    const bool slab = op.mesh_halo2 >= 0;
+    geo.hlo = slab && op.mesh_halo_lo >= 0 ? 0 : -1;
+    geo.hhi = slab && op.mesh_halo_hi >= 0 ? 2 : -1;
+    geo.zrot = slab ? 1 : 0;
+    if (hf && hf->on) {
+        geo.flags = hf->my_flags;
+        geo.epoch = hf->epoch;
+        geo.recv_mask = hf->recv_mask;
+        geo.world = hf->world;
+        geo.err = hf->err;
+    }
     geo.ntx = (geo.nx + kTile - 1) / kTile;
     geo.nty = (geo.ny + kTile - 1) / kTile;
     auto kern = spmm_mesh_poly2_kernel;
@@ -626,9 +654,11 @@ int launch_mesh_poly2(const DevOp& op, const View& X, int m, const EpiArgs& ea, 
     geo.nzc = (geo.nz + geo.zc - 1) / geo.zc;
     const int64_t items = per_chunk * geo.nzc;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, ctas)));
-    CUtensorMap xmap;
+    CUtensorMap xmap, lmap;
     make_map(&xmap, X, m, op, kBox2, kBox2);
-    kern<<<grid, kMeshThreads, smem, s>>>(xmap, op, ea, m, geo);
+    if (slab) make_map(&lmap, X, m, op, kBox2, kBox2, 4, op.mesh_halo2);  // [z0-2, z0-1 | z1, z1+1]
+    else lmap = xmap;
+    kern<<<grid, kMeshThreads, smem, s>>>(xmap, lmap, op, ea, m, geo);
     SPB_LAUNCH_CHECK();
     return grid;
 }
@@ -811,13 +841,14 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
 
 bool spmm_mesh_poly2_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
     if (!spmm_mesh_ok(op, X, m, ea) || op.mesh_box27 || ea.mode != EPI_POLY) return false;
-    // one GPU (no slab halo), H column-major
-    return op.mesh_halo_lo < 0 && op.mesh_halo_hi < 0 && op.mesh_z0 == 0 && op.mesh_nzg == op.mesh_nz &&
-           ea.H.rs == 1 && ea.Y.rs == 1;
+    // one GPU, or a z-slab with the two-plane halo set up; H column-major
+    const bool one = op.mesh_halo_lo < 0 && op.mesh_halo_hi < 0 && op.mesh_z0 == 0 && op.mesh_nzg == op.mesh_nz;
+    return (one || op.mesh_halo2 >= 0) && ea.H.rs == 1 && ea.Y.rs == 1;
 }
 
-int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s) {
-    return launch_mesh_poly2(op, X, m, ea, s);
+int spmm_mesh_poly2_launch(const DevOp& op, const View& X, int m, const EpiArgs& ea, cudaStream_t s,
+                           const HaloFuse* hf) {
+    return launch_mesh_poly2(op, X, m, ea, s, hf);
 }
 
 int spmm_mesh_launch(const DevOp& op, const View& X, int m, EpiArgs& ea, cudaStream_t s, const HaloFuse* hf) {

@@ -219,12 +219,14 @@ bool halo_fuse_prepare(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_
 
 using WriteValue64Fn = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
 
-bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s) {
+bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s,
+                   const std::vector<HaloPlan::CeSeg>* segs) {
     static const bool off = [] {
         const char* e = std::getenv("SPB_HALO_CE");
         return e && e[0] == '0';
     }();
-    if (off || !cm.sym.on || !cm.halo.on || !cm.halo.ce_ok || X.rs != 1) return false;
+    if (!segs && off) return false;
+    if (!cm.sym.on || !cm.halo.on || (!segs && !cm.halo.ce_ok) || X.rs != 1) return false;
     if (cm.sym_delta(X.ptr, cm.rank) == INT64_MIN) return false;
     if (!cm.sym.side) {
         void* fn = nullptr;
@@ -246,7 +248,9 @@ bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s)
     hf.total = 0;
     SPB_CUDA(cudaEventRecord(cm.sym.ev_ready, s));
     SPB_CUDA(cudaStreamWaitEvent(cm.sym.side, cm.sym.ev_ready, 0));
-    for (const auto& sg : hp.ce) {
+    int64_t sent = 0;
+    for (const auto& sg : segs ? *segs : hp.ce) {
+        sent += sg.rows;
         // one column: any pitch >= the width (cudaMemcpy2D requires width <= pitch)
         const size_t pitch = sizeof(double) * static_cast<size_t>(m > 1 ? X.cs : sg.rows);
         const double* src = X.ptr + sg.src_row;
@@ -261,7 +265,7 @@ bool halo_ce_start(Comm& cm, const View& X, int m, HaloFuse& hf, cudaStream_t s)
             if (r != 0) throw SpError(8, "cuStreamWriteValue64 failed: " + std::to_string(r));
         }
     SPB_CUDA(cudaEventRecord(cm.sym.ev_done, cm.sym.side));
-    cm.bytes_moved += hp.total_send * m * 8;
+    cm.bytes_moved += sent * m * 8;
     return true;
 }
 
