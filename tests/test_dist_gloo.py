@@ -149,3 +149,46 @@ def test_halo_plan_row_partitioned_spmv_is_exact(world):
     for r in range(world):
         assert got[r] == got[0]
     assert np.frombuffer(got[0]).reshape(-1, 3).tobytes() == Y.tobytes()
+
+
+# ---- the two-plane slab halo of the two-step polynomial kernel (Solver ctor, csrc/solver.cu) ----
+def _slab_ce2(nx, ny, nz, world, rank, rows_cap):
+    """Copy plan of rank `rank`: (peer, src_row, dst_row, rows); the four-plane region starts at
+    h2 = rows_cap rounded up to 32 rows, the same on every rank: [z0-2, z0-1 | z1, z1+1]."""
+    P = nx * ny
+    r0, nl = row_partition(nx * ny * nz, world)[rank]
+    h2 = (rows_cap + 31) // 32 * 32
+    segs = []
+    if r0 > 0:
+        segs.append((rank - 1, 0, h2 + 2 * P, 2 * P))
+    if r0 + nl < nx * ny * nz:
+        segs.append((rank + 1, nl - 2 * P, h2, 2 * P))
+    return segs, h2
+
+
+@pytest.mark.parametrize("nz,world", [(16, 2), (16, 4), (32, 8), (128, 8), (12, 3)])
+def test_slab_two_plane_halo_lands_on_the_right_planes(nz, world):
+    import numpy as np
+    nx, ny = 8, 6
+    P = nx * ny
+    n = nx * ny * nz
+    rows_cap = max(nl for _, nl in row_partition(n, world)) + 2 * P + 32
+    # every rank's block as global row ids (own rows, then the 4-plane region), filled by the plan
+    blocks = []
+    for r in range(world):
+        r0, nl = row_partition(n, world)[r]
+        b = np.full((rows_cap + 31) // 32 * 32 + 4 * P, -1, dtype=np.int64)
+        b[:nl] = np.arange(r0, r0 + nl)
+        blocks.append(b)
+    for r in range(world):
+        segs, h2 = _slab_ce2(nx, ny, nz, world, r, rows_cap)
+        for peer, src, dst, rows in segs:
+            blocks[peer][dst:dst + rows] = blocks[r][src:src + rows]
+    for r in range(world):
+        r0, nl = row_partition(n, world)[r]
+        h2 = (rows_cap + 31) // 32 * 32
+        lo, hi = blocks[r][h2:h2 + 2 * P], blocks[r][h2 + 2 * P:h2 + 4 * P]
+        if r0 > 0:
+            assert np.array_equal(lo, np.arange(r0 - 2 * P, r0))           # planes z0-2, z0-1
+        if r0 + nl < n:
+            assert np.array_equal(hi, np.arange(r0 + nl, r0 + nl + 2 * P))  # planes z1, z1+1
