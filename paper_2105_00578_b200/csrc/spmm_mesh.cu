@@ -840,7 +840,11 @@ bool spmm_mesh_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
 }
 
 bool spmm_mesh_poly2_ok(const DevOp& op, const View& X, int m, const EpiArgs& ea) {
-    if (!spmm_mesh_ok(op, X, m, ea) || op.mesh_box27 || ea.mode != EPI_POLY) return false;
+    static const bool off = [] {  // SPB_POLY2=0: one step per launch (the bit-exactness test's reference)
+        const char* e = std::getenv("SPB_POLY2");
+        return e && e[0] == '0';
+    }();
+    if (off || !spmm_mesh_ok(op, X, m, ea) || op.mesh_box27 || ea.mode != EPI_POLY) return false;
     // one GPU, or a z-slab with the two-plane halo set up; H column-major
     const bool one = op.mesh_halo_lo < 0 && op.mesh_halo_hi < 0 && op.mesh_z0 == 0 && op.mesh_nzg == op.mesh_nz;
     return (one || op.mesh_halo2 >= 0) && ea.H.rs == 1 && ea.Y.rs == 1;

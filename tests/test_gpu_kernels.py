@@ -337,3 +337,22 @@ def test_block_combine_rejects_bad_shapes(ctx):
         ctx.mult(np.ones((4, 3)), np.ones((2, 2)))
     with pytest.raises(DimensionError):
         ctx.mult(np.ones((4, 65)), np.ones((65, 2)))
+
+
+def test_two_step_polynomial_kernel_bit_identical(tmp_path):
+    """spmm_mesh_poly2_kernel (two polynomial steps per pass) against one step per launch
+    (SPB_POLY2=0): the same bytes for every degree (odd / even step counts) and width."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    outs = []
+    for env_val in ("0", "1"):
+        f = tmp_path / f"poly2_{env_val}.bin"
+        env = dict(os.environ, SPB_POLY2=env_val)
+        r = subprocess.run([sys.executable, str(here / "poly2_workload.py"), str(f)], capture_output=True, text=True,
+                           timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(f.read_bytes())
+    assert len(outs[0]) > 0 and outs[0] == outs[1]
