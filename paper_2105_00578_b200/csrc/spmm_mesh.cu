@@ -20,6 +20,12 @@
 // 1.2x (the halo) instead of the ~3x of per-plane gathers (z-1, z, z+1 reads of
 // the same element from three different tiles) — and write Y (and H) with
 // coalesced 256-byte warp stores.
+//
+// Multi-GPU: a rank whose rows are whole z planes (mesh_plan_slab, on the global ids before
+// localization) runs the same kernel on its slab; the neighbours' boundary planes, which the
+// halo plan puts after the own rows, come through a second tensor map once the copy engine's
+// flags arrived. spmm_mesh_poly2_kernel fuses two polynomial steps per pass (5/7-point
+// meshes; on slabs with a two-plane halo), bit-identical to two single steps.
 #include "bulk.cuh"
 #include "ops.cuh"
 #include "spmm_epilogue.cuh"
