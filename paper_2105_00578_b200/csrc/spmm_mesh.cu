@@ -236,6 +236,12 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                     xiv[j] = p1[(row_of(j) + 1) * kHaloW + lane + 2];
                 }
                 const int r0 = 4 * warp;  // box row of tile row r0 - 1
+                // warp-uniform: every output of the warp has all 26 neighbours (no presence tests;
+                // the same operations in the same order as the general path)
+                bool in = zm && zp && xm && xp && live[0];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) in = in && ym[j] && yp[j] && live[j];
+                const bool all_in = __all_sync(0xffffffffu, in);
 #pragma unroll
                 for (int dzi = 0; dzi < 3; ++dzi) {
                     const double* pl = dzi == 0 ? p0 : dzi == 1 ? p1 : p2;
@@ -245,6 +251,20 @@ __global__ void __launch_bounds__(kMeshThreads, 2)
                     for (int r = 0; r < 6; ++r)
 #pragma unroll
                         for (int d = 0; d < 3; ++d) v[r][d] = pl[(r0 + r) * kHaloW + lane + 1 + d];
+                    if (all_in) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+#pragma unroll
+                            for (int dyi = 0; dyi < 3; ++dyi)
+#pragma unroll
+                                for (int dxi = 0; dxi < 3; ++dxi) {
+                                    if (dzi == 1 && dyi == 1 && dxi == 1)
+                                        accv[j] = __dadd_rn(accv[j], __dmul_rn(26.0, xiv[j]));
+                                    else
+                                        accv[j] = __dsub_rn(accv[j], v[j + dyi][dxi]);
+                                }
+                        continue;
+                    }
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
 #pragma unroll
